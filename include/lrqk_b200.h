@@ -1,0 +1,205 @@
+/*
+ * lrqk_b200.h -- C-ABI of the B200-native LRQK decode-time sparse-attention
+ * path (arXiv 2510.23649).  Plain pointers, sizes and a cudaStream_t passed
+ * as void*; no torch or C++ types cross this boundary.
+ *
+ * The reference exposes this path as a Python function API over float64
+ * numpy arrays (pkg/src/lrqk/__init__.py:10-82); it has no FFI of its own.
+ * Each entry point below names the reference function(s) it replaces.  The
+ * Python host mirror (paper_2510_23649_b200/) binds this header with ctypes;
+ * INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - "layer" = one attention layer's decode state for B sequences x Hq query
+ *    heads (GQA: Hkv key/value heads, G = Hq / Hkv query heads per KV head).
+ *    Every (sequence, query head) pair is one reference DecodeSession
+ *    (session.py:62-131); K/V rows are stored once per KV head, while proxy
+ *    rows, B factors, selections and counters are per query head
+ *    (SURVEY.md Appendix A.11).
+ *  - All buffers are caller-allocated (sizes: lrqk_layer_buffer_bytes).  The
+ *    library never allocates device memory.
+ *  - Row vectors are padded to dim_stride / rank_stride elements (multiples
+ *    of 8); padding must be zero.  head_dim / rank are the true sizes used for
+ *    the 1/sqrt(d) scale and for the r x r solves.
+ *  - Return value: 0 on success, else an LRQK_E* code for argument / launch
+ *    errors.  Numerical conditions found on the device (non-finite input,
+ *    SPD solve failed after jitter, index out of range) are OR-ed into the
+ *    device status word `status` and read with lrqk_read_status().
+ */
+#ifndef LRQK_B200_H
+#define LRQK_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LRQK_ABI_VERSION 1
+
+/* storage dtypes */
+#define LRQK_F32 0
+#define LRQK_BF16 1
+
+/* slow-tier placement ("physical cache policy") */
+#define LRQK_SLOW_HBM 0  /* full K/V history in HBM; selected rows gathered by index   */
+#define LRQK_SLOW_HOST 1 /* full K/V history in mapped pinned host memory; GPU holds   */
+                         /* only the selected rows in per-head slots; misses over PCIe */
+
+/* return codes */
+#define LRQK_OK 0
+#define LRQK_EINVAL 1
+#define LRQK_ECUDA 2
+#define LRQK_EUNSUPPORTED 3
+
+/* device status bits (ref: errors.py:4-9, cache.py:183-189) */
+#define LRQK_ST_NONFINITE 1u     /* NonFiniteError                         */
+#define LRQK_ST_SOLVE_FAILED 2u  /* SolveFailedError (jitter retry failed) */
+#define LRQK_ST_INDEX_RANGE 4u   /* IndexError (selection out of range)    */
+#define LRQK_ST_CAPACITY 8u      /* store capacity t_max exhausted          */
+#define LRQK_ST_JITTERED 16u     /* informational: a jittered solve ran     */
+
+typedef struct lrqk_layer {
+    /* ---- shapes / configuration ---- */
+    int32_t batch, n_q_heads, n_kv_heads;
+    int32_t head_dim, dim_stride;
+    int32_t rank, rank_stride;
+    int32_t t_max;                 /* tokens the stores can hold            */
+    int32_t k_budget, lite_budget; /* ref: SessionConfig.k_budget/lite_budget */
+    int32_t s_cap;                 /* k_budget + lite_budget                */
+    int32_t n_slots;               /* s_cap + 1 (slots per head, host policy) */
+    int32_t cand_cap;              /* radix-select candidate capacity / head */
+    int32_t dtype;                 /* LRQK_F32 | LRQK_BF16                  */
+    int32_t policy;                /* LRQK_SLOW_HBM | LRQK_SLOW_HOST        */
+    int32_t max_iter;              /* ref: DecodeConfig.max_iter            */
+    float lambda_1, lambda_2, tol; /* ref: DecodeConfig                     */
+
+    /* ---- persistent state ---- */
+    void *proxy;                   /* A_K store [B,Hq,t_max,rank_stride] dtype  (cache.py proxy store) */
+    float *B_Q, *B_K;              /* [B,Hq,rank_stride,dim_stride] f32           */
+    void *slow_k, *slow_v;         /* [B,Hkv,t_max,dim_stride] dtype (device or mapped host) */
+    void *slot_k, *slot_v;         /* [B,Hq,n_slots,dim_stride] dtype (host policy only)     */
+    int32_t *ctx_len;              /* [B] tokens stored; the new token gets index ctx_len[b]  */
+    int32_t *res_idx;              /* [B,Hq,s_cap] fast-tier index set, ascending            */
+    int32_t *res_slot;             /* [B,Hq,s_cap] slot of each resident row (host policy)   */
+    int32_t *res_cnt;              /* [B,Hq]                                                 */
+    int32_t *spare_slot;           /* [B,Hq] free slot that receives the next appended row   */
+    int32_t *miss_idx, *miss_slot; /* [B,Hq,s_cap] rows to fetch this step (host policy)     */
+    int32_t *miss_cnt;             /* [B,Hq]                                                 */
+    int64_t *c_miss, *c_total;     /* [B,Hq] cumulative counters (cache.py:63-74)            */
+    int32_t *step_miss, *step_total; /* [B,Hq] this step's counts (StepReport)               */
+
+    /* ---- per-step scratch ---- */
+    float *q_hat, *k_hat;          /* [B,Hq,rank_stride]                      */
+    float *eta;                    /* [B,Hq,2] line-search steps (eta_Q, eta_K) */
+    uint32_t *keys;                /* [B,Hq,t_max] order-preserving score keys */
+    uint32_t *hist;                /* [B,Hq,2048] top-11-bit key histogram (zero between steps) */
+    int32_t *sel_meta;             /* [B,Hq,16]                               */
+    int32_t *sure_idx;             /* [B,Hq,k_budget]                         */
+    uint64_t *cand;                /* [B,Hq,cand_cap]                          */
+    float *red_scratch;            /* [B,Hq,red_chunks,rank_stride*(rank_stride+1)] */
+    float *attn_scratch;           /* [B,Hq,attn_splits,dim_stride+2]          */
+    int32_t *counters;             /* [B,Hq,8] arrival counters, zero between steps */
+    uint32_t *status;              /* [1] device status word                  */
+} lrqk_layer_t;
+
+/* Sizes (bytes) of every buffer in lrqk_layer_t for the given configuration,
+ * written to out[] in the order of lrqk_buffer_names().  Returns the count. */
+int lrqk_layer_buffer_bytes(const lrqk_layer_t *cfg, size_t *out, int max_out);
+const char *lrqk_buffer_names(void);
+int lrqk_abi_version(void);
+int lrqk_red_chunks(const lrqk_layer_t *cfg);
+int lrqk_attn_splits(const lrqk_layer_t *cfg);
+
+/* Prompt seeding: proxy[0..l) and slow K/V[0..l) must already hold the
+ * prompt; sets ctx_len=l, fast tier = last lite_budget prompt rows, zeroes
+ * counters/hist, fills slots (host policy).  ref: cache.py:114-124. */
+int lrqk_seed_prompt(const lrqk_layer_t *L, int32_t prompt_len, void *stream);
+
+/* Per-token compression + B line-search update + append of k_hat/k/v.
+ * ref: decode.py:122-184 (decode_compress, update_projections),
+ *      cache.py:199-214 (append_token), session.py:95-98.
+ * q [B,Hq,dim_stride], k/v [B,Hkv,dim_stride] dtype. */
+int lrqk_decode_compress(const lrqk_layer_t *L, const void *q, const void *k, const void *v,
+                         int update_b, void *stream);
+
+/* Proxy scores over tokens 0..t (incl. the just-appended row) as
+ * order-preserving keys + per-head radix histogram.  ref: cache.py:141-146. */
+int lrqk_score(const lrqk_layer_t *L, void *stream);
+
+/* Top-k + lite-window selection fused with hit/miss accounting and slot
+ * replacement.  ref: cache.py:149-196, linalg.py:96-110. */
+int lrqk_select(const lrqk_layer_t *L, void *stream);
+
+/* Host policy: copy this step's missed K/V rows from the pinned host slow
+ * tier into their slots (zero-copy PCIe reads).  ref: cache.py:193-194. */
+int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);
+
+/* Exact softmax attention over the selected rows; out [B,Hq,dim_stride] f32.
+ * ref: attention.py:23-34, session.py:101-102. */
+int lrqk_attention(const lrqk_layer_t *L, const void *q, float *out, void *stream);
+
+/* One whole decode step of one layer (the five calls above in the
+ * reference's order, session.py:90-104); advance!=0 also bumps ctx_len. */
+int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const void *v,
+                     float *out, int advance, void *stream);
+
+/* ctx_len[b] += 1 for every sequence (end of a multi-layer step). */
+int lrqk_advance(int32_t *ctx_len, int32_t batch, void *stream);
+
+/* Standalone proxy scores for the drop-in proxy_scores(q_hat, store):
+ * scores[h, i] = store[h, i, :] . q_hat[h, :], n_heads independent rows.  */
+int lrqk_proxy_scores_f32(const void *store, int32_t dtype, const float *q_hat, float *scores,
+                          int32_t n_heads, int32_t n_rows, int32_t rank_stride, void *stream);
+
+/* Standalone selection for the drop-in select_active(scores, t, k, lite):
+ * scores [n_heads, t+1] f32 -> omega [n_heads, s_cap] ascending, count. */
+int lrqk_select_scores(const float *scores, int32_t n_heads, int32_t t, int32_t k_budget,
+                       int32_t lite_budget, int32_t *omega, int32_t *omega_cnt,
+                       void *workspace, size_t workspace_bytes, void *stream);
+size_t lrqk_select_scores_workspace(int32_t n_heads, int32_t t, int32_t k_budget, int32_t lite_budget);
+
+/* ---- prefill factorisation (ref: prefill.py:197-230) ---- */
+typedef struct lrqk_prefill {
+    int32_t n_heads;        /* independent (Q,K) problems                     */
+    int32_t group;          /* query heads sharing one K (GQA); K index = h / group */
+    int32_t len, head_dim, dim_stride, rank, rank_stride;
+    int32_t dtype;          /* dtype of Q, K                                  */
+    int32_t max_iter;
+    float lambda_q, lambda_k, tol;
+    int32_t want_objective; /* record the Lagrangian after init and each sweep */
+    const void *Q;          /* [n_heads, len, dim_stride]                     */
+    const void *K;          /* [n_heads/group, len, dim_stride]               */
+    float *A_Q, *A_K;       /* [n_heads, len, rank_stride] in: init, out: factors */
+    float *B_Q, *B_K;       /* [n_heads, rank_stride, dim_stride] out         */
+    float *objective;       /* [n_heads, max_iter+1] (NaN where not reached)  */
+    int32_t *sweeps;        /* [n_heads]                                      */
+    int32_t *converged;     /* [n_heads]                                      */
+    float *scratch;         /* lrqk_prefill_scratch_bytes()                   */
+    uint32_t *status;
+} lrqk_prefill_t;
+
+size_t lrqk_prefill_scratch_bytes(const lrqk_prefill_t *P);
+int lrqk_prefill_factorize(const lrqk_prefill_t *P, void *stream);
+
+/* Copy the status word to host memory (synchronises the stream). */
+int lrqk_read_status(const uint32_t *status, uint32_t *host_out, void *stream);
+
+/* Name of the last CUDA error seen by the library (thread-local). */
+const char *lrqk_last_error(void);
+
+/* ABI self-checks for binders: sizeof(lrqk_layer_t), sizeof(lrqk_prefill_t). */
+size_t lrqk_sizeof_layer(void);
+size_t lrqk_sizeof_prefill(void);
+
+/* Pinned, mapped, portable host memory for the LRQK_SLOW_HOST slow tier
+ * (cudaHostAlloc); lrqk_host_device_ptr returns the device alias. */
+void *lrqk_host_alloc(size_t bytes);
+void lrqk_host_free(void *p);
+void *lrqk_host_device_ptr(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LRQK_B200_H */

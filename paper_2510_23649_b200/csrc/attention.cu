@@ -1,0 +1,349 @@
+// K6: gather-fused exact attention over the selected rows
+//     (attention.py:23-34, session.py:101-102)
+// K5b: host-policy miss gather from the pinned host slow tier (cache.py:193-194)
+// plus prompt seeding (cache.py:114-124) and small utilities.
+#include "common.cuh"
+
+namespace lrqk {
+
+constexpr int kAttnThreads = 128;
+
+struct AttnArgs {
+    lrqk_layer_t L;
+    const void *q;
+    float *out;
+};
+
+// One block = one split of kAttnRows selected rows of one (b, h).  Lanes are
+// grouped LPR per row (16-byte packs across d); each group runs an online
+// softmax over its rows; groups, warps and finally splits are merged with the
+// usual (max, sum, acc) rescaling.  The last split block of a head merges the
+// split partials and writes the output.
+template <typename T, int LPR, int PPL>
+__global__ void __launch_bounds__(kAttnThreads)
+attention_kernel(const AttnArgs a) {
+    const lrqk_layer_t &L = a.L;
+    constexpr int N = Pack<T>::N;
+    constexpr int RPW = 32 / LPR;
+    constexpr int U = 4;
+    constexpr int NW = kAttnThreads / 32;
+    __shared__ float s_m[NW * RPW], s_l[NW * RPW];
+    __shared__ int s_flag;
+    extern __shared__ __align__(16) float s_acc[];  // [NW*RPW][d]
+    const int bh = blockIdx.y, split = blockIdx.x;
+    const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
+    const int d = L.dim_stride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int sub = lane / LPR, sl = lane - sub * LPR;
+    const int S = L.res_cnt[bh];
+    const bool host = L.policy == LRQK_SLOW_HOST;
+    const T *kb, *vb;
+    if (host) {
+        kb = reinterpret_cast<const T *>(L.slot_k) + (size_t)bh * L.n_slots * d;
+        vb = reinterpret_cast<const T *>(L.slot_v) + (size_t)bh * L.n_slots * d;
+    } else {
+        const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+        kb = reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
+        vb = reinterpret_cast<const T *>(L.slow_v) + kv_rows * d;
+    }
+    const int *src = (host ? L.res_slot : L.res_idx) + (size_t)bh * L.s_cap;
+    // scale folded into log2 domain: p = 2^(x*c - m), c = log2(e)/sqrt(head_dim)
+    const float c = 1.4426950408889634f * rsqrtf((float)L.head_dim);
+    float qv[PPL][N];
+    {
+        const T *qr = reinterpret_cast<const T *>(a.q) + (size_t)bh * d;
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp) Pack<T>::load(qr + (sl + pp * LPR) * N, qv[pp]);
+    }
+    float m = -INFINITY, l = 0.f;
+    float acc[PPL][N];
+#pragma unroll
+    for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+        for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
+    const int r0 = split * kAttnRows, r1 = min(S, r0 + kAttnRows);
+    const int step = NW * RPW;
+    for (int base = r0 + warp * RPW + sub; base < r1 + sub; base += step * U) {
+        float kx[U][PPL][N], vx[U][PPL][N];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = base + u * step;
+            if (j < r1) {
+                const size_t row = (size_t)src[j] * d;
+#pragma unroll
+                for (int pp = 0; pp < PPL; ++pp) {
+                    Pack<T>::load(kb + row + (sl + pp * LPR) * N, kx[u][pp]);
+                    Pack<T>::load(vb + row + (sl + pp * LPR) * N, vx[u][pp]);
+                }
+            } else {
+#pragma unroll
+                for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+                    for (int e = 0; e < N; ++e) { kx[u][pp][e] = 0.f; vx[u][pp][e] = 0.f; }
+            }
+        }
+        float x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float s = 0.f;
+#pragma unroll
+            for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+                for (int e = 0; e < N; ++e) s = fmaf(kx[u][pp][e], qv[pp][e], s);
+            s = group_sum<LPR>(s);
+            x[u] = (base + u * step < r1) ? s * c : -INFINITY;
+        }
+        float mx = m;
+#pragma unroll
+        for (int u = 0; u < U; ++u) mx = fmaxf(mx, x[u]);
+        if (mx == -INFINITY) continue;
+        const float scale = exp2f(m - mx);
+        l *= scale;
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+            for (int e = 0; e < N; ++e) acc[pp][e] *= scale;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float p = exp2f(x[u] - mx);
+            l += p;
+#pragma unroll
+            for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+                for (int e = 0; e < N; ++e) acc[pp][e] = fmaf(p, vx[u][pp][e], acc[pp][e]);
+        }
+        m = mx;
+    }
+    // per-group partials to shared
+    const int gidx = warp * RPW + sub;
+    if (sl == 0) { s_m[gidx] = m; s_l[gidx] = l; }
+#pragma unroll
+    for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+        for (int e = 0; e < N; ++e) s_acc[gidx * d + (sl + pp * LPR) * N + e] = acc[pp][e];
+    __syncthreads();
+    // merge groups -> split partial
+    float *part = L.attn_scratch + ((size_t)bh * gridDim.x + split) * (size_t)(d + 2);
+    float M = -INFINITY;
+    for (int i = 0; i < NW * RPW; ++i) M = fmaxf(M, s_m[i]);
+    for (int i = tid; i < d; i += blockDim.x) {
+        float sacc = 0.f;
+        for (int gI = 0; gI < NW * RPW; ++gI)
+            if (s_m[gI] != -INFINITY) sacc += s_acc[gI * d + i] * exp2f(s_m[gI] - M);
+        part[2 + i] = sacc;
+    }
+    if (tid == 0) {
+        float sl2 = 0.f;
+        for (int gI = 0; gI < NW * RPW; ++gI)
+            if (s_m[gI] != -INFINITY) sl2 += s_l[gI] * exp2f(s_m[gI] - M);
+        part[0] = M;
+        part[1] = sl2;
+    }
+    if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_ATTN, gridDim.x, &s_flag)) return;
+    // merge the splits of this head
+    const float *parts = L.attn_scratch + (size_t)bh * gridDim.x * (size_t)(d + 2);
+    float MM = -INFINITY;
+    for (int sp = 0; sp < gridDim.x; ++sp) MM = fmaxf(MM, __ldcg(parts + (size_t)sp * (d + 2)));
+    float denom = 0.f;
+    for (int sp = 0; sp < gridDim.x; ++sp) {
+        const float ms = __ldcg(parts + (size_t)sp * (d + 2));
+        if (ms != -INFINITY) denom += __ldcg(parts + (size_t)sp * (d + 2) + 1) * exp2f(ms - MM);
+    }
+    const float inv = 1.f / denom;
+    for (int i = tid; i < d; i += blockDim.x) {
+        float o = 0.f;
+        for (int sp = 0; sp < gridDim.x; ++sp) {
+            const float ms = __ldcg(parts + (size_t)sp * (d + 2));
+            if (ms != -INFINITY) o += __ldcg(parts + (size_t)sp * (d + 2) + 2 + i) * exp2f(ms - MM);
+        }
+        a.out[(size_t)bh * d + i] = o * inv;
+    }
+}
+
+int attn_splits(const lrqk_layer_t &L) { return (L.s_cap + kAttnRows - 1) / kAttnRows; }
+
+template <typename T>
+static int launch_attention_t(const AttnArgs &a, cudaStream_t st) {
+    const lrqk_layer_t &L = a.L;
+    constexpr int N = Pack<T>::N;
+    const int packs = L.dim_stride / N;
+    dim3 grid(attn_splits(L), L.batch * L.n_q_heads);
+    const int lpr = packs < 32 ? packs : 32;
+    const int ppl = packs / lpr;
+    const size_t smem = (size_t)(kAttnThreads / 32) * (32 / lpr) * L.dim_stride * sizeof(float);
+#define LRQK_ATTN(LP, PP)                                                                        \
+    do {                                                                                         \
+        auto fn = attention_kernel<T, LP, PP>;                                                   \
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+        fn<<<grid, kAttnThreads, smem, st>>>(a);                                                 \
+    } while (0)
+    if (ppl == 1) {
+        switch (lpr) {
+            case 1: LRQK_ATTN(1, 1); break;
+            case 2: LRQK_ATTN(2, 1); break;
+            case 4: LRQK_ATTN(4, 1); break;
+            case 8: LRQK_ATTN(8, 1); break;
+            case 16: LRQK_ATTN(16, 1); break;
+            case 32: LRQK_ATTN(32, 1); break;
+            default: return LRQK_EUNSUPPORTED;
+        }
+    } else if (ppl == 2 && lpr == 32) {
+        LRQK_ATTN(32, 2);
+    } else {
+        return LRQK_EUNSUPPORTED;
+    }
+#undef LRQK_ATTN
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+int launch_attention(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st) {
+    AttnArgs a{L, q, out};
+    return L.dtype == LRQK_BF16 ? launch_attention_t<__nv_bfloat16>(a, st) : launch_attention_t<float>(a, st);
+}
+
+// ---------------------------------------------------------------------------
+// K5b: missed rows, pinned host -> slots.  One warp copies 16-byte packs of
+// several rows at once so that enough PCIe reads are in flight.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+gather_misses_kernel(const lrqk_layer_t L) {
+    const int bh = blockIdx.y;
+    const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
+    const int n = L.miss_cnt[bh];
+    const size_t row_bytes = (size_t)L.dim_stride * (L.dtype == LRQK_BF16 ? 2 : 4);
+    const int packs = (int)(row_bytes / 16);
+    const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+    const uint4 *sk = reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(L.slow_k) + kv_rows * row_bytes);
+    const uint4 *sv = reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(L.slow_v) + kv_rows * row_bytes);
+    uint4 *dk = reinterpret_cast<uint4 *>(reinterpret_cast<char *>(L.slot_k) + (size_t)bh * L.n_slots * row_bytes);
+    uint4 *dv = reinterpret_cast<uint4 *>(reinterpret_cast<char *>(L.slot_v) + (size_t)bh * L.n_slots * row_bytes);
+    const int *mi = L.miss_idx + (size_t)bh * L.s_cap;
+    const int *ms = L.miss_slot + (size_t)bh * L.s_cap;
+    const int total = n * packs;
+    constexpr int U = 4;
+    for (int e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < total; e0 += gridDim.x * blockDim.x * U) {
+        uint4 kx[U], vx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < total) {
+                const int j = e / packs, p = e - j * packs;
+                const size_t off = (size_t)mi[j] * packs + p;
+                kx[u] = sk[off];
+                vx[u] = sv[off];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = e0 + u * blockDim.x;
+            if (e < total) {
+                const int j = e / packs, p = e - j * packs;
+                const size_t off = (size_t)ms[j] * packs + p;
+                dk[off] = kx[u];
+                dv[off] = vx[u];
+            }
+        }
+    }
+}
+
+int launch_gather(const lrqk_layer_t &L, cudaStream_t st) {
+    if (L.policy != LRQK_SLOW_HOST) return LRQK_OK;
+    const int row_bytes = L.dim_stride * (L.dtype == LRQK_BF16 ? 2 : 4);
+    const int per_head = L.s_cap * (row_bytes / 16);
+    const int gx = max(1, min(16, (per_head + 1023) / 1024));
+    gather_misses_kernel<<<dim3(gx, L.batch * L.n_q_heads), 256, 0, st>>>(L);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
+// prompt seeding: fast tier = last lite_budget prompt rows (cache.py:114-124)
+// ---------------------------------------------------------------------------
+__global__ void seed_kernel(const lrqk_layer_t L, int prompt_len) {
+    const int bh = blockIdx.x;
+    const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
+    const int lo = max(0, prompt_len - L.lite_budget);
+    const int n = prompt_len - lo;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        L.res_idx[(size_t)bh * L.s_cap + i] = lo + i;
+        if (L.policy == LRQK_SLOW_HOST) L.res_slot[(size_t)bh * L.s_cap + i] = i;
+    }
+    if (threadIdx.x == 0) {
+        L.res_cnt[bh] = n;
+        L.c_miss[bh] = 0;
+        L.c_total[bh] = 0;
+        L.step_miss[bh] = 0;
+        L.step_total[bh] = 0;
+        if (L.policy == LRQK_SLOW_HOST) L.spare_slot[bh] = n;
+        if (h == 0) L.ctx_len[b] = prompt_len;
+    }
+    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) L.hist[(size_t)bh * kHistBins + i] = 0u;
+    for (int i = threadIdx.x; i < kMetaInts; i += blockDim.x) L.sel_meta[(size_t)bh * kMetaInts + i] = 0;
+    for (int i = threadIdx.x; i < kCounterInts; i += blockDim.x) L.counters[(size_t)bh * kCounterInts + i] = 0;
+    if (L.policy == LRQK_SLOW_HOST) {
+        const size_t row_bytes = (size_t)L.dim_stride * (L.dtype == LRQK_BF16 ? 2 : 4);
+        const int packs = (int)(row_bytes / 16);
+        const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+        const uint4 *sk = reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(L.slow_k) + kv_rows * row_bytes);
+        const uint4 *sv = reinterpret_cast<const uint4 *>(reinterpret_cast<const char *>(L.slow_v) + kv_rows * row_bytes);
+        uint4 *dk = reinterpret_cast<uint4 *>(reinterpret_cast<char *>(L.slot_k) + (size_t)bh * L.n_slots * row_bytes);
+        uint4 *dv = reinterpret_cast<uint4 *>(reinterpret_cast<char *>(L.slot_v) + (size_t)bh * L.n_slots * row_bytes);
+        for (int e = threadIdx.x; e < n * packs; e += blockDim.x) {
+            const int j = e / packs, p = e - j * packs;
+            dk[(size_t)j * packs + p] = sk[(size_t)(lo + j) * packs + p];
+            dv[(size_t)j * packs + p] = sv[(size_t)(lo + j) * packs + p];
+        }
+    }
+}
+
+int launch_seed(const lrqk_layer_t &L, int prompt_len, cudaStream_t st) {
+    seed_kernel<<<L.batch * L.n_q_heads, 256, 0, st>>>(L, prompt_len);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+__global__ void advance_kernel(int32_t *ctx_len, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) ctx_len[i] += 1;
+}
+int launch_advance(int32_t *ctx_len, int n, cudaStream_t st) {
+    advance_kernel<<<(n + 255) / 256, 256, 0, st>>>(ctx_len, n);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+// standalone proxy scores (float out) for the drop-in proxy_scores()
+template <typename T>
+__global__ void proxy_scores_kernel(const T *store, const float *qh, float *out, int n_heads, int n_rows, int R) {
+    const int h = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_rows) return;
+    const T *row = store + ((size_t)h * n_rows + i) * R;
+    const float *q = qh + (size_t)h * R;
+    float s = 0.f;
+    for (int p = 0; p < R; ++p) s = fmaf(to_float<T>(row[p]), q[p], s);
+    out[(size_t)h * n_rows + i] = s;
+}
+int launch_proxy_scores(const void *store, int dtype, const float *qh, float *out, int n_heads, int n_rows, int R,
+                        cudaStream_t st) {
+    dim3 grid((n_rows + 255) / 256, n_heads);
+    if (dtype == LRQK_BF16)
+        proxy_scores_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(store), qh,
+                                                                 out, n_heads, n_rows, R);
+    else
+        proxy_scores_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float *>(store), qh, out, n_heads,
+                                                         n_rows, R);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+__global__ void fill_int_kernel(int32_t *p, int n, int v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+int launch_fill_int(int32_t *p, int n, int v, cudaStream_t st) {
+    if (n <= 0) return LRQK_OK;
+    fill_int_kernel<<<(n + 255) / 256, 256, 0, st>>>(p, n, v);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+}  // namespace lrqk

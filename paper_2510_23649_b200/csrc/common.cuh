@@ -1,0 +1,180 @@
+// Shared device helpers for the LRQK sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/lrqk_b200.h"
+
+#define LRQK_DEV __device__ __forceinline__
+
+namespace lrqk {
+
+constexpr int kHistBits = 11;
+constexpr int kHistBins = 1 << kHistBits;  // 2048 bins on the top 11 key bits
+constexpr int kMetaInts = 16;
+constexpr int kCounterInts = 8;
+constexpr int kRedRows = 256;      // resident rows per compression partial
+constexpr int kAttnRows = 128;     // selected rows per attention split
+
+// sel_meta layout, per (b, h)
+enum Meta : int {
+    M_THR_BIN = 0,     // radix bin holding the k-th largest candidate
+    M_N_ABOVE = 1,     // candidates in bins above it
+    M_N_BIN = 2,       // candidates in that bin
+    M_K_EFF = 3,       // min(k_budget, lite_start)
+    M_LITE = 4,        // lite_start
+    M_SURE = 5,        // sure list length (atomic)
+    M_CAND = 6,        // candidate list length (atomic)
+    M_MODE = 7,        // 0 radix path, 1 everything fits, 2 overflow fallback
+};
+
+enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2 };
+
+// ---------------------------------------------------------------------------
+// vector loads: 16 bytes of storage -> float lanes
+// ---------------------------------------------------------------------------
+template <typename T> struct Pack;
+template <> struct Pack<float> {
+    static constexpr int N = 4;
+    LRQK_DEV static void load(const float *p, float (&o)[4]) {
+        float4 v = *reinterpret_cast<const float4 *>(p);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+    LRQK_DEV static void load_nc(const float *p, float (&o)[4]) {
+        float4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+    LRQK_DEV static void store(float *p, const float (&o)[4]) {
+        *reinterpret_cast<float4 *>(p) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+    LRQK_DEV static float cvt(float x) { return x; }
+    LRQK_DEV static float to_f(float x) { return x; }
+};
+template <> struct Pack<__nv_bfloat16> {
+    static constexpr int N = 8;
+    LRQK_DEV static void unpack(uint4 v, float (&o)[8]) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o[2 * i] = __uint_as_float(w[i] << 16);
+            o[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+    LRQK_DEV static void load(const __nv_bfloat16 *p, float (&o)[8]) {
+        unpack(*reinterpret_cast<const uint4 *>(p), o);
+    }
+    LRQK_DEV static void load_nc(const __nv_bfloat16 *p, float (&o)[8]) {
+        uint4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+        unpack(v, o);
+    }
+    LRQK_DEV static void store(__nv_bfloat16 *p, const float (&o)[8]) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t *>(&h);
+        }
+        *reinterpret_cast<uint4 *>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    LRQK_DEV static __nv_bfloat16 cvt(float x) { return __float2bfloat16_rn(x); }
+    LRQK_DEV static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+};
+
+template <typename T> LRQK_DEV T from_float(float x);
+template <> LRQK_DEV float from_float<float>(float x) { return x; }
+template <> LRQK_DEV __nv_bfloat16 from_float<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <typename T> LRQK_DEV float to_float(T x);
+template <> LRQK_DEV float to_float<float>(float x) { return x; }
+template <> LRQK_DEV float to_float<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// ---------------------------------------------------------------------------
+// order-preserving float -> uint32 key; -0.0 is canonicalised to +0.0 so that
+// the two compare equal, as numpy's argsort sees them.
+// ---------------------------------------------------------------------------
+LRQK_DEV uint32_t score_key(float x) {
+    uint32_t u = __float_as_uint(x);
+    if (u == 0x80000000u) u = 0u;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+LRQK_DEV float key_score(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return __uint_as_float(u);
+}
+
+LRQK_DEV float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+LRQK_DEV float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+template <int W> LRQK_DEV float group_sum(float v) {
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+LRQK_DEV void set_status(uint32_t *st, uint32_t bits) {
+    if (st) atomicOr(st, bits);
+}
+
+// Block-wide exclusive scan of one int per thread (blockDim.x <= 1024).
+// `warp_tot` must hold 32 ints of shared memory.  Returns the exclusive
+// prefix; *total receives the block sum.
+LRQK_DEV int block_exclusive_scan(int v, int *warp_tot, int *total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int w = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nw) warp_tot[lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    int base = wid ? warp_tot[wid - 1] : 0;
+    int res = base + x - v;
+    int tot = warp_tot[nw - 1];
+    __syncthreads();
+    if (total) *total = tot;
+    return res;
+}
+
+// "last block to arrive" detection for per-head multi-CTA reductions.
+// All threads of the block must call it; returns true in exactly one block
+// per group once `expected` blocks have arrived, and re-arms the counter.
+LRQK_DEV bool last_arrival(int *counter, int expected, int *s_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        int prev = atomicAdd(counter, 1);
+        int last = (prev == expected - 1);
+        if (last) {
+            atomicExch(counter, 0);
+            __threadfence();
+        }
+        *s_flag = last;
+    }
+    __syncthreads();
+    return *s_flag != 0;
+}
+
+}  // namespace lrqk

@@ -1,0 +1,383 @@
+"""Batched LRQK decode engine: device state per attention layer and the
+multi-layer decode step, driven through the C-ABI (include/lrqk_b200.h).
+
+One `LayerState` holds the reference's per-head session state for B
+sequences x Hq query heads at once (ref: session.py:62-131, cache.py:84-138):
+
+    proxy store  A_K   [B, Hq, t_max, rank_stride]   storage dtype (HBM)
+    B factors    B_Q/K [B, Hq, rank_stride, dim_stride] f32 (HBM)
+    slow tier    K, V  [B, Hkv, t_max, dim_stride]   HBM, or mapped pinned host
+    fast tier    index set Omega_{t-1} per head (+ K/V slots in host policy)
+    counters     c_miss / c_total per head (int64)
+
+`Engine` stacks L layers that share their per-step scratch (keys, histograms,
+candidates, partials), runs a decode step as a fixed kernel sequence per
+layer, and can capture the whole step in a CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NonFiniteError, SolveFailedError
+
+SHARED_SCRATCH = ("q_hat", "k_hat", "eta", "keys", "hist", "sel_meta", "sure_idx", "cand", "red_scratch",
+                  "attn_scratch", "counters", "miss_idx", "miss_slot", "miss_cnt", "status")
+
+
+def pow2_at_least(x: int, lo: int = 8) -> int:
+    v = lo
+    while v < x:
+        v *= 2
+    return v
+
+
+def torch_dtype(name: str):
+    return {"bf16": torch.bfloat16, "f32": torch.float32, "fp32": torch.float32}[name]
+
+
+def lib_dtype(name: str) -> int:
+    return _lib.BF16 if name == "bf16" else _lib.F32
+
+
+@dataclass(frozen=True)
+class LayerShape:
+    batch: int
+    n_q_heads: int
+    n_kv_heads: int
+    head_dim: int
+    rank: int
+    k_budget: int
+    lite_budget: int
+    t_max: int
+    dtype: str = "bf16"      # storage dtype of proxy rows and K/V rows
+    policy: str = "hbm"      # "hbm" | "host"  (slow-tier placement)
+
+    @property
+    def dim_stride(self):
+        return pow2_at_least(self.head_dim)
+
+    @property
+    def rank_stride(self):
+        return pow2_at_least(self.rank)
+
+    @property
+    def group(self):
+        return self.n_q_heads // self.n_kv_heads
+
+
+class HostTier:
+    """Mapped pinned host buffer (cudaHostAlloc) with a numpy view."""
+
+    def __init__(self, nbytes: int):
+        lib = _lib.lib()
+        self.nbytes = nbytes
+        self.ptr = lib.lrqk_host_alloc(nbytes)
+        if not self.ptr:
+            raise MemoryError(f"lrqk_host_alloc({nbytes}) failed: {lib.lrqk_last_error().decode()}")
+        self.dev_ptr = lib.lrqk_host_device_ptr(self.ptr)
+        C.memset(self.ptr, 0, nbytes)
+
+    def as_tensor(self, dtype, shape):
+        buf = (C.c_uint8 * self.nbytes).from_address(self.ptr)
+        arr = np.frombuffer(buf, dtype=np.uint8)
+        t = torch.from_numpy(arr)
+        return t.view(dtype).view(*shape)
+
+    def __del__(self):
+        try:
+            if self.ptr and _lib._lib is not None:
+                _lib._lib.lrqk_host_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+class LayerState:
+    """Device state of one LRQK attention layer (all sequences and heads)."""
+
+    def __init__(self, shape: LayerShape, *, lambda_1=1.0, lambda_2=1.0, max_iter=2, tol=1e-2,
+                 device="cuda", shared: dict | None = None, ctx_len: torch.Tensor | None = None,
+                 cand_cap: int | None = None):
+        lib = _lib.lib()
+        self.shape = shape
+        self.device = torch.device(device)
+        s = _lib.LayerStruct()
+        s.batch, s.n_q_heads, s.n_kv_heads = shape.batch, shape.n_q_heads, shape.n_kv_heads
+        s.head_dim, s.dim_stride = shape.head_dim, shape.dim_stride
+        s.rank, s.rank_stride = shape.rank, shape.rank_stride
+        s.t_max = shape.t_max
+        s.k_budget, s.lite_budget = shape.k_budget, shape.lite_budget
+        s.s_cap = shape.k_budget + shape.lite_budget
+        s.n_slots = s.s_cap + 1
+        s.cand_cap = cand_cap or self._default_cand_cap(shape)
+        s.dtype = lib_dtype(shape.dtype)
+        s.policy = _lib.SLOW_HOST if shape.policy == "host" else _lib.SLOW_HBM
+        s.max_iter, s.lambda_1, s.lambda_2, s.tol = max_iter, lambda_1, lambda_2, tol
+        sizes = (C.c_size_t * 64)()
+        n = lib.lrqk_layer_buffer_bytes(C.byref(s), sizes, 64)
+        if n < 0:
+            raise ValueError(f"unsupported layer configuration {shape}")
+        self.nbytes = dict(zip(_lib.BUFFER_NAMES, [int(sizes[i]) for i in range(n)]))
+        self.buf: dict[str, torch.Tensor] = {}
+        self.host_tiers = {}
+        for name in _lib.BUFFER_NAMES:
+            nb = self.nbytes[name]
+            if shared is not None and name in SHARED_SCRATCH and name in shared:
+                t = shared[name]
+                if t.numel() < nb:
+                    raise ValueError(f"shared buffer {name} too small")
+            elif name == "ctx_len" and ctx_len is not None:
+                t = ctx_len
+            elif name in ("slow_k", "slow_v") and shape.policy == "host":
+                ht = HostTier(max(nb, 16))
+                self.host_tiers[name] = ht
+                setattr(s, name, ht.dev_ptr)
+                continue
+            else:
+                t = torch.zeros(max(nb, 16), dtype=torch.uint8, device=self.device)
+                if shared is not None and name in SHARED_SCRATCH:
+                    shared[name] = t
+            self.buf[name] = t
+            setattr(s, name, t.data_ptr())
+        self.struct = s
+        self.sdt = torch_dtype(shape.dtype)
+
+    @staticmethod
+    def _default_cand_cap(shape: LayerShape) -> int:
+        words = (shape.t_max + 31) // 32
+        s_cap = shape.k_budget + shape.lite_budget
+        budget = 200 * 1024 - (words * 4 + 4 * s_cap * 4 + ((s_cap + 32) // 32 + 4) * 4)
+        return int(max(1024, min(16384, budget // 8)))
+
+    # ---- typed views -------------------------------------------------------
+    def view(self, name):
+        sh = self.shape
+        B, Hq, Hkv, T = sh.batch, sh.n_q_heads, sh.n_kv_heads, sh.t_max
+        ds, rs = sh.dim_stride, sh.rank_stride
+        S = sh.k_budget + sh.lite_budget
+        spec = {
+            "proxy": (self.sdt, (B, Hq, T, rs)),
+            "B_Q": (torch.float32, (B, Hq, rs, ds)),
+            "B_K": (torch.float32, (B, Hq, rs, ds)),
+            "slow_k": (self.sdt, (B, Hkv, T, ds)),
+            "slow_v": (self.sdt, (B, Hkv, T, ds)),
+            "slot_k": (self.sdt, (B, Hq, S + 1, ds)),
+            "slot_v": (self.sdt, (B, Hq, S + 1, ds)),
+            "ctx_len": (torch.int32, (B,)),
+            "res_idx": (torch.int32, (B, Hq, S)),
+            "res_slot": (torch.int32, (B, Hq, S)),
+            "res_cnt": (torch.int32, (B, Hq)),
+            "c_miss": (torch.int64, (B, Hq)),
+            "c_total": (torch.int64, (B, Hq)),
+            "step_miss": (torch.int32, (B, Hq)),
+            "step_total": (torch.int32, (B, Hq)),
+            "q_hat": (torch.float32, (B, Hq, rs)),
+            "k_hat": (torch.float32, (B, Hq, rs)),
+            "eta": (torch.float32, (B, Hq, 2)),
+            "keys": (torch.int32, (B, Hq, T)),
+            "status": (torch.int32, (1,)),
+        }[name]
+        dt, shp = spec
+        if name in self.host_tiers:
+            return self.host_tiers[name].as_tensor(dt, shp)
+        n = int(np.prod(shp)) * torch.empty((), dtype=dt).element_size()
+        return self.buf[name][:n].view(dt).view(*shp)
+
+    @property
+    def ptr(self):
+        return C.byref(self.struct)
+
+    # ---- status -------------------------------------------------------------
+    def raise_status(self, clear=True):
+        st = int(self.view("status").item()) & 0xffffffff
+        if clear:
+            self.view("status").zero_()
+        if st & _lib.ST_NONFINITE:
+            raise NonFiniteError("non-finite values in the decode path")
+        if st & _lib.ST_SOLVE_FAILED:
+            raise SolveFailedError("SPD solve failed even with jitter")
+        if st & _lib.ST_INDEX_RANGE:
+            raise IndexError("selection references a token outside the store")
+        if st & _lib.ST_CAPACITY:
+            raise RuntimeError("LRQK store capacity (t_max) exhausted")
+        return st
+
+    # ---- prompt ----------------------------------------------------------------
+    def load_prompt(self, A_K, B_Q, B_K, K, V):
+        """Install prefill results: A_K [B,Hq,l,r] f32, B_* [B,Hq,r,d] f32,
+        K/V [B,Hkv,l,d]; then seed the fast tier (cache.py:114-124)."""
+        sh = self.shape
+        l = K.shape[2]
+        if l > sh.t_max:
+            raise ValueError(f"prompt of {l} tokens exceeds t_max={sh.t_max}")
+        prox = self.view("proxy")
+        prox[:, :, :l, : A_K.shape[-1]].copy_(A_K.to(self.sdt))
+        self.view("B_Q")[:, :, : B_Q.shape[2], : B_Q.shape[3]].copy_(B_Q)
+        self.view("B_K")[:, :, : B_K.shape[2], : B_K.shape[3]].copy_(B_K)
+        sk, sv = self.view("slow_k"), self.view("slow_v")
+        d = K.shape[-1]
+        if "slow_k" in self.host_tiers:
+            sk[:, :, :l, :d].copy_(K.to(self.sdt).cpu())
+            sv[:, :, :l, :d].copy_(V.to(self.sdt).cpu())
+        else:
+            sk[:, :, :l, :d].copy_(K.to(self.sdt))
+            sv[:, :, :l, :d].copy_(V.to(self.sdt))
+        _lib.check(_lib.lib().lrqk_seed_prompt(self.ptr, l, _lib.stream_ptr()), "lrqk_seed_prompt")
+
+    # ---- decode ----------------------------------------------------------------
+    def step(self, q, k, v, out, advance=True, stream=None):
+        _lib.check(_lib.lib().lrqk_decode_step(self.ptr, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                               out.data_ptr(), int(advance), _lib.stream_ptr(stream)),
+                   "lrqk_decode_step")
+
+
+def pad_last(x: torch.Tensor, width: int) -> torch.Tensor:
+    if x.shape[-1] == width:
+        return x
+    out = x.new_zeros(*x.shape[:-1], width)
+    out[..., : x.shape[-1]] = x
+    return out
+
+
+def randn_init(l: int, r: int, seed: int):
+    """Reference randn init: PCG64 default_rng(seed), A_Q then A_K (prefill.py:124-127)."""
+    g = np.random.default_rng(seed)
+    return g.standard_normal((l, r)), g.standard_normal((l, r))
+
+
+def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter=2, tol=1e-2,
+                             A_Q0=None, A_K0=None, want_objective=False, dtype="bf16", seed=0,
+                             group=None):
+    """Batched prefill factorisation on the GPU (ref: prefill.py:197-230).
+
+    Q [H, l, d], K [H/group, l, d] device tensors.  A_Q0/A_K0: [l, r] or
+    [H, l, r] initial factors (default: the reference randn draw).
+    Returns dict(A_Q, A_K [H,l,r], B_Q, B_K [H,r,d], objective [H, max_iter+1],
+    sweeps [H], converged [H]) as device tensors.
+    """
+    lib = _lib.lib()
+    dev = Q.device
+    H, l, d = Q.shape
+    group = group or (H // K.shape[0])
+    ds, rs = pow2_at_least(d), pow2_at_least(rank)
+    sdt = torch_dtype(dtype)
+    Qp = pad_last(Q.to(sdt), ds).contiguous()
+    Kp = pad_last(K.to(sdt), ds).contiguous()
+    if A_Q0 is None or A_K0 is None:
+        aq, ak = randn_init(l, rank, seed)
+        A_Q0, A_K0 = aq, ak
+    def prep(A):
+        A = torch.as_tensor(A, dtype=torch.float32, device=dev)
+        if A.dim() == 2:
+            A = A.unsqueeze(0).expand(H, l, A.shape[-1])
+        return pad_last(A, rs).contiguous().clone()
+    A_Q, A_K = prep(A_Q0), prep(A_K0)
+    B_Q = torch.zeros(H, rs, ds, dtype=torch.float32, device=dev)
+    B_K = torch.zeros(H, rs, ds, dtype=torch.float32, device=dev)
+    obj = torch.full((H, max_iter + 1), float("nan"), dtype=torch.float32, device=dev)
+    sweeps = torch.zeros(H, dtype=torch.int32, device=dev)
+    conv = torch.zeros(H, dtype=torch.int32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    P = _lib.PrefillStruct()
+    P.n_heads, P.group, P.len, P.head_dim, P.dim_stride = H, group, l, d, ds
+    P.rank, P.rank_stride, P.dtype, P.max_iter = rank, rs, lib_dtype(dtype), max_iter
+    P.lambda_q, P.lambda_k, P.tol = lambda_q, lambda_k, tol
+    P.want_objective = int(want_objective)
+    P.Q, P.K = Qp.data_ptr(), Kp.data_ptr()
+    P.A_Q, P.A_K, P.B_Q, P.B_K = A_Q.data_ptr(), A_K.data_ptr(), B_Q.data_ptr(), B_K.data_ptr()
+    P.objective, P.sweeps, P.converged = obj.data_ptr(), sweeps.data_ptr(), conv.data_ptr()
+    P.status = status.data_ptr()
+    nbytes = lib.lrqk_prefill_scratch_bytes(C.byref(P))
+    scratch = torch.empty(max(16, nbytes // 4 + 16), dtype=torch.float32, device=dev)
+    P.scratch = scratch.data_ptr()
+    _lib.check(lib.lrqk_prefill_factorize(C.byref(P), _lib.stream_ptr()), "lrqk_prefill_factorize")
+    st = int(status.item())
+    if st & _lib.ST_NONFINITE:
+        raise NonFiniteError("prefill factors diverged")
+    if st & _lib.ST_SOLVE_FAILED:
+        raise SolveFailedError("prefill SPD solve failed even with jitter")
+    return dict(A_Q=A_Q[..., :rank], A_K=A_K[..., :rank], B_Q=B_Q[:, :rank, :d], B_K=B_K[:, :rank, :d],
+                A_K_padded=A_K, B_Q_padded=B_Q, B_K_padded=B_K, objective=obj, sweeps=sweeps,
+                converged=conv)
+
+
+class Engine:
+    """L stacked LRQK attention layers decoded together (one token per
+    sequence per step).  Layer inputs are the post-projection q/k/v rows
+    [L, B, H, d]; outputs are the attention rows [L, B, Hq, d] (f32)."""
+
+    def __init__(self, n_layers: int, shape: LayerShape, *, lambda_1=1.0, lambda_2=1.0, max_iter=2,
+                 tol=1e-2, device="cuda"):
+        self.n_layers = n_layers
+        self.shape = shape
+        self.device = torch.device(device)
+        self.ctx_len = torch.zeros(max(16, 4 * shape.batch), dtype=torch.uint8, device=self.device)
+        self.shared: dict = {}
+        self.layers = [LayerState(shape, lambda_1=lambda_1, lambda_2=lambda_2, max_iter=max_iter, tol=tol,
+                                  device=device, shared=self.shared, ctx_len=self.ctx_len)
+                       for _ in range(n_layers)]
+        sh = shape
+        sdt = torch_dtype(sh.dtype)
+        self.q_buf = torch.zeros(n_layers, sh.batch, sh.n_q_heads, sh.dim_stride, dtype=sdt, device=self.device)
+        self.k_buf = torch.zeros(n_layers, sh.batch, sh.n_kv_heads, sh.dim_stride, dtype=sdt, device=self.device)
+        self.v_buf = torch.zeros_like(self.k_buf)
+        self.out_buf = torch.zeros(n_layers, sh.batch, sh.n_q_heads, sh.dim_stride, dtype=torch.float32,
+                                   device=self.device)
+        self.graph = None
+        self.kernels_per_step = None
+
+    @property
+    def ctx(self):
+        return self.ctx_len[: 4 * self.shape.batch].view(torch.int32)
+
+    def launches_per_step(self):
+        """Kernels one decode step launches (compress, score, scan, finalize,
+        [gather], attention per layer, plus the ctx advance)."""
+        per = 5 + (1 if self.shape.policy == "host" else 0)
+        return self.n_layers * per + 1
+
+    def decode_step(self, q=None, k=None, v=None, out=None, stream=None):
+        q = self.q_buf if q is None else q
+        k = self.k_buf if k is None else k
+        v = self.v_buf if v is None else v
+        out = self.out_buf if out is None else out
+        lib = _lib.lib()
+        sp = _lib.stream_ptr(stream)
+        for i, layer in enumerate(self.layers):
+            _lib.check(lib.lrqk_decode_step(layer.ptr, q[i].data_ptr(), k[i].data_ptr(), v[i].data_ptr(),
+                                            out[i].data_ptr(), 0, sp), "lrqk_decode_step")
+        _lib.check(lib.lrqk_advance(self.ctx.data_ptr(), self.shape.batch, sp), "lrqk_advance")
+        return out
+
+    def capture(self, warmup_steps=0):
+        """Capture one decode step (all layers) into a CUDA graph."""
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.decode_step(stream=torch.cuda.current_stream())
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = g
+        return g
+
+    def replay(self):
+        if self.graph is None:
+            self.capture()
+        self.graph.replay()
+        return self.out_buf
+
+    def counters(self):
+        cm = torch.stack([l.view("c_miss") for l in self.layers])
+        ct = torch.stack([l.view("c_total") for l in self.layers])
+        return cm, ct
+
+    def raise_status(self):
+        return self.layers[0].raise_status()
