@@ -1,0 +1,468 @@
+"""Benchmark of the LRQK decode-time sparse-attention path on B200.
+
+Metric (BASELINE.json): decode tokens/s at 128K context with LLaMA-3-8B
+attention shapes (32 layers, 32 q / 8 kv heads, d=128, r=32, top-k 2048,
+16 recent tokens, bf16), plus the proxy-score kernel's HBM GB/s.
+
+A "step" is one decode token for every sequence through all 32 layers:
+per layer compress -> B update -> append -> proxy scores -> top-k select ->
+hit/miss -> gather-fused attention.  Synthetic Q/K/V, the
+prompt factorised on the GPU by the prefill kernels (K1).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun): weak scaling, --batch-per-gpu sequences per rank,
+sharded by batch with no collective inside the step; the per-step
+last-layer outputs are all-gathered over NCCL.  Timing is CUDA events,
+max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: layers, Hq, Hkv, d, ctx, r, k, lite, dtype
+    "c4": dict(layers=32, hq=32, hkv=8, d=128, ctx=131072, r=32, k=2048, lite=16, dtype="bf16",
+               desc="C4: LLaMA-3-8B attention shapes, 32 layers, 128K ctx, r=32, top-k 2048, 16 recent, bf16"),
+    "c2": dict(layers=32, hq=32, hkv=8, d=128, ctx=32768, r=32, k=1024, lite=16, dtype="bf16",
+               desc="C2: LLaMA-3-8B shapes, 32 layers, 32K ctx, r=32, top-k 1024, bf16"),
+    "c3": dict(layers=28, hq=28, hkv=4, d=128, ctx=65536, r=32, k=2048, lite=16, dtype="bf16",
+               desc="C3: Qwen2.5-7B shapes, 28 layers, 64K ctx, r=32, top-k 2048, bf16"),
+    "c1": dict(layers=1, hq=32, hkv=8, d=128, ctx=4096, r=32, k=256, lite=16, dtype="f32",
+               desc="C1: one layer, LLaMA-3-8B head shape, 4K ctx, r=32, top-k 256, fp32"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    p.add_argument("--batch-per-gpu", type=int, default=1)
+    p.add_argument("--ctx", type=int, default=None)
+    p.add_argument("--layers", type=int, default=None)
+    p.add_argument("--rank", type=int, default=None)
+    p.add_argument("--topk", type=int, default=None)
+    p.add_argument("--policy", choices=["hbm", "host"], default="hbm")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-s", type=float, default=15.0)
+    p.add_argument("--profile-steps", type=int, default=0,
+                   help="only run N eager steps after setup (for ncu); prints nothing else")
+    return p.parse_args()
+
+
+def workload(args):
+    w = dict(WORKLOADS[args.workload])
+    if args.ctx:
+        w["ctx"] = args.ctx
+    if args.layers:
+        w["layers"] = args.layers
+    if args.rank:
+        w["r"] = args.rank
+    if args.topk:
+        w["k"] = args.topk
+    return w
+
+
+# --------------------------------------------------------------------------
+# distributed plumbing
+# --------------------------------------------------------------------------
+def dist_init(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------
+# clocks sampled during the timed region
+# --------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.proc = None
+        self.path = os.path.join(tempfile.gettempdir(), f"lrqk_clocks_{os.getpid()}.csv")
+        self.dev = device_index
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# algorithmic bytes
+# --------------------------------------------------------------------------
+def step_bytes(w, B, t, S, e):
+    """Per layer: A_K read, scores write+read, attention K/V gather,
+    resident K/A reads for compression, B factors read+write."""
+    Hq, d, r = w["hq"], w["d"], w["r"]
+    a_k = B * Hq * t * r * e
+    scores = 2 * B * Hq * t * 4
+    attn = B * Hq * S * 2 * d * e
+    resid = B * Hq * S * (d + r) * e
+    bfac = B * Hq * 2 * r * d * 4 * 2
+    return dict(a_k=a_k, scores=scores, attn=attn, resid=resid, bfac=bfac,
+                total=a_k + scores + attn + resid + bfac)
+
+
+# --------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------
+def run_ours(args, world, rank, local):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_23649_b200 import _lib
+    from paper_2510_23649_b200.engine import Engine, LayerShape, prefill_factorize_device
+
+    w = workload(args)
+    dev = torch.device("cuda", local)
+    B = args.batch_per_gpu
+    L, Hq, Hkv, d, ctx, r, k, lite = w["layers"], w["hq"], w["hkv"], w["d"], w["ctx"], w["r"], w["k"], w["lite"]
+    extra_steps = args.warmup + args.steps + max(args.profile_steps, 0) + 64
+    t_max = ctx + 2 * extra_steps
+    shape = LayerShape(batch=B, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, rank=r, k_budget=k, lite_budget=lite,
+                       t_max=t_max, dtype=w["dtype"], policy=args.policy)
+    eng = Engine(L, shape, device=dev)
+    sdt = torch.bfloat16 if w["dtype"] == "bf16" else torch.float32
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    # ---- prompt: synthetic Q/K/V, factorised by the GPU prefill kernels ----
+    torch.cuda.synchronize()
+    t0 = time.time()
+    prefill_ms = 0.0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for li, layer in enumerate(eng.layers):
+        Qp = torch.randn(B * Hq, ctx, d, device=dev, generator=gen).to(sdt)
+        Kp = torch.randn(B * Hkv, ctx, d, device=dev, generator=gen).to(sdt)
+        Vp = torch.randn(B * Hkv, ctx, d, device=dev, generator=gen).to(sdt)
+        ev0.record()
+        res = prefill_factorize_device(Qp, Kp, r, dtype=w["dtype"], group=Hq // Hkv)
+        ev1.record()
+        torch.cuda.synchronize()
+        prefill_ms += ev0.elapsed_time(ev1)
+        layer.load_prompt(res["A_K"].reshape(B, Hq, ctx, r), res["B_Q"].reshape(B, Hq, r, d),
+                          res["B_K"].reshape(B, Hq, r, d), Kp.view(B, Hkv, ctx, d), Vp.view(B, Hkv, ctx, d))
+        del Qp, Kp, Vp, res
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+
+    # ---- per-step inputs: a pool of synthetic decode rows ------------------
+    pool = 8
+    q_pool = torch.randn(pool, L, B, Hq, d, device=dev, generator=gen).to(sdt)
+    k_pool = torch.randn(pool, L, B, Hkv, d, device=dev, generator=gen).to(sdt)
+    v_pool = torch.randn(pool, L, B, Hkv, d, device=dev, generator=gen).to(sdt)
+
+    def load_inputs(i):
+        eng.q_buf[..., :d].copy_(q_pool[i % pool], non_blocking=True)
+        eng.k_buf[..., :d].copy_(k_pool[i % pool], non_blocking=True)
+        eng.v_buf[..., :d].copy_(v_pool[i % pool], non_blocking=True)
+
+    if args.profile_steps > 0:  # eager steps for ncu
+        for i in range(args.profile_steps):
+            load_inputs(i)
+            eng.decode_step()
+        torch.cuda.synchronize()
+        eng.raise_status()
+        return None
+
+    # ---- warm up, capture -----------------------------------------------------
+    for i in range(2):
+        load_inputs(i)
+        eng.decode_step()
+    torch.cuda.synchronize()
+    eng.raise_status()
+    eng.capture()
+    gather_buf = None
+    if world > 1:
+        gather_buf = torch.empty(world, B, Hq, shape.dim_stride, device=dev)
+
+    def one_step(i):
+        load_inputs(i)
+        eng.replay()
+        if world > 1:  # final per-head output gather over NVLink (NCCL)
+            dist.all_gather_into_tensor(gather_buf, eng.out_buf[-1])
+
+    step_i = 2
+    for _ in range(args.warmup):
+        one_step(step_i)
+        step_i += 1
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start.record()
+    for _ in range(args.steps):
+        one_step(step_i)
+        step_i += 1
+    stop.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clock_info = clocks.stop()
+    ms = start.elapsed_time(stop)
+    eng.raise_status()
+    t_now = int(eng.ctx[0].item())
+
+    # ---- end to end: host inputs in, host outputs out, per step ------------
+    q_host = q_pool[:4].cpu().pin_memory()
+    k_host = k_pool[:4].cpu().pin_memory()
+    v_host = v_pool[:4].cpu().pin_memory()
+    out_host = torch.empty(L, B, Hq, shape.dim_stride, dtype=torch.float32).pin_memory()
+    h2d = (q_host[0].numel() + k_host[0].numel() + v_host[0].numel()) * q_host.element_size()
+    d2h = out_host.numel() * 4
+    e2e_steps = max(5, args.steps // 2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(e2e_steps):
+        j = i % 4
+        eng.q_buf[..., :d].copy_(q_host[j], non_blocking=True)
+        eng.k_buf[..., :d].copy_(k_host[j], non_blocking=True)
+        eng.v_buf[..., :d].copy_(v_host[j], non_blocking=True)
+        eng.replay()
+        if world > 1:
+            dist.all_gather_into_tensor(gather_buf, eng.out_buf[-1])
+        out_host.copy_(eng.out_buf, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    step_i += e2e_steps
+
+    # ---- dominant kernel (proxy score) timed on its stream ------------------
+    lib = _lib.lib()
+    stream = torch.cuda.current_stream()
+    sp = _lib.stream_ptr(stream)
+    n_prof = 3
+    evs = []
+    for i in range(n_prof):
+        load_inputs(step_i)
+        step_i += 1
+        for li, layer in enumerate(eng.layers):
+            q, kk, vv, out = eng.q_buf[li], eng.k_buf[li], eng.v_buf[li], eng.out_buf[li]
+            _lib.check(lib.lrqk_decode_compress(layer.ptr, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), 1, sp), "compress")
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _lib.check(lib.lrqk_score(layer.ptr, sp), "score")
+            b_.record(stream)
+            evs.append((a, b_))
+            _lib.check(lib.lrqk_select(layer.ptr, sp), "select")
+            _lib.check(lib.lrqk_gather_misses(layer.ptr, sp), "gather")
+            _lib.check(lib.lrqk_attention(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "attention")
+        _lib.check(lib.lrqk_advance(eng.ctx.data_ptr(), B, sp), "advance")
+    torch.cuda.synchronize()
+    eng.raise_status()
+    score_ms = float(np.mean([a.elapsed_time(b_) for a, b_ in evs]))
+
+    # ---- aggregate over ranks ------------------------------------------------
+    vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(vals[0]), float(vals[1])
+    total_seq = B * world
+    ms_per_step = ms / args.steps
+    tok_s = total_seq * args.steps / (ms / 1e3)
+    e2e_tok_s = total_seq * e2e_steps / (e2e_ms / 1e3)
+
+    S = k + lite
+    e = 2 if w["dtype"] == "bf16" else 4
+    t_mid = t_now  # context during the profile steps
+    byt = step_bytes(w, B, t_mid, S, e)
+    score_bytes = B * Hq * (t_mid + 1) * (r * e + 4)  # A_K read + key write per launch
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    score_gbs = score_bytes / (score_ms / 1e3) / 1e9
+    step_gbs = byt["total"] * L / (ms_per_step / 1e3) / 1e9
+    return dict(
+        metric="decode tokens/s at 128K ctx (LLaMA-3-8B shape); proxy-score HBM GB/s",
+        value=round(tok_s, 3), unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+        ms_per_step=round(ms_per_step, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
+        dtype=w["dtype"], data="synthetic (random N(0,1) Q/K/V per layer; prompt factorised on GPU)",
+        config=dict(workload=w["desc"], ctx=w["ctx"], layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
+                    rank=r, top_k=k, lite=lite, batch_per_gpu=B, global_batch=total_seq,
+                    slow_tier=args.policy,
+                    parallelism=f"batch-sharded over {world} GPU(s), no collective inside the step; "
+                                f"NCCL all-gather of last-layer outputs per step" if world > 1 else "1 GPU",
+                    l2="no flush: each step streams %.1f GB (> 126 MB L2)" % (byt["total"] * L / 1e9)),
+        roofline=dict(bound="hbm", kernel="score_kernel (proxy scores + radix histogram)",
+                      achieved=round(score_gbs, 1), peak=hbm_peak, unit="GB/s",
+                      frac=round(score_gbs / hbm_peak, 4), traffic=None,
+                      algorithmic_bytes_per_launch=score_bytes, avg_launch_ms=round(score_ms, 5),
+                      step_frac_of_hbm=round(step_gbs / hbm_peak, 4), step_algorithmic_GBps=round(step_gbs, 1),
+                      peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"),
+        e2e=dict(value=round(e2e_tok_s, 3), unit="tokens/s", h2d_bytes_per_step=int(h2d),
+                 d2h_bytes_per_step=int(d2h), steps=e2e_steps,
+                 path="Engine public API: pinned host q/k/v -> H2D -> graph replay -> D2H outputs"),
+        gpu_launches=eng.launches_per_step() * args.steps,
+        clocks=clock_info,
+        prefill=dict(ms_total_gpu=round(prefill_ms, 2), heads=L * B * Hq, ctx=ctx, setup_s=round(setup_s, 2)),
+        bytes_per_token_layer=byt,
+    )
+
+
+# --------------------------------------------------------------------------
+# CPU arm: the oracle port of the reference (numpy fp64), bounded sample
+# --------------------------------------------------------------------------
+def _cpu_worker(argtuple):
+    ctx, d, r, k, lite, n_steps, seed = argtuple
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import lrqk_oracle as O
+
+    rng = np.random.default_rng(seed)
+    K = rng.standard_normal((ctx, d))
+    V = rng.standard_normal((ctx, d))
+    P = rng.standard_normal((ctx, r))
+    BQ = rng.standard_normal((r, d)) / math.sqrt(d)
+    BK = rng.standard_normal((r, d)) / math.sqrt(d)
+    st = O.seed_head(K, V, O.Factors(None, P, BQ, BK), k, lite)
+    # first step fills the resident set to its steady-state size
+    O.head_step(st, rng.standard_normal(d), rng.standard_normal(d), rng.standard_normal(d))
+    t0 = time.perf_counter()
+    for _ in range(n_steps):
+        O.head_step(st, rng.standard_normal(d), rng.standard_normal(d), rng.standard_normal(d))
+    return (time.perf_counter() - t0) / n_steps
+
+
+def cpu_baseline(w, total_seq, budget_s=15.0, steps_override=None):
+    """Time the oracle port on P = cores processes, one head session each, and
+    extrapolate to the whole job (layers x heads x sequences; heads are
+    independent)."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    ctx = w["ctx"]
+    # probe one step to size the sample
+    probe = _cpu_worker((ctx, w["d"], w["r"], w["k"], w["lite"], 1, 0))
+    n_steps = steps_override or max(2, min(20, int(budget_s / max(probe, 1e-3) / 2)))
+    with mp.get_context("spawn").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        per = pool.map(_cpu_worker, [(ctx, w["d"], w["r"], w["k"], w["lite"], n_steps, 1 + i) for i in range(cores)])
+        wall = time.perf_counter() - t0
+    head_steps_per_s = cores / float(np.mean(per))
+    sessions = w["layers"] * w["hq"] * total_seq
+    tok_s = head_steps_per_s / sessions * total_seq
+    return dict(value=round(tok_s, 5), unit="tokens/s", cores=cores, kind="port",
+                sample=f"{cores} processes x 1 head session ({ctx} ctx, k={w['k']}, r={w['r']}, fp64 numpy oracle) "
+                       f"x {n_steps} decode steps; {np.mean(per)*1e3:.1f} ms/head-step; extrapolated to "
+                       f"{sessions} head sessions per token (layers x q-heads x sequences)",
+                ms_per_head_step=round(float(np.mean(per)) * 1e3, 3), wall_s=round(wall, 1))
+
+
+def run_reference(args, world, rank):
+    w = workload(args)
+    total_seq = args.batch_per_gpu * world
+    if rank != 0:
+        return None
+    # each "step" of this arm is one bounded parallel sample round
+    t0 = time.perf_counter()
+    cb = cpu_baseline(w, total_seq, budget_s=args.cpu_sample_s, steps_override=max(2, args.steps // 10))
+    wall = time.perf_counter() - t0
+    ms_per_step = 1e3 * total_seq / cb["value"] if cb["value"] else None
+    return dict(metric="decode tokens/s at 128K ctx (LLaMA-3-8B shape); proxy-score HBM GB/s",
+                value=cb["value"], unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=round(ms_per_step, 3) if ms_per_step else None, higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=w["desc"], ctx=w["ctx"], layers=w["layers"], global_batch=total_seq,
+                            rank=w["r"], top_k=w["k"], lite=w["lite"]),
+                impl="reference", cpu_baseline=dict(cb, value=cb["value"]),
+                e2e=dict(value=cb["value"], unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                wall_s=round(wall, 1))
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_init(args)
+    if args.impl == "reference":
+        out = run_reference(args, world, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    res = run_ours(args, world, rank, local)
+    if res is None:
+        return
+    if rank == 0:
+        if not args.no_cpu_baseline and world == 1:
+            res["cpu_baseline"] = cpu_baseline(workload(args), res["config"]["global_batch"], args.cpu_sample_s)
+        else:
+            res["cpu_baseline"] = None
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

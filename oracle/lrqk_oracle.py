@@ -382,6 +382,30 @@ def attend(q, K, V):
 # one head's decode session  (ref: session.py:62-117, cache.py:84-138)
 # --------------------------------------------------------------------------
 
+class _Rows:
+    """Append-only row store with amortised doubling, as the reference's
+    _RowStore (ref: cache.py:21-51), so the oracle's per-step cost matches
+    the reference's rather than an O(t) copy per append."""
+
+    def __init__(self, rows, extra=16):
+        rows = np.asarray(rows, dtype=np.float64)
+        self.buf = np.empty((max(16, rows.shape[0] + extra), rows.shape[1]))
+        self.buf[: rows.shape[0]] = rows
+        self.n = rows.shape[0]
+
+    def append(self, row):
+        if self.n == self.buf.shape[0]:
+            grown = np.empty((2 * self.buf.shape[0], self.buf.shape[1]))
+            grown[: self.n] = self.buf[: self.n]
+            self.buf = grown
+        self.buf[self.n] = np.ravel(row)
+        self.n += 1
+
+    @property
+    def rows(self):
+        return self.buf[: self.n]
+
+
 @dataclass
 class HeadState:
     """All state one (sequence, q-head) session carries between steps.
@@ -404,6 +428,15 @@ class HeadState:
     c_miss: int = 0
     c_total: int = 0
     per_step: list = field(default_factory=list)
+
+    def __post_init__(self):
+        self._K, self._V, self._P = _Rows(self.K), _Rows(self.V), _Rows(self.proxy)
+
+    def append(self, k, v, k_hat):
+        self._K.append(k)
+        self._V.append(v)
+        self._P.append(k_hat)
+        self.K, self.V, self.proxy = self._K.rows, self._V.rows, self._P.rows
 
 
 def seed_head(K, V, factors, k_budget, lite_budget, **decode_kw):
@@ -444,9 +477,7 @@ def head_step(st: HeadState, q, k, v):
                           st.lam1, st.lam2, st.max_iter, st.tol)
     st.B_Q, st.B_K, _, _ = refresh_projections(q, k, comp, st.B_Q, st.B_K)
     t = st.K.shape[0]
-    st.K = np.vstack([st.K, k])
-    st.V = np.vstack([st.V, v])
-    st.proxy = np.vstack([st.proxy, comp.k_hat])
+    st.append(k, v, comp.k_hat)
     before = np.union1d(res, [t])
     scores = proxy_scores(comp.q_hat, st.proxy)
     _, _, omega = select(scores, t, st.k_budget, st.lite_budget)

@@ -18,6 +18,7 @@ layer, and can capture the whole step in a CUDA graph.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 from dataclasses import dataclass
 
@@ -246,10 +247,16 @@ def pad_last(x: torch.Tensor, width: int) -> torch.Tensor:
     return out
 
 
+@functools.lru_cache(maxsize=4)
 def randn_init(l: int, r: int, seed: int):
-    """Reference randn init: PCG64 default_rng(seed), A_Q then A_K (prefill.py:124-127)."""
+    """Reference randn init: PCG64 default_rng(seed), A_Q then A_K
+    (prefill.py:124-127).  The draw depends only on (l, r, seed), so one
+    draw serves every head and layer."""
     g = np.random.default_rng(seed)
-    return g.standard_normal((l, r)), g.standard_normal((l, r))
+    aq, ak = g.standard_normal((l, r)), g.standard_normal((l, r))
+    aq.flags.writeable = False
+    ak.flags.writeable = False
+    return aq, ak
 
 
 def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter=2, tol=1e-2,
