@@ -59,6 +59,7 @@ extern "C" {
 #define LRQK_ST_INDEX_RANGE 4u   /* IndexError (selection out of range)    */
 #define LRQK_ST_CAPACITY 8u      /* store capacity t_max exhausted          */
 #define LRQK_ST_JITTERED 16u     /* informational: a jittered solve ran     */
+#define LRQK_ST_FALLBACK 32u     /* informational: direct-solve fallback ran */
 
 typedef struct lrqk_layer {
     /* ---- shapes / configuration ---- */
@@ -94,7 +95,7 @@ typedef struct lrqk_layer {
     float *q_hat, *k_hat;          /* [B,Hq,rank_stride]                      */
     float *eta;                    /* [B,Hq,2] line-search steps (eta_Q, eta_K) */
     uint32_t *keys;                /* [B,Hq,t_max] order-preserving score keys */
-    uint32_t *hist;                /* [B,Hq,2048] top-11-bit key histogram (zero between steps) */
+    uint32_t *hist;                /* [B,Hq,2,2048] coarse + fine radix histograms (zero between steps) */
     int32_t *sel_meta;             /* [B,Hq,16]                               */
     int32_t *sure_idx;             /* [B,Hq,k_budget]                         */
     uint64_t *cand;                /* [B,Hq,cand_cap]                          */

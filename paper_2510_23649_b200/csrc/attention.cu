@@ -142,22 +142,37 @@ attention_kernel(const AttnArgs a) {
     }
     if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_ATTN, gridDim.x, &s_flag)) return;
     // merge the splits of this head
-    const float *parts = L.attn_scratch + (size_t)bh * gridDim.x * (size_t)(d + 2);
-    float MM = -INFINITY;
-    for (int sp = 0; sp < gridDim.x; ++sp) MM = fmaxf(MM, __ldcg(parts + (size_t)sp * (d + 2)));
-    float denom = 0.f;
-    for (int sp = 0; sp < gridDim.x; ++sp) {
-        const float ms = __ldcg(parts + (size_t)sp * (d + 2));
-        if (ms != -INFINITY) denom += __ldcg(parts + (size_t)sp * (d + 2) + 1) * exp2f(ms - MM);
+    __shared__ float s_ms[64], s_w[64];
+    __shared__ float s_den;
+    const int nsp = gridDim.x;
+    const float *parts = L.attn_scratch + (size_t)bh * nsp * (size_t)(d + 2);
+    for (int sp = tid; sp < nsp; sp += blockDim.x) {
+        s_ms[sp] = __ldcg(parts + (size_t)sp * (d + 2));
+        s_w[sp] = __ldcg(parts + (size_t)sp * (d + 2) + 1);
     }
-    const float inv = 1.f / denom;
-    for (int i = tid; i < d; i += blockDim.x) {
-        float o = 0.f;
-        for (int sp = 0; sp < gridDim.x; ++sp) {
-            const float ms = __ldcg(parts + (size_t)sp * (d + 2));
-            if (ms != -INFINITY) o += __ldcg(parts + (size_t)sp * (d + 2) + 2 + i) * exp2f(ms - MM);
+    __syncthreads();
+    if (tid == 0) {
+        float MM = -INFINITY;
+        for (int sp = 0; sp < nsp; ++sp) MM = fmaxf(MM, s_ms[sp]);
+        float den = 0.f;
+        for (int sp = 0; sp < nsp; ++sp) {
+            const float w = s_ms[sp] != -INFINITY ? exp2f(s_ms[sp] - MM) : 0.f;
+            den = fmaf(s_w[sp], w, den);
+            s_ms[sp] = w;  // now the split weight
         }
-        a.out[(size_t)bh * d + i] = o * inv;
+        s_den = den;
+    }
+    __syncthreads();
+    const float inv = 1.f / s_den;
+    for (int i = tid; i < d; i += blockDim.x) {
+        float o0 = 0.f, o1 = 0.f;
+        int sp = 0;
+        for (; sp + 1 < nsp; sp += 2) {
+            o0 = fmaf(__ldcg(parts + (size_t)sp * (d + 2) + 2 + i), s_ms[sp], o0);
+            o1 = fmaf(__ldcg(parts + (size_t)(sp + 1) * (d + 2) + 2 + i), s_ms[sp + 1], o1);
+        }
+        if (sp < nsp) o0 = fmaf(__ldcg(parts + (size_t)sp * (d + 2) + 2 + i), s_ms[sp], o0);
+        a.out[(size_t)bh * d + i] = (o0 + o1) * inv;
     }
 }
 
@@ -279,7 +294,7 @@ __global__ void seed_kernel(const lrqk_layer_t L, int prompt_len) {
         if (L.policy == LRQK_SLOW_HOST) L.spare_slot[bh] = n;
         if (h == 0) L.ctx_len[b] = prompt_len;
     }
-    for (int i = threadIdx.x; i < kHistBins; i += blockDim.x) L.hist[(size_t)bh * kHistBins + i] = 0u;
+    for (int i = threadIdx.x; i < 2 * kHistBins; i += blockDim.x) L.hist[(size_t)bh * 2 * kHistBins + i] = 0u;
     for (int i = threadIdx.x; i < kMetaInts; i += blockDim.x) L.sel_meta[(size_t)bh * kMetaInts + i] = 0;
     for (int i = threadIdx.x; i < kCounterInts; i += blockDim.x) L.counters[(size_t)bh * kCounterInts + i] = 0;
     if (L.policy == LRQK_SLOW_HOST) {

@@ -7,6 +7,7 @@
 namespace lrqk {
 int launch_compress(const lrqk_layer_t &L, const void *q, const void *k, const void *v, int update_b, cudaStream_t st);
 int compress_chunks(const lrqk_layer_t &L);
+size_t compress_scratch_floats_per_head(const lrqk_layer_t &L);
 int launch_score(const lrqk_layer_t &L, const float *ext_scores, cudaStream_t st);
 int launch_select(const lrqk_layer_t &L, cudaStream_t st);
 int launch_gather(const lrqk_layer_t &L, cudaStream_t st);
@@ -42,7 +43,8 @@ static int validate(const lrqk_layer_t *L) {
     if (!pow2(L->dim_stride) || L->dim_stride < 8 || L->dim_stride > 256) return LRQK_EUNSUPPORTED;
     if (!pow2(L->rank_stride) || L->rank_stride < 8 || L->rank_stride > 64) return LRQK_EUNSUPPORTED;
     if (L->k_budget < 1 || L->lite_budget < 1 || L->s_cap != L->k_budget + L->lite_budget) return LRQK_EINVAL;
-    if (L->t_max < 1 || L->t_max >= (1 << 21)) return LRQK_EUNSUPPORTED;
+    if (L->t_max < 32 || L->t_max % 32 || L->t_max >= (1 << 21)) return LRQK_EUNSUPPORTED;
+    if (L->s_cap > 8192) return LRQK_EUNSUPPORTED;
     if (L->dtype != LRQK_F32 && L->dtype != LRQK_BF16) return LRQK_EINVAL;
     if (L->policy == LRQK_SLOW_HOST && L->n_slots != L->s_cap + 1) return LRQK_EINVAL;
     if (L->cand_cap < 1) return LRQK_EINVAL;
@@ -113,11 +115,11 @@ int lrqk_layer_buffer_bytes(const lrqk_layer_t *L, size_t *out, int max_out) {
         BH * R * 4,                     // k_hat
         BH * 2 * 4,                     // eta
         BH * T * 4,                     // keys
-        BH * kHistBins * 4,             // hist
+        BH * 2 * kHistBins * 4,         // hist (two radix levels)
         BH * kMetaInts * 4,             // sel_meta
         BH * (size_t)L->k_budget * 4,   // sure_idx
         BH * (size_t)L->cand_cap * 8,   // cand
-        BH * (size_t)compress_chunks(*L) * (R * R + R) * 4,  // red_scratch
+        BH * compress_scratch_floats_per_head(*L) * 4,       // red_scratch
         BH * (size_t)attn_splits(*L) * (d + 2) * 4,         // attn_scratch
         BH * kCounterInts * 4,          // counters
         4,                              // status
@@ -209,7 +211,7 @@ static SelWs sel_layout(int32_t n_heads, int32_t t, int32_t k_budget, int32_t li
     L.dim_stride = 8;
     L.rank = 8;
     L.rank_stride = 8;
-    L.t_max = t + 1;
+    L.t_max = ((t + 1 + 31) / 32) * 32;
     L.k_budget = k_budget;
     L.lite_budget = lite_budget;
     L.s_cap = k_budget + lite_budget;
@@ -233,7 +235,7 @@ static SelWs sel_layout(int32_t n_heads, int32_t t, int32_t k_budget, int32_t li
     L.step_miss = (int32_t *)take(BH * 4);
     L.step_total = (int32_t *)take(BH * 4);
     L.keys = (uint32_t *)take(BH * L.t_max * 4);
-    L.hist = (uint32_t *)take(BH * kHistBins * 4);
+    L.hist = (uint32_t *)take(BH * 2 * kHistBins * 4);
     L.sel_meta = (int32_t *)take(BH * kMetaInts * 4);
     L.sure_idx = (int32_t *)take(BH * (size_t)k_budget * 4);
     L.cand = (uint64_t *)take(BH * (size_t)L.cand_cap * 8);

@@ -29,7 +29,7 @@ enum Meta : int {
     M_MODE = 7,        // 0 radix path, 1 everything fits, 2 overflow fallback
 };
 
-enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2 };
+enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3 };
 
 // ---------------------------------------------------------------------------
 // vector loads: 16 bytes of storage -> float lanes
@@ -84,6 +84,22 @@ template <> struct Pack<__nv_bfloat16> {
     LRQK_DEV static __nv_bfloat16 cvt(float x) { return __float2bfloat16_rn(x); }
     LRQK_DEV static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
 };
+
+template <typename T> LRQK_DEV void unpack16(uint4 v, float (&o)[Pack<T>::N]);
+template <> LRQK_DEV void unpack16<float>(uint4 v, float (&o)[4]) {
+    o[0] = __uint_as_float(v.x); o[1] = __uint_as_float(v.y);
+    o[2] = __uint_as_float(v.z); o[3] = __uint_as_float(v.w);
+}
+template <> LRQK_DEV void unpack16<__nv_bfloat16>(uint4 v, float (&o)[8]) { Pack<__nv_bfloat16>::unpack(v, o); }
+
+// Proxy-store layout: rows are interleaved in tiles of 32, so that the 16-byte
+// pack p of rows 32*i .. 32*i+31 is one contiguous 512-byte run:
+//     pack index(row, p) = ((row / 32) * packs_per_row + p) * 32 + row % 32
+// The proxy-score GEMV then has lane = row and every warp load fully
+// coalesced; a single row (gathered by index) is packs_per_row 16-byte pieces.
+LRQK_DEV size_t proxy_pack_offset(int row, int p, int packs_per_row) {
+    return ((size_t)(row >> 5) * packs_per_row + p) * 32 + (row & 31);
+}
 
 template <typename T> LRQK_DEV T from_float(float x);
 template <> LRQK_DEV float from_float<float>(float x) { return x; }

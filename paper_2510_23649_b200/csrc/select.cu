@@ -1,55 +1,78 @@
-// K3: proxy scores fused with the radix histogram (cache.py:141-146)
+// K3: proxy scores fused with the (sampled) radix histogram (cache.py:141-146)
 // K4: top-k + lite-window selection (cache.py:149-171, linalg.py:96-110)
 // K5: hit/miss accounting and slot replacement (cache.py:174-196, 63-74)
 //
 // Selection is exact, including the reference's tie rule: the k largest
 // scores win, equal scores prefer the lower index, the result is ascending.
-// Scores become order-preserving uint32 keys (-0.0 == +0.0).  The top-k among
-// [0, lite_start) is found by a radix select on the 53-bit composite
+// Scores become order-preserving uint32 keys (-0.0 == +0.0) and every token
+// gets the unique 53-bit composite
 //     comp = key(32) || (2^21 - 1 - index)(21)
-// which is unique per token and orders exactly like (score desc, index asc).
-//   pass 1 (fused into the score kernel): histogram of the top 11 key bits;
-//   pass 2 (select_scan): tokens above the threshold bin are certain winners,
-//           tokens inside it become candidates (key, index);
-//   pass 3 (select_finalize, one block per head): exact radix select of the
-//           remaining winners among the candidates, ascending compaction via
-//           a shared-memory bitmap, then the cache update.
-// Degenerate score distributions (threshold bin larger than cand_cap) take an
-// exact fallback that radix-selects over the full key array.
+// which orders exactly like (score desc, index asc).
+//
+//   score_kernel   streams the proxy store once (lane = row, tiles of 32 rows
+//                  interleaved so every load is a 512-byte run), writes keys,
+//                  and histograms the top 11 key bits of every s-th tile
+//                  (s = 1, i.e. exact, up to 16K candidate rows).  The last
+//                  block of a head turns the histogram into two bins:
+//                  tokens above b_hi are certainly in the top k, tokens in
+//                  [b_lo, b_hi] are candidates, everything below is out.
+//   select_kernel  re-reads the keys, appends the certain winners and the
+//                  candidates; the last block of a head then verifies
+//                  |sure| <= k <= |sure| + |cand| (the sampled bounds are only
+//                  a hint), bitonic-sorts the candidates' composites, builds
+//                  omega_k ascending through a shared bitmap, appends omega_l,
+//                  and does the cache update.  If the verification fails the
+//                  block falls back to an exact radix select over all keys.
 #include "common.cuh"
 
 namespace lrqk {
 
 constexpr int kScoreThreads = 256;
-constexpr int kScoreChunk = 4096;   // rows per score work item
-constexpr int kScanChunk = 8192;    // keys per select_scan work item
-constexpr int kFinThreads = 1024;
+constexpr int kSelThreads = 512;
 constexpr int kIdxBits = 21;        // tokens per head < 2^21
 constexpr uint32_t kIdxMax = (1u << kIdxBits) - 1u;
+constexpr int kSampleRows = 16384;  // histogram rows per head before sampling kicks in
+
+// extra sel_meta fields (common.cuh holds the first ones)
+enum MetaExt : int { M_B_HI = 8, M_B_LO = 9, M_STRIDE = 10, M_S2 = 11 };
+
+// fine (level-2) bin of a key inside the candidate band [b_lo, b_hi]
+LRQK_DEV int fine_bin(uint32_t key, int b_lo, int s2) {
+    return (int)(key >> (32 - kHistBits - s2)) - (b_lo << s2);
+}
+
 
 LRQK_DEV uint64_t make_comp(uint32_t key, int idx) {
     return ((uint64_t)key << kIdxBits) | (uint64_t)(kIdxMax - (uint32_t)idx);
 }
 LRQK_DEV int comp_index(uint64_t c) { return (int)(kIdxMax - (uint32_t)(c & kIdxMax)); }
 
+LRQK_DEV int sample_stride(int n_rows) {  // in 32-row tiles
+    const int tiles = (n_rows + 31) >> 5;
+    const int want = kSampleRows >> 5;
+    return tiles <= want ? 1 : (tiles + want - 1) / want;
+}
+
 struct ScoreArgs {
     lrqk_layer_t L;
     const float *ext_scores;  // standalone path: precomputed float scores [BH, t+1]
+    int parts;                // work items per head
 };
 
 // Find D in [0, nbins) with  above(D) < m <= above(D) + hist[D], scanning bins
-// from the top.  Whole block participates.  Results in s_out[0]=D, s_out[1]=above.
+// from the top (whole block).  s_out[0] = D (or -1 if total < m), s_out[1] = above.
 __device__ void find_crossing(const int *hist, int nbins, int m, int *s_scan, int *s_out) {
     const int nt = blockDim.x;
     const int per = (nbins + nt - 1) / nt;
-    const int hi = nbins - 1 - threadIdx.x * per;  // my bins: hi, hi-1, ..., hi-per+1
+    const int hi = nbins - 1 - threadIdx.x * per;
+    if (threadIdx.x == 0) { s_out[0] = -1; s_out[1] = 0; }
     int local = 0;
     for (int i = 0; i < per; ++i) {
         const int bin = hi - i;
         if (bin >= 0) local += hist[bin];
     }
     int total;
-    int above = block_exclusive_scan(local, s_scan, &total);
+    const int above = block_exclusive_scan(local, s_scan, &total);
     if (above < m && m <= above + local) {
         int acc = above;
         for (int i = 0; i < per; ++i) {
@@ -67,80 +90,98 @@ __device__ void find_crossing(const int *hist, int nbins, int m, int *s_scan, in
 }
 
 // ---------------------------------------------------------------------------
-// K3: score kernel.  TPR = lanes per proxy row (rank_stride*sizeof(T)/16).
+// K3: score kernel.  NPK = 16-byte packs per proxy row (rank_stride*e/16).
 // ---------------------------------------------------------------------------
-template <typename T, int TPR>
+template <typename T, int NPK>
 __global__ void __launch_bounds__(kScoreThreads)
 score_kernel(const ScoreArgs a) {
     const lrqk_layer_t &L = a.L;
     constexpr int N = Pack<T>::N;
-    constexpr int RPW = 32 / TPR;                       // rows per warp step
-    constexpr int U = 8;                                // steps in flight
+    constexpr int R = NPK * N;
+    constexpr int U = NPK <= 4 ? 4 : (NPK <= 8 ? 2 : 1);  // tiles in flight per warp
+    constexpr int NW = kScoreThreads / 32;
     __shared__ int s_hist[kHistBins];
     __shared__ int s_scan[32];
     __shared__ int s_flag;
     __shared__ int s_out[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int BH = L.batch * L.n_q_heads;
-    const int R = L.rank_stride;
-    const int nch_max = (L.t_max + kScoreChunk - 1) / kScoreChunk;
-    const int sub = lane / TPR, sl = lane - sub * TPR;
+    const int P = a.parts;
 
-    for (int item = blockIdx.x; item < BH * nch_max; item += gridDim.x) {
-        const int bh = item / nch_max, ch = item - bh * nch_max;
+    for (int item = blockIdx.x; item < BH * P; item += gridDim.x) {
+        const int bh = item / P, part = item - bh * P;
         const int b = bh / L.n_q_heads;
         const int t = L.ctx_len[b];
+        if (t >= L.t_max) continue;
         const int n = t + 1;  // scores over tokens 0..t
-        const int nch = (n + kScoreChunk - 1) / kScoreChunk;
-        if (ch >= nch || t >= L.t_max) continue;
         const int lite_start = max(0, n - L.lite_budget);
+        const int tiles = (n + 31) >> 5;
+        const int tpp = (tiles + P - 1) / P;
+        const int tile0 = part * tpp, tile1 = min(tiles, tile0 + tpp);
+        const int stride = sample_stride(lite_start);
         for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = 0;
         __syncthreads();
-        const int row0 = ch * kScoreChunk, row1 = min(n, row0 + kScoreChunk);
         uint32_t *keys = L.keys + (size_t)bh * L.t_max;
         if (a.ext_scores == nullptr) {
-            float qv[N];
-            const float *qh = L.q_hat + (size_t)bh * R + sl * N;
+            float qv[R];
+            const float *qh = L.q_hat + (size_t)bh * L.rank_stride;
 #pragma unroll
-            for (int e = 0; e < N; ++e) qv[e] = qh[e];
-            const T *base = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
-            const int step = (kScoreThreads / 32) * RPW;
-            for (int r0 = row0 + warp * RPW + sub; r0 < row1 + sub; r0 += step * U) {
-                float x[U][N];
+            for (int e = 0; e < R; ++e) qv[e] = qh[e];
+            const uint4 *base = reinterpret_cast<const uint4 *>(reinterpret_cast<const T *>(L.proxy) +
+                                                                 (size_t)bh * L.t_max * R);
+            for (int tb = tile0 + warp; tb < tile1; tb += NW * U) {
+                uint4 x[U][NPK];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int row = r0 + u * step;
-                    if (row < row1) Pack<T>::load_nc(base + (size_t)row * R + sl * N, x[u]);
+                    const int tile = tb + u * NW;
+                    if (tile < tile1) {
+                        const uint4 *p = base + (size_t)tile * NPK * 32 + lane;
+#pragma unroll
+                        for (int pk = 0; pk < NPK; ++pk) {
+                            uint4 v;
+                            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p + pk * 32));
+                            x[u][pk] = v;
+                        }
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int row = r0 + u * step;
-                    float s = 0.f;
+                    const int tile = tb + u * NW;
+                    if (tile >= tile1) break;
+                    float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-                    for (int e = 0; e < N; ++e) s = fmaf(x[u][e], qv[e], s);
-                    s = group_sum<TPR>(s);
-                    if (sl == 0 && row < row1) {
-                        const uint32_t key = score_key(s);
-                        keys[row] = key;
-                        if (row < lite_start) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
+                    for (int pk = 0; pk < NPK; ++pk) {
+                        float f[N];
+                        unpack16<T>(x[u][pk], f);
+#pragma unroll
+                        for (int e = 0; e < N; e += 2) {
+                            s0 = fmaf(f[e], qv[pk * N + e], s0);
+                            s1 = fmaf(f[e + 1], qv[pk * N + e + 1], s1);
+                        }
                     }
+                    const int row = tile * 32 + lane;
+                    const uint32_t key = score_key(s0 + s1);
+                    if (row < n) keys[row] = key;
+                    if (row < lite_start && (tile % stride) == 0)
+                        atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
                 }
             }
         } else {
             const float *sc = a.ext_scores + (size_t)bh * n;
-            for (int row = row0 + tid; row < row1; row += blockDim.x) {
+            for (int row = tile0 * 32 + tid; row < min(n, tile1 * 32); row += blockDim.x) {
                 const uint32_t key = score_key(sc[row]);
                 keys[row] = key;
-                if (row < lite_start) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
+                if (row < lite_start && ((row >> 5) % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
             }
         }
         __syncthreads();
-        uint32_t *ghist = L.hist + (size_t)bh * kHistBins;
+        uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;
         for (int i = tid; i < kHistBins; i += blockDim.x)
             if (s_hist[i]) atomicAdd(ghist + i, (uint32_t)s_hist[i]);
         int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
-        if (!last_arrival(cnt, nch, &s_flag)) continue;
-        // ---- last block of this head: locate the threshold bin -----------
+        if (!last_arrival(cnt, P, &s_flag)) continue;
+        // ---- last block of this head: candidate bins ------------------------
         int *meta = L.sel_meta + (size_t)bh * kMetaInts;
         const int k_eff = min(L.k_budget, lite_start);
         if (lite_start == 0 || k_eff >= lite_start) {
@@ -151,80 +192,38 @@ score_kernel(const ScoreArgs a) {
             continue;
         }
         for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = (int)__ldcg(ghist + i);
-        if (tid == 0) { s_out[0] = -1; s_out[1] = 0; }
         __syncthreads();
-        find_crossing(s_hist, kHistBins, k_eff, s_scan, s_out);
+        int b_hi, b_lo;
+        if (stride == 1) {  // exact histogram: the threshold bin itself
+            find_crossing(s_hist, kHistBins, k_eff, s_scan, s_out);
+            b_hi = b_lo = s_out[0];
+        } else {
+            const int m_hi = max(1, (int)(0.8f * k_eff / stride));
+            find_crossing(s_hist, kHistBins, m_hi, s_scan, s_out);
+            b_hi = s_out[0] < 0 ? kHistBins - 1 : s_out[0];
+            const int m_lo = (int)ceilf(1.25f * k_eff / stride) + 8;
+            find_crossing(s_hist, kHistBins, m_lo, s_scan, s_out);
+            b_lo = s_out[0] < 0 ? 0 : s_out[0];
+        }
         if (tid == 0) {
-            const int bin = s_out[0];
-            meta[M_THR_BIN] = bin;
-            meta[M_N_ABOVE] = s_out[1];
-            meta[M_N_BIN] = s_hist[bin];
+            meta[M_B_HI] = b_hi;
+            meta[M_B_LO] = b_lo;
+            meta[M_STRIDE] = stride;
+            int s2 = 0;
+            while (s2 < 32 - kHistBits && ((b_hi - b_lo + 1) << (s2 + 1)) <= kHistBins) ++s2;
+            meta[M_S2] = s2;
             meta[M_K_EFF] = k_eff;
             meta[M_LITE] = lite_start;
             meta[M_SURE] = 0;
             meta[M_CAND] = 0;
-            meta[M_MODE] = (s_hist[bin] <= L.cand_cap) ? 0 : 2;
+            meta[M_MODE] = 0;
         }
         __syncthreads();
     }
 }
 
-// ---------------------------------------------------------------------------
-// K4a: split the keys below lite_start into certain winners and candidates.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-select_scan_kernel(const lrqk_layer_t L) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int BH = L.batch * L.n_q_heads;
-    const int nch_max = (L.t_max + kScanChunk - 1) / kScanChunk;
-    for (int item = blockIdx.x; item < BH * nch_max; item += gridDim.x) {
-        const int bh = item / nch_max, ch = item - bh * nch_max;
-        const int *meta = L.sel_meta + (size_t)bh * kMetaInts;
-        if (meta[M_MODE] != 0) continue;
-        const int lite_start = meta[M_LITE];
-        const int row0 = ch * kScanChunk;
-        if (row0 >= lite_start) continue;
-        const int row1 = min(lite_start, row0 + kScanChunk);
-        const uint32_t thr = (uint32_t)meta[M_THR_BIN];
-        const uint32_t *keys = L.keys + (size_t)bh * L.t_max;
-        int *sure_cnt = L.sel_meta + (size_t)bh * kMetaInts + M_SURE;
-        int *cand_cnt = L.sel_meta + (size_t)bh * kMetaInts + M_CAND;
-        int *sure = L.sure_idx + (size_t)bh * L.k_budget;
-        uint64_t *cand = L.cand + (size_t)bh * L.cand_cap;
-        for (int base = row0; base < row1; base += blockDim.x * 4) {
-            uint32_t kv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = base + u * blockDim.x + tid;
-                kv[u] = i < row1 ? __ldcg(keys + i) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = base + u * blockDim.x + tid;
-                const uint32_t bin = kv[u] >> (32 - kHistBits);
-                const bool is_sure = i < row1 && bin > thr;
-                const bool is_cand = i < row1 && bin == thr;
-                const unsigned ms = __ballot_sync(0xffffffffu, is_sure);
-                const unsigned mc = __ballot_sync(0xffffffffu, is_cand);
-                if (ms) {
-                    int basei = 0;
-                    if (lane == 0) basei = atomicAdd(sure_cnt, __popc(ms));
-                    basei = __shfl_sync(0xffffffffu, basei, 0);
-                    if (is_sure) sure[basei + __popc(ms & ((1u << lane) - 1u))] = i;
-                }
-                if (mc) {
-                    int basei = 0;
-                    if (lane == 0) basei = atomicAdd(cand_cnt, __popc(mc));
-                    basei = __shfl_sync(0xffffffffu, basei, 0);
-                    if (is_cand) cand[basei + __popc(mc & ((1u << lane) - 1u))] = make_comp(kv[u], i);
-                }
-            }
-        }
-    }
-}
-
-// Radix select over unique composites: returns thr such that exactly m
-// elements have comp >= thr.  get(i) yields element i's composite.
+// Radix select over unique composites (exact fallback): returns thr such that
+// exactly m elements have comp >= thr.
 template <class Get>
 __device__ uint64_t radix_top_m(Get get, int n, int m, int nbits, int *s_hist, int *s_scan, int *s_out) {
     uint64_t prefix = 0;
@@ -242,8 +241,6 @@ __device__ uint64_t radix_top_m(Get get, int n, int m, int nbits, int *s_hist, i
                 atomicAdd(&s_hist[(int)((c >> shift) & (uint64_t)(nb - 1))], 1);
         }
         __syncthreads();
-        if (threadIdx.x == 0) { s_out[0] = 0; s_out[1] = 0; }
-        __syncthreads();
         find_crossing(s_hist, nb, m, s_scan, s_out);
         const int D = s_out[0];
         m -= s_out[1];
@@ -254,201 +251,310 @@ __device__ uint64_t radix_top_m(Get get, int n, int m, int nbits, int *s_hist, i
 }
 
 // ---------------------------------------------------------------------------
-// K4b + K5: finalise the selection of one head and update its cache state.
+// K4 + K5: sure/candidate split with an exact fine histogram of the
+// candidate band, then (last block per head) the exact top-k, ascending
+// omega, and the cache update.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kFinThreads)
-select_finalize_kernel(const lrqk_layer_t L) {
+constexpr int kLocSure = 1024;  // block-local append buffers (spill to global beyond)
+constexpr int kLocCand = 2048;
+
+__global__ void __launch_bounds__(kSelThreads)
+select_kernel(const lrqk_layer_t L, int parts) {
     extern __shared__ __align__(16) uint32_t fsm[];
     __shared__ int s_hist[kHistBins];
     __shared__ int s_scan[32];
     __shared__ int s_out[2];
-    __shared__ int s_tot[4];
-    const int bh = blockIdx.x;
-    const int b = bh / L.n_q_heads;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int t = L.ctx_len[b];
-    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
-    if (t >= L.t_max) return;
-    const int mode = meta[M_MODE];
-    const int lite_start = meta[M_LITE];
-    const int k_eff = meta[M_K_EFF];
-    const int n_words = (lite_start + 31) >> 5;
-    const int S = k_eff + (t + 1 - lite_start);  // |omega_k| + |omega_l|
+    __shared__ int s_flag;
+    __shared__ int s_cnt[4];
+    const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
+    const int BH = L.batch * L.n_q_heads;
     const bool host = L.policy == LRQK_SLOW_HOST;
 
-    // shared layout: [bitmap n_words][new list s_cap][prev list s_cap][prev slots s_cap]
-    //                [new slots s_cap][slot-used bitmap][cand cand_cap (u64)]
-    uint32_t *bitmap = fsm;
-    int *newl = reinterpret_cast<int *>(bitmap + ((n_words + 3) & ~3));
-    int *prevl = newl + L.s_cap;
-    int *prevs = prevl + L.s_cap;
-    int *news = prevs + L.s_cap;
-    uint32_t *slot_used = reinterpret_cast<uint32_t *>(news + L.s_cap);
-    const int slot_words = (L.n_slots + 31) >> 5;
-    uint64_t *cand_s = reinterpret_cast<uint64_t *>(slot_used + ((slot_words + 3) & ~3));
-
-    // ---- Omega_k -----------------------------------------------------------
-    if (mode == 1) {
-        for (int i = tid; i < k_eff; i += nt) newl[i] = i;  // everything fits
-    } else {
-        for (int w = tid; w < n_words; w += nt) bitmap[w] = 0u;
-        __syncthreads();
+    for (int item = blockIdx.x; item < BH * parts; item += gridDim.x) {
+        const int bh = item / parts, part = item - bh * parts;
+        const int b = bh / L.n_q_heads;
+        const int t = L.ctx_len[b];
+        if (t >= L.t_max) continue;
+        int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+        const int mode0 = meta[M_MODE];
+        const int lite_start = meta[M_LITE];
+        const int k_eff = meta[M_K_EFF];
         const uint32_t *keys = L.keys + (size_t)bh * L.t_max;
-        if (mode == 0) {
-            const int n_sure = meta[M_SURE];
-            const int n_cand = meta[M_CAND];
-            const int need = k_eff - n_sure;
-            const uint64_t *cand = L.cand + (size_t)bh * L.cand_cap;
-            for (int i = tid; i < n_cand; i += nt) cand_s[i] = __ldcg(cand + i);
-            const int *sure = L.sure_idx + (size_t)bh * L.k_budget;
-            for (int i = tid; i < n_sure; i += nt) {
-                const int x = __ldcg(sure + i);
-                atomicOr(&bitmap[x >> 5], 1u << (x & 31));
-            }
+        uint32_t *hist2 = L.hist + (size_t)bh * 2 * kHistBins + kHistBins;
+        int *sure = L.sure_idx + (size_t)bh * L.k_budget;
+        uint64_t *cand = L.cand + (size_t)bh * L.cand_cap;
+        // ---- scan part: certain winners, candidates, fine histogram ----------
+        if (mode0 == 0) {
+            const int b_hi = meta[M_B_HI], b_lo = meta[M_B_LO], s2 = meta[M_S2];
+            const int per = (lite_start + parts - 1) / parts;
+            const int row0 = part * per, row1 = min(lite_start, row0 + per);
+            int *loc_sure = reinterpret_cast<int *>(fsm);
+            uint64_t *loc_cand = reinterpret_cast<uint64_t *>(fsm + kLocSure);
+            for (int i = tid; i < kHistBins; i += nt) s_hist[i] = 0;
+            if (tid < 4) s_cnt[tid] = 0;
             __syncthreads();
-            if (need > 0) {
-                // all candidates share the top kHistBits key bits
-                const int nbits = 32 - kHistBits + kIdxBits;
-                const uint64_t lowmask = (1ull << nbits) - 1ull;
-                auto get = [&](int i) { return cand_s[i] & lowmask; };
-                const uint64_t thr = radix_top_m(get, n_cand, need, nbits, s_hist, s_scan, s_out);
-                for (int i = tid; i < n_cand; i += nt) {
-                    if ((cand_s[i] & lowmask) >= thr) {
-                        const int x = comp_index(cand_s[i]);
-                        atomicOr(&bitmap[x >> 5], 1u << (x & 31));
+            for (int base = row0; base < row1; base += nt * 4) {
+                uint32_t kv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = base + u * nt + tid;
+                    kv[u] = i < row1 ? __ldcg(keys + i) : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = base + u * nt + tid;
+                    const int bin = (int)(kv[u] >> (32 - kHistBits));
+                    const bool is_sure = i < row1 && bin > b_hi;
+                    const bool is_cand = i < row1 && bin >= b_lo && bin <= b_hi;
+                    const unsigned ms = __ballot_sync(0xffffffffu, is_sure);
+                    const unsigned mc = __ballot_sync(0xffffffffu, is_cand);
+                    if (ms) {
+                        int basei = 0;
+                        if (lane == 0) basei = atomicAdd(&s_cnt[0], __popc(ms));
+                        basei = __shfl_sync(0xffffffffu, basei, 0);
+                        const int pos = basei + __popc(ms & ((1u << lane) - 1u));
+                        if (is_sure) {
+                            if (pos < kLocSure) loc_sure[pos] = i;
+                            else {  // rare spill: straight to the global list
+                                const int g = atomicAdd(meta + M_SURE, 1);
+                                if (g < L.k_budget) sure[g] = i;
+                            }
+                        }
+                    }
+                    if (mc) {
+                        int basei = 0;
+                        if (lane == 0) basei = atomicAdd(&s_cnt[1], __popc(mc));
+                        basei = __shfl_sync(0xffffffffu, basei, 0);
+                        const int pos = basei + __popc(mc & ((1u << lane) - 1u));
+                        if (is_cand) {
+                            atomicAdd(&s_hist[fine_bin(kv[u], b_lo, s2)], 1);
+                            if (pos < kLocCand) loc_cand[pos] = make_comp(kv[u], i);
+                            else {
+                                const int g = atomicAdd(meta + M_CAND, 1);
+                                if (g < L.cand_cap) cand[g] = make_comp(kv[u], i);
+                            }
+                        }
                     }
                 }
             }
-        } else {
-            // exact fallback over the whole key array
-            auto get = [&](int i) { return make_comp(__ldcg(keys + i), i); };
-            const uint64_t thr = radix_top_m(get, lite_start, k_eff, 32 + kIdxBits, s_hist, s_scan, s_out);
-            for (int i = tid; i < lite_start; i += nt)
-                if (make_comp(__ldcg(keys + i), i) >= thr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
-        }
-        __syncthreads();
-        // ascending compaction of the bitmap
-        const int per = (n_words + nt - 1) / nt;
-        const int w0 = tid * per;
-        int local = 0;
-        for (int w = w0; w < min(n_words, w0 + per); ++w) local += __popc(bitmap[w]);
-        int total;
-        int off = block_exclusive_scan(local, s_scan, &total);
-        for (int w = w0; w < min(n_words, w0 + per); ++w) {
-            uint32_t bits = bitmap[w];
-            while (bits) {
-                const int bpos = __ffs(bits) - 1;
-                bits &= bits - 1u;
-                newl[off++] = (w << 5) + bpos;
+            __syncthreads();
+            const int ns = min(s_cnt[0], kLocSure), nc = min(s_cnt[1], kLocCand);
+            if (tid == 0) {
+                s_cnt[2] = ns ? atomicAdd(meta + M_SURE, ns) : 0;
+                s_cnt[3] = nc ? atomicAdd(meta + M_CAND, nc) : 0;
             }
+            __syncthreads();
+            for (int j = tid; j < ns; j += nt)
+                if (s_cnt[2] + j < L.k_budget) sure[s_cnt[2] + j] = loc_sure[j];
+            for (int j = tid; j < nc; j += nt)
+                if (s_cnt[3] + j < L.cand_cap) cand[s_cnt[3] + j] = loc_cand[j];
+            for (int i = tid; i < kHistBins; i += nt)
+                if (s_hist[i]) atomicAdd(hist2 + i, (uint32_t)s_hist[i]);
         }
-        if (tid == 0 && total != k_eff) set_status(L.status, LRQK_ST_INDEX_RANGE);
-    }
-    // ---- Omega_l (always contains t) --------------------------------------
-    for (int i = tid; i < t + 1 - lite_start; i += nt) newl[k_eff + i] = lite_start + i;
+        if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_SELECT, parts, &s_flag)) continue;
 
-    // ---- K5: hit/miss against Omega_{t-1} U {t} ---------------------------
-    const int n_prev = L.res_cnt[bh];
-    int *res_idx = L.res_idx + (size_t)bh * L.s_cap;
-    int *res_slot = L.res_slot + (size_t)bh * L.s_cap;
-    for (int i = tid; i < n_prev; i += nt) {
-        prevl[i] = res_idx[i];
-        if (host) prevs[i] = res_slot[i];
-    }
-    if (host) for (int w = tid; w < slot_words; w += nt) slot_used[w] = 0u;
-    __syncthreads();
-    const int spare = host ? L.spare_slot[bh] : 0;
-    int hits_local = 0;
-    for (int i = tid; i < S; i += nt) {
-        const int x = newl[i];
-        int pos = -1;
-        if (x != t) {
-            int lo = 0, hi = n_prev - 1;
-            while (lo <= hi) {
-                const int mid = (lo + hi) >> 1;
-                const int v = prevl[mid];
-                if (v == x) { pos = mid; break; }
-                if (v < x) lo = mid + 1; else hi = mid - 1;
+        // ================= finalize (one block per head) =====================
+        const int n_words = (lite_start + 31) >> 5;
+        const int S = k_eff + (t + 1 - lite_start);  // |omega_k| + |omega_l|
+        uint32_t *bitmap = fsm;
+        int *newl = reinterpret_cast<int *>(bitmap + ((((L.t_max + 31) >> 5) + 3) & ~3));
+        int *prevl = newl + L.s_cap;
+        int *prevs = prevl + L.s_cap;
+        int *news = prevs + L.s_cap;
+        uint32_t *slot_used = reinterpret_cast<uint32_t *>(news + L.s_cap);
+        const int slot_words = (L.n_slots + 31) >> 5;
+        uint64_t *crit = reinterpret_cast<uint64_t *>(slot_used + ((slot_words + 3) & ~3));
+        if (mode0 == 1) {
+            for (int i = tid; i < k_eff; i += nt) newl[i] = i;  // everything fits
+        } else {
+            for (int w = tid; w < n_words; w += nt) bitmap[w] = 0u;
+            const int n_sure = __ldcg(meta + M_SURE);
+            const int n_cand = __ldcg(meta + M_CAND);
+            const int need = k_eff - n_sure;
+            bool ok = n_sure <= L.k_budget && need >= 0 && need <= n_cand && n_cand <= L.cand_cap;
+            __syncthreads();
+            if (ok) {
+                for (int i = tid; i < n_sure; i += nt) {
+                    const int x = __ldcg(sure + i);
+                    atomicOr(&bitmap[x >> 5], 1u << (x & 31));
+                }
+                if (need > 0) {
+                    const int b_lo = meta[M_B_LO], s2 = meta[M_S2];
+                    for (int i = tid; i < kHistBins; i += nt) s_hist[i] = (int)__ldcg(hist2 + i);
+                    if (tid == 0) s_cnt[0] = 0;
+                    __syncthreads();
+                    find_crossing(s_hist, kHistBins, need, s_scan, s_out);
+                    const int fstar = s_out[0];
+                    const int need2 = need - s_out[1];
+                    const int n_crit = fstar >= 0 ? s_hist[fstar] : 0;
+                    int M = 1;
+                    while (M < n_crit) M <<= 1;
+                    if (fstar < 0 || M > L.cand_cap) ok = false;  // uniform
+                    if (ok) {
+                        for (int i = tid; i < n_cand; i += nt) {
+                            const uint64_t c = __ldcg(cand + i);
+                            const int f = fine_bin((uint32_t)(c >> kIdxBits), b_lo, s2);
+                            if (f > fstar) {
+                                const int x = comp_index(c);
+                                atomicOr(&bitmap[x >> 5], 1u << (x & 31));
+                            } else if (f == fstar) {
+                                crit[atomicAdd(&s_cnt[0], 1)] = c;
+                            }
+                        }
+                        __syncthreads();
+                        for (int i = n_crit + tid; i < M; i += nt) crit[i] = 0ull;
+                        __syncthreads();
+                        for (int kk = 2; kk <= M; kk <<= 1) {  // bitonic sort, descending
+                            for (int j = kk >> 1; j > 0; j >>= 1) {
+                                for (int i = tid; i < M; i += nt) {
+                                    const int ixj = i ^ j;
+                                    if (ixj > i) {
+                                        const uint64_t x = crit[i], y = crit[ixj];
+                                        const bool desc = (i & kk) == 0;
+                                        if (desc ? (x < y) : (x > y)) { crit[i] = y; crit[ixj] = x; }
+                                    }
+                                }
+                                __syncthreads();
+                            }
+                        }
+                        for (int i = tid; i < need2; i += nt) {
+                            const int x = comp_index(crit[i]);
+                            atomicOr(&bitmap[x >> 5], 1u << (x & 31));
+                        }
+                    }
+                }
+            }
+            if (!ok) {
+                // exact fallback over the whole key array
+                __syncthreads();
+                for (int w = tid; w < n_words; w += nt) bitmap[w] = 0u;
+                if (tid == 0) set_status(L.status, LRQK_ST_FALLBACK);
+                auto get = [&](int i) { return make_comp(__ldcg(keys + i), i); };
+                const uint64_t thr = radix_top_m(get, lite_start, k_eff, 32 + kIdxBits, s_hist, s_scan, s_out);
+                for (int i = tid; i < lite_start; i += nt)
+                    if (make_comp(__ldcg(keys + i), i) >= thr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+            }
+            __syncthreads();
+            // ascending compaction of the bitmap
+            const int per = (n_words + nt - 1) / nt;
+            const int w0 = tid * per;
+            int local = 0;
+            for (int w = w0; w < min(n_words, w0 + per); ++w) local += __popc(bitmap[w]);
+            int total;
+            int off = block_exclusive_scan(local, s_scan, &total);
+            for (int w = w0; w < min(n_words, w0 + per); ++w) {
+                uint32_t bits = bitmap[w];
+                while (bits) {
+                    const int bpos = __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    newl[off++] = (w << 5) + bpos;
+                }
+            }
+            if (tid == 0 && total != k_eff) set_status(L.status, LRQK_ST_INDEX_RANGE);
+        }
+        for (int i = tid; i < t + 1 - lite_start; i += nt) newl[k_eff + i] = lite_start + i;  // omega_l
+
+        // ---- K5: hit/miss against Omega_{t-1} U {t} ---------------------------
+        const int n_prev = L.res_cnt[bh];
+        int *res_idx = L.res_idx + (size_t)bh * L.s_cap;
+        int *res_slot = L.res_slot + (size_t)bh * L.s_cap;
+        for (int i = tid; i < n_prev; i += nt) {
+            prevl[i] = res_idx[i];
+            if (host) prevs[i] = res_slot[i];
+        }
+        if (host) for (int w = tid; w < slot_words; w += nt) slot_used[w] = 0u;
+        __syncthreads();
+        const int spare = host ? L.spare_slot[bh] : 0;
+        int hits_local = 0;
+        for (int i = tid; i < S; i += nt) {
+            const int x = newl[i];
+            int pos = -1;
+            if (x != t) {
+                int lo = 0, hi = n_prev - 1;
+                while (lo <= hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const int v = prevl[mid];
+                    if (v == x) { pos = mid; break; }
+                    if (v < x) lo = mid + 1; else hi = mid - 1;
+                }
+            }
+            hits_local += ((x == t) || pos >= 0) ? 1 : 0;
+            if (host) {
+                int s = -1;
+                if (x == t) s = spare;
+                else if (pos >= 0) s = prevs[pos];
+                news[i] = s;
+                if (s >= 0) atomicOr(&slot_used[s >> 5], 1u << (s & 31));
             }
         }
-        const bool hit = (x == t) || pos >= 0;
-        hits_local += hit;
+        int hits;
+        block_exclusive_scan(hits_local, s_scan, &hits);
+        const int miss = S - hits;
         if (host) {
-            int s = -1;
-            if (x == t) s = spare;
-            else if (pos >= 0) s = prevs[pos];
-            news[i] = s;
-            if (s >= 0) atomicOr(&slot_used[s >> 5], 1u << (s & 31));
-        }
-    }
-    int hits;
-    block_exclusive_scan(hits_local, s_scan, &hits);
-    const int miss = S - hits;
-    if (host) {
-        __syncthreads();
-        // misses in ascending order, paired with free slots in ascending order
-        int mloc = 0;
-        const int per = (S + nt - 1) / nt;
-        const int i0 = tid * per;
-        for (int i = i0; i < min(S, i0 + per); ++i) mloc += news[i] < 0;
-        int mtot;
-        int moff = block_exclusive_scan(mloc, s_scan, &mtot);
-        int floc = 0;
-        const int fper = (slot_words + nt - 1) / nt;
-        const int f0 = tid * fper;
-        for (int w = f0; w < min(slot_words, f0 + fper); ++w) {
-            uint32_t freew = ~slot_used[w];
-            if (w == slot_words - 1 && (L.n_slots & 31)) freew &= (1u << (L.n_slots & 31)) - 1u;
-            floc += __popc(freew);
-        }
-        int ftot;
-        int foff = block_exclusive_scan(floc, s_scan, &ftot);
-        // free slot list -> prevs (reuse) ; miss positions -> prevl (reuse)
-        __syncthreads();
-        int *free_list = prevs;
-        int *miss_pos = prevl;
-        for (int w = f0; w < min(slot_words, f0 + fper); ++w) {
-            uint32_t freew = ~slot_used[w];
-            if (w == slot_words - 1 && (L.n_slots & 31)) freew &= (1u << (L.n_slots & 31)) - 1u;
-            while (freew) {
-                const int bpos = __ffs(freew) - 1;
-                freew &= freew - 1u;
-                free_list[foff++] = (w << 5) + bpos;
+            __syncthreads();
+            // misses in ascending order, paired with free slots in ascending order
+            const int per = (S + nt - 1) / nt;
+            const int i0 = tid * per;
+            int mloc = 0;
+            for (int i = i0; i < min(S, i0 + per); ++i) mloc += news[i] < 0;
+            int mtot;
+            int moff = block_exclusive_scan(mloc, s_scan, &mtot);
+            const int fper = (slot_words + nt - 1) / nt;
+            const int f0 = tid * fper;
+            int floc = 0;
+            for (int w = f0; w < min(slot_words, f0 + fper); ++w) {
+                uint32_t freew = ~slot_used[w];
+                if (w == slot_words - 1 && (L.n_slots & 31)) freew &= (1u << (L.n_slots & 31)) - 1u;
+                floc += __popc(freew);
             }
+            int ftot;
+            int foff = block_exclusive_scan(floc, s_scan, &ftot);
+            __syncthreads();
+            int *free_list = prevs;
+            int *miss_pos = prevl;
+            for (int w = f0; w < min(slot_words, f0 + fper); ++w) {
+                uint32_t freew = ~slot_used[w];
+                if (w == slot_words - 1 && (L.n_slots & 31)) freew &= (1u << (L.n_slots & 31)) - 1u;
+                while (freew) {
+                    const int bpos = __ffs(freew) - 1;
+                    freew &= freew - 1u;
+                    free_list[foff++] = (w << 5) + bpos;
+                }
+            }
+            for (int i = i0; i < min(S, i0 + per); ++i)
+                if (news[i] < 0) miss_pos[moff++] = i;
+            __syncthreads();
+            int *mi = L.miss_idx + (size_t)bh * L.s_cap;
+            int *ms = L.miss_slot + (size_t)bh * L.s_cap;
+            for (int j = tid; j < mtot; j += nt) {
+                const int i = miss_pos[j];
+                const int s = free_list[j];
+                news[i] = s;
+                mi[j] = newl[i];
+                ms[j] = s;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                L.miss_cnt[bh] = mtot;
+                L.spare_slot[bh] = (ftot > mtot) ? free_list[mtot] : 0;
+                if (ftot <= mtot) set_status(L.status, LRQK_ST_CAPACITY);
+            }
+            for (int i = tid; i < S; i += nt) res_slot[i] = news[i];
         }
-        for (int i = i0; i < min(S, i0 + per); ++i)
-            if (news[i] < 0) miss_pos[moff++] = i;
-        __syncthreads();
-        int *mi = L.miss_idx + (size_t)bh * L.s_cap;
-        int *ms = L.miss_slot + (size_t)bh * L.s_cap;
-        for (int j = tid; j < mtot; j += nt) {
-            const int i = miss_pos[j];
-            const int s = free_list[j];
-            news[i] = s;
-            mi[j] = newl[i];
-            ms[j] = s;
-        }
-        __syncthreads();
+        for (int i = tid; i < S; i += nt) res_idx[i] = newl[i];
         if (tid == 0) {
-            L.miss_cnt[bh] = mtot;
-            L.spare_slot[bh] = (ftot > mtot) ? free_list[mtot] : 0;
-            if (ftot <= mtot) set_status(L.status, LRQK_ST_CAPACITY);
+            L.res_cnt[bh] = S;
+            L.c_miss[bh] += miss;
+            L.c_total[bh] += S;
+            L.step_miss[bh] = miss;
+            L.step_total[bh] = S;
+            meta[M_SURE] = 0;
+            meta[M_CAND] = 0;
         }
-        for (int i = tid; i < S; i += nt) res_slot[i] = news[i];
+        uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;  // both levels, ready for the next step
+        for (int i = tid; i < 2 * kHistBins; i += nt) ghist[i] = 0u;
+        __syncthreads();
     }
-    for (int i = tid; i < S; i += nt) res_idx[i] = newl[i];
-    if (tid == 0) {
-        L.res_cnt[bh] = S;
-        L.c_miss[bh] += miss;
-        L.c_total[bh] += S;
-        L.step_miss[bh] = miss;
-        L.step_total[bh] = S;
-        meta[M_SURE] = 0;
-        meta[M_CAND] = 0;
-    }
-    // clear the histogram for the next step
-    uint32_t *ghist = L.hist + (size_t)bh * kHistBins;
-    for (int i = tid; i < kHistBins; i += nt) ghist[i] = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -465,14 +571,20 @@ int num_sms() {
     return g_num_sms;
 }
 
+static int score_parts(const lrqk_layer_t &L) {
+    const int BH = L.batch * L.n_q_heads;
+    const int tiles = (L.t_max + 31) / 32;
+    const int want = (num_sms() * 4 + BH - 1) / BH;
+    return max(1, min(want, max(1, tiles / 8)));
+}
+
 template <typename T>
 static int launch_score_t(const ScoreArgs &a, cudaStream_t st) {
     const lrqk_layer_t &L = a.L;
     const int BH = L.batch * L.n_q_heads;
-    const int items = BH * ((L.t_max + kScoreChunk - 1) / kScoreChunk);
-    const int grid = max(1, min(items, num_sms() * 4));
-    const int tpr = L.rank_stride * (int)sizeof(T) / 16;
-    switch (tpr) {
+    const int grid = max(1, min(BH * a.parts, num_sms() * 4));
+    const int npk = L.rank_stride * (int)sizeof(T) / 16;
+    switch (npk) {
         case 1: score_kernel<T, 1><<<grid, kScoreThreads, 0, st>>>(a); break;
         case 2: score_kernel<T, 2><<<grid, kScoreThreads, 0, st>>>(a); break;
         case 4: score_kernel<T, 4><<<grid, kScoreThreads, 0, st>>>(a); break;
@@ -484,25 +596,28 @@ static int launch_score_t(const ScoreArgs &a, cudaStream_t st) {
 }
 
 int launch_score(const lrqk_layer_t &L, const float *ext_scores, cudaStream_t st) {
-    ScoreArgs a{L, ext_scores};
+    ScoreArgs a{L, ext_scores, score_parts(L)};
     return L.dtype == LRQK_BF16 ? launch_score_t<__nv_bfloat16>(a, st) : launch_score_t<float>(a, st);
 }
 
 size_t finalize_smem_bytes(const lrqk_layer_t &L) {
     const size_t n_words = ((size_t)L.t_max + 31) / 32;
     const size_t slot_words = ((size_t)L.n_slots + 31) / 32;
-    return ((n_words + 3) & ~(size_t)3) * 4 + 4 * (size_t)L.s_cap * 4 + ((slot_words + 3) & ~(size_t)3) * 4 +
-           (size_t)L.cand_cap * 8;
+    size_t cand_pow2 = 1;
+    while (cand_pow2 < (size_t)L.cand_cap) cand_pow2 <<= 1;
+    const size_t fin = ((n_words + 3) & ~(size_t)3) * 4 + 4 * (size_t)L.s_cap * 4 +
+                       ((slot_words + 3) & ~(size_t)3) * 4 + cand_pow2 * 8;
+    const size_t scan = (size_t)kLocSure * 4 + (size_t)kLocCand * 8;
+    return fin > scan ? fin : scan;
 }
 
 int launch_select(const lrqk_layer_t &L, cudaStream_t st) {
     const int BH = L.batch * L.n_q_heads;
-    const int items = BH * ((L.t_max + kScanChunk - 1) / kScanChunk);
-    const int grid = max(1, min(items, num_sms() * 4));
-    select_scan_kernel<<<grid, 256, 0, st>>>(L);
+    const int parts = max(1, min((num_sms() * 2 + BH - 1) / BH, max(1, L.t_max / 4096)));
+    const int grid = max(1, min(BH * parts, num_sms() * 2));
     const size_t smem = finalize_smem_bytes(L);
-    cudaFuncSetAttribute(select_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    select_finalize_kernel<<<BH, kFinThreads, smem, st>>>(L);
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    select_kernel<<<grid, kSelThreads, smem, st>>>(L, parts);
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 

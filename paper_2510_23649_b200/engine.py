@@ -60,6 +60,10 @@ class LayerShape:
     dtype: str = "bf16"      # storage dtype of proxy rows and K/V rows
     policy: str = "hbm"      # "hbm" | "host"  (slow-tier placement)
 
+    def __post_init__(self):
+        # stores are tiled in 32-row groups (proxy layout, common.cuh)
+        object.__setattr__(self, "t_max", (self.t_max + 31) // 32 * 32)
+
     @property
     def dim_stride(self):
         return pow2_at_least(self.head_dim)
@@ -164,7 +168,6 @@ class LayerState:
         ds, rs = sh.dim_stride, sh.rank_stride
         S = sh.k_budget + sh.lite_budget
         spec = {
-            "proxy": (self.sdt, (B, Hq, T, rs)),
             "B_Q": (torch.float32, (B, Hq, rs, ds)),
             "B_K": (torch.float32, (B, Hq, rs, ds)),
             "slow_k": (self.sdt, (B, Hkv, T, ds)),
@@ -190,6 +193,23 @@ class LayerState:
             return self.host_tiers[name].as_tensor(dt, shp)
         n = int(np.prod(shp)) * torch.empty((), dtype=dt).element_size()
         return self.buf[name][:n].view(dt).view(*shp)
+
+    @property
+    def pack_elems(self):
+        return 16 // torch.empty((), dtype=self.sdt).element_size()
+
+    def proxy_tiles(self):
+        """Raw proxy store in its interleaved layout [B, Hq, T/32, packs, 32, N]
+        (common.cuh: proxy_pack_offset)."""
+        sh = self.shape
+        N = self.pack_elems
+        shp = (sh.batch, sh.n_q_heads, sh.t_max // 32, sh.rank_stride // N, 32, N)
+        n = int(np.prod(shp)) * torch.empty((), dtype=self.sdt).element_size()
+        return self.buf["proxy"][:n].view(self.sdt).view(*shp)
+
+    def proxy_rows(self):
+        """Logical copy of the proxy store, [B, Hq, T, rank_stride]."""
+        return from_tiles(self.proxy_tiles())
 
     @property
     def ptr(self):
@@ -218,8 +238,10 @@ class LayerState:
         l = K.shape[2]
         if l > sh.t_max:
             raise ValueError(f"prompt of {l} tokens exceeds t_max={sh.t_max}")
-        prox = self.view("proxy")
-        prox[:, :, :l, : A_K.shape[-1]].copy_(A_K.to(self.sdt))
+        tl = (l + 31) // 32
+        rows = A_K.new_zeros(sh.batch, sh.n_q_heads, tl * 32, sh.rank_stride)
+        rows[:, :, :l, : A_K.shape[-1]] = A_K
+        self.proxy_tiles()[:, :, :tl].copy_(to_tiles(rows.to(self.sdt), self.pack_elems))
         self.view("B_Q")[:, :, : B_Q.shape[2], : B_Q.shape[3]].copy_(B_Q)
         self.view("B_K")[:, :, : B_K.shape[2], : B_K.shape[3]].copy_(B_K)
         sk, sv = self.view("slow_k"), self.view("slow_v")
@@ -237,6 +259,18 @@ class LayerState:
         _lib.check(_lib.lib().lrqk_decode_step(self.ptr, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                out.data_ptr(), int(advance), _lib.stream_ptr(stream)),
                    "lrqk_decode_step")
+
+
+def to_tiles(rows: torch.Tensor, N: int) -> torch.Tensor:
+    """[..., T, R] (T multiple of 32) -> interleaved [..., T/32, R/N, 32, N]."""
+    *lead, T, R = rows.shape
+    return rows.reshape(*lead, T // 32, 32, R // N, N).transpose(-3, -2)
+
+
+def from_tiles(tiles: torch.Tensor) -> torch.Tensor:
+    """Inverse of to_tiles: [..., T/32, R/N, 32, N] -> [..., T, R]."""
+    *lead, nt, npk, _, N = tiles.shape
+    return tiles.transpose(-3, -2).reshape(*lead, nt * 32, npk * N)
 
 
 def pad_last(x: torch.Tensor, width: int) -> torch.Tensor:

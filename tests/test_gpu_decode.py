@@ -33,7 +33,7 @@ def _gpu_state(layer, b, h, t):
     res = layer.view("res_idx")[b, h, :n].cpu().numpy().astype(np.int64)
     K = layer.view("slow_k")[b, g, :t, :d].float().cpu().numpy().astype(np.float64)
     V = layer.view("slow_v")[b, g, :t, :d].float().cpu().numpy().astype(np.float64)
-    P = layer.view("proxy")[b, h, :t, :r].float().cpu().numpy().astype(np.float64)
+    P = layer.proxy_rows()[b, h, :t, :r].float().cpu().numpy().astype(np.float64)
     BQ = layer.view("B_Q")[b, h, :r, :d].cpu().numpy().astype(np.float64)
     BK = layer.view("B_K")[b, h, :r, :d].cpu().numpy().astype(np.float64)
     return res, K, V, P, BQ, BK
@@ -213,3 +213,42 @@ def test_host_policy_matches_hbm_policy(dtype):
     slot_rows = L.view("slot_k")[0, 0][slots].cpu()
     want = L.view("slow_k")[0, 0][idx.cpu()]
     assert torch.equal(slot_rows, want)
+
+
+def _select_exact_check(layer, t, kb, lb):
+    keys = layer.view("keys").cpu().numpy().view(np.uint32)
+    cnt = layer.view("res_cnt").cpu().numpy()
+    idx = layer.view("res_idx").cpu().numpy()
+    for b in range(layer.shape.batch):
+        for h in range(layer.shape.n_q_heads):
+            got = idx[b, h, : cnt[b, h]].astype(np.int64)
+            _, _, exact = O.select(_keys_to_scores(keys[b, h, : t + 1]), t, kb, lb)
+            np.testing.assert_array_equal(got, exact)
+
+
+@pytest.mark.parametrize("kind", ["gaussian", "ties", "constant"])
+def test_selection_exact_at_long_context(kind):
+    """Contexts beyond 16K rows take the sampled-histogram path (coarse bins
+    from a 1/s sample, exact fine histogram of the candidate band); heavy ties
+    and constant scores exercise the verification / exact fallback."""
+    rng = np.random.default_rng(3)
+    B, Hq, Hkv, d, r, kb, lb, l = 1, 2, 1, 128, 32, 2048, 16, 40000
+    if kind == "gaussian":
+        A = rng.standard_normal((B, Hq, l, r))
+    elif kind == "ties":
+        A = np.round(rng.standard_normal((B, Hq, l, r)) * 2) / 2  # few distinct score values
+    else:
+        A = np.ones((B, Hq, l, r))
+    K = quantize(rng.standard_normal((B, Hkv, l + 3, d)), "bf16")
+    V = quantize(rng.standard_normal((B, Hkv, l + 3, d)), "bf16")
+    BQ = rng.standard_normal((B, Hq, r, d)) / np.sqrt(d)
+    BK = rng.standard_normal((B, Hq, r, d)) / np.sqrt(d)
+    layer = make_layer(B, Hq, Hkv, d, r, kb, lb, t_max=l + 8, dtype="bf16")
+    seed_layer(layer, quantize(A, "bf16"), BQ, BK, K[:, :, :l], V[:, :, :l])
+    out = torch.zeros(B, Hq, d, device="cuda")
+    Q = quantize(rng.standard_normal((B, Hq, l + 3, d)), "bf16")
+    for t in range(l, l + 3):
+        layer.step(rows_dev(Q[:, :, t], layer), rows_dev(K[:, :, t], layer), rows_dev(V[:, :, t], layer), out)
+        torch.cuda.synchronize()
+        layer.raise_status()
+        _select_exact_check(layer, t, kb, lb)
