@@ -103,6 +103,9 @@ typedef struct lrqk_layer {
     float *attn_scratch;           /* [B,Hq,attn_splits,dim_stride+2]          */
     int32_t *counters;             /* [B,Hq,8] arrival counters, zero between steps */
     uint32_t *status;              /* [1] device status word                  */
+
+    /* ---- persistent precompute of the next step's compression (K2p) ---- */
+    float *pre;                    /* [B,Hq,pre_floats]: P^-1, R^-1, P, R, Z_Q, Z_K, W, flags */
 } lrqk_layer_t;
 
 /* Sizes (bytes) of every buffer in lrqk_layer_t for the given configuration,
@@ -117,6 +120,14 @@ int lrqk_attn_splits(const lrqk_layer_t *cfg);
  * prompt; sets ctx_len=l, fast tier = last lite_budget prompt rows, zeroes
  * counters/hist, fills slots (host policy).  ref: cache.py:114-124. */
 int lrqk_seed_prompt(const lrqk_layer_t *L, int32_t prompt_len, void *stream);
+
+/* Precompute, from the current fast-tier set Omega and B factors, everything
+ * the next token's compression needs except q and k (A_res^T K_res,
+ * A_res^T A_res, the r x r inverses, Z_Q, Z_K).  Runs after lrqk_select of
+ * the previous step (after lrqk_gather_misses in the host policy) and after
+ * lrqk_seed_prompt; may overlap the rest of the step on a side stream.
+ * ref: decode.py:84-119 (the q/k-independent parts of update_qhat/khat). */
+int lrqk_compress_prepare(const lrqk_layer_t *L, void *stream);
 
 /* Per-token compression + B line-search update + append of k_hat/k/v.
  * ref: decode.py:122-184 (decode_compress, update_projections),
@@ -199,6 +210,10 @@ size_t lrqk_sizeof_prefill(void);
 void *lrqk_host_alloc(size_t bytes);
 void lrqk_host_free(void *p);
 void *lrqk_host_device_ptr(void *p);
+
+/* Development tracing of kernel phases (%globaltimer records). */
+int lrqk_trace_enable(int on);
+int lrqk_trace_read(unsigned long long *out, int cap);
 
 #ifdef __cplusplus
 }

@@ -21,6 +21,7 @@ ST_SOLVE_FAILED = 2
 ST_INDEX_RANGE = 4
 ST_CAPACITY = 8
 ST_JITTERED = 16
+ST_FALLBACK = 32
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 
@@ -31,7 +32,7 @@ _FLOAT_FIELDS = ("lambda_1", "lambda_2", "tol")
 BUFFER_NAMES = ("proxy", "B_Q", "B_K", "slow_k", "slow_v", "slot_k", "slot_v", "ctx_len", "res_idx",
                 "res_slot", "res_cnt", "spare_slot", "miss_idx", "miss_slot", "miss_cnt", "c_miss",
                 "c_total", "step_miss", "step_total", "q_hat", "k_hat", "eta", "keys", "hist",
-                "sel_meta", "sure_idx", "cand", "red_scratch", "attn_scratch", "counters", "status")
+                "sel_meta", "sure_idx", "cand", "red_scratch", "attn_scratch", "counters", "status", "pre")
 
 
 class LayerStruct(C.Structure):
@@ -71,6 +72,7 @@ SIGNATURES = {
     "lrqk_attn_splits": (C.c_int, [C.POINTER(LayerStruct)]),
     "lrqk_seed_prompt": (C.c_int, [C.POINTER(LayerStruct), C.c_int32, _P]),
     "lrqk_decode_compress": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P, C.c_int, _P]),
+    "lrqk_compress_prepare": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_score": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_select": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_gather_misses": (C.c_int, [C.POINTER(LayerStruct), _P]),
@@ -87,6 +89,8 @@ SIGNATURES = {
     "lrqk_host_alloc": (_P, [C.c_size_t]),
     "lrqk_host_free": (None, [_P]),
     "lrqk_host_device_ptr": (_P, [_P]),
+    "lrqk_trace_enable": (C.c_int, [C.c_int]),
+    "lrqk_trace_read": (C.c_int, [_P, C.c_int]),
 }
 
 

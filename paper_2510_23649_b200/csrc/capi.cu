@@ -8,6 +8,8 @@ namespace lrqk {
 int launch_compress(const lrqk_layer_t &L, const void *q, const void *k, const void *v, int update_b, cudaStream_t st);
 int compress_chunks(const lrqk_layer_t &L);
 size_t compress_scratch_floats_per_head(const lrqk_layer_t &L);
+size_t compress_pre_floats_per_head(const lrqk_layer_t &L);
+int launch_prepare(const lrqk_layer_t &L, cudaStream_t st);
 int launch_score(const lrqk_layer_t &L, const float *ext_scores, cudaStream_t st);
 int launch_select(const lrqk_layer_t &L, cudaStream_t st);
 int launch_gather(const lrqk_layer_t &L, cudaStream_t st);
@@ -78,7 +80,7 @@ const char *lrqk_last_error(void) { return g_err; }
 const char *lrqk_buffer_names(void) {
     return "proxy,B_Q,B_K,slow_k,slow_v,slot_k,slot_v,ctx_len,res_idx,res_slot,res_cnt,spare_slot,miss_idx,"
            "miss_slot,miss_cnt,c_miss,c_total,step_miss,step_total,q_hat,k_hat,eta,keys,hist,sel_meta,sure_idx,"
-           "cand,red_scratch,attn_scratch,counters,status";
+           "cand,red_scratch,attn_scratch,counters,status,pre";
 }
 
 int lrqk_red_chunks(const lrqk_layer_t *L) { return compress_chunks(*L); }
@@ -123,6 +125,7 @@ int lrqk_layer_buffer_bytes(const lrqk_layer_t *L, size_t *out, int max_out) {
         BH * (size_t)attn_splits(*L) * (d + 2) * 4,         // attn_scratch
         BH * kCounterInts * 4,          // counters
         4,                              // status
+        BH * compress_pre_floats_per_head(*L) * 4,  // pre
     };
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < n && i < max_out; ++i) out[i] = v[i];
@@ -133,7 +136,15 @@ int lrqk_seed_prompt(const lrqk_layer_t *L, int32_t prompt_len, void *stream) {
     int rc = validate(L);
     if (rc) return rc;
     if (prompt_len < 1 || prompt_len > L->t_max) return LRQK_EINVAL;
-    return check(launch_seed(*L, prompt_len, (cudaStream_t)stream));
+    int rc2 = check(launch_seed(*L, prompt_len, (cudaStream_t)stream));
+    if (rc2) return rc2;
+    return check(launch_prepare(*L, (cudaStream_t)stream));
+}
+
+int lrqk_compress_prepare(const lrqk_layer_t *L, void *stream) {
+    int rc = validate(L);
+    if (rc) return rc;
+    return check(launch_prepare(*L, (cudaStream_t)stream));
 }
 
 int lrqk_decode_compress(const lrqk_layer_t *L, const void *q, const void *k, const void *v, int update_b,
@@ -179,6 +190,7 @@ int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const 
     if ((rc = check(launch_select(*L, st)))) return rc;
     if ((rc = check(launch_gather(*L, st)))) return rc;
     if ((rc = check(launch_attention(*L, q, out, st)))) return rc;
+    if ((rc = check(launch_prepare(*L, st)))) return rc;
     if (advance) rc = check(launch_advance(L->ctx_len, L->batch, st));
     return rc;
 }
@@ -292,3 +304,26 @@ int lrqk_read_status(const uint32_t *status, uint32_t *host_out, void *stream) {
 }
 
 }  // extern "C"
+
+// ---- development tracing (see common.cuh) --------------------------------
+namespace lrqk {
+__device__ int g_lrqk_trace_on = 0;
+__device__ unsigned int g_lrqk_trace_n = 0;
+__device__ unsigned long long g_lrqk_trace[kTraceCap][2];
+}  // namespace lrqk
+
+extern "C" int lrqk_trace_enable(int on) {
+    unsigned int zero = 0;
+    if (cudaMemcpyToSymbol(lrqk::g_lrqk_trace_on, &on, sizeof(int)) != cudaSuccess) return LRQK_ECUDA;
+    if (cudaMemcpyToSymbol(lrqk::g_lrqk_trace_n, &zero, sizeof zero) != cudaSuccess) return LRQK_ECUDA;
+    return LRQK_OK;
+}
+
+extern "C" int lrqk_trace_read(unsigned long long *out, int cap) {
+    unsigned int n = 0;
+    if (cudaMemcpyFromSymbol(&n, lrqk::g_lrqk_trace_n, sizeof n) != cudaSuccess) return -1;
+    if ((int)n > cap) n = cap;
+    if (n > (unsigned)lrqk::kTraceCap) n = lrqk::kTraceCap;
+    if (n && cudaMemcpyFromSymbol(out, lrqk::g_lrqk_trace, (size_t)n * 16) != cudaSuccess) return -1;
+    return (int)n;
+}

@@ -14,7 +14,7 @@ constexpr int kHistBits = 11;
 constexpr int kHistBins = 1 << kHistBits;  // 2048 bins on the top 11 key bits
 constexpr int kMetaInts = 16;
 constexpr int kCounterInts = 8;
-constexpr int kRedRows = 256;      // resident rows per compression partial
+constexpr int kRedRows = 384;      // resident rows per compression partial
 constexpr int kAttnRows = 128;     // selected rows per attention split
 
 // sel_meta layout, per (b, h)
@@ -29,7 +29,7 @@ enum Meta : int {
     M_MODE = 7,        // 0 radix path, 1 everything fits, 2 overflow fallback
 };
 
-enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3 };
+enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3, C_PREPARE = 4 };
 
 // ---------------------------------------------------------------------------
 // vector loads: 16 bytes of storage -> float lanes
@@ -193,4 +193,26 @@ LRQK_DEV bool last_arrival(int *counter, int expected, int *s_flag) {
     return *s_flag != 0;
 }
 
+}  // namespace lrqk
+
+// ---------------------------------------------------------------------------
+// Development tracing: when g_lrqk_trace_on is set (lrqk_trace_enable), thread
+// 0 of a block records (tag, block, %globaltimer) records.  Off by default.
+// ---------------------------------------------------------------------------
+namespace lrqk {
+constexpr int kTraceCap = 1 << 16;
+extern __device__ int g_lrqk_trace_on;
+extern __device__ unsigned int g_lrqk_trace_n;
+extern __device__ unsigned long long g_lrqk_trace[kTraceCap][2];
+LRQK_DEV void trace(int tag) {
+    if (g_lrqk_trace_on && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const unsigned i = atomicAdd(&g_lrqk_trace_n, 1u);
+        if (i < kTraceCap) {
+            g_lrqk_trace[i][0] = ((unsigned long long)tag << 48) | ((unsigned long long)blockIdx.y << 24) | blockIdx.x;
+            g_lrqk_trace[i][1] = t;
+        }
+    }
+}
 }  // namespace lrqk

@@ -5,25 +5,29 @@
 //      decode_compress, _line_search_step, update_projections),
 //      cache.py:199-214 (append_token), session.py:95-98 (order).
 //
-// Work layout: grid.y = B*Hq (one reference session per y).  Along grid.x,
-//   blocks 0..n_chunks-1  ("reduce" blocks) each take kRedRows rows of the
-//       previous resident set Omega_{t-1} and produce partial sums of
-//           G_res = A_res^T A_res            (decode.py:106)
-//           m_res = (q K_res^T) A_res        (decode.py:105)
-//   block n_chunks       ("prep" block) works concurrently on everything that
-//       does not depend on Omega_{t-1}:  R = B_K B_K^T, its inverse,
-//       k_hat0 = (k B_K^T) R^-1 (decode.py:79-81), B_Q B_Q^T, q B_Q^T, q.k.
-// The last block of the head to arrive ("finish") forms
-//   P = B_Q B_Q^T + l2 G_res, inverts it, and runs the alternation with the
-// closed form of a rank-1-updated SPD system
-//        x (S + l1 v^T v) = b + l1 qk v
-//        =>  x = y + u * l1 (qk - y.v) / (1 + l1 v.u),  y = b S^-1, u = v S^-1,
-// which is algebraically the reference's solve_spd(M, RHS) with
-// M = S + l1 v^T v (decode.py:100-108, 115-119).  Inverses come from an
-// in-place Gauss-Jordan sweep without pivoting: every pivot is > 0 exactly
-// when the matrix is numerically SPD, i.e. when the reference's Cholesky
-// succeeds.  If P or R is not SPD the finish block solves each full system
-// directly with the reference's single jitter retry (linalg.py:80-91).
+// The reference solves, per token (decode.py:84-119),
+//     q_hat = solve(P + l1 k_hat^T k_hat,  q B_Q^T + l1 qk k_hat + l2 (q K_res^T) A_res)
+//     k_hat = solve(R + l1 q_hat^T q_hat,  k B_K^T + l1 qk q_hat)
+// with P = B_Q B_Q^T + l2 A_res^T A_res and R = B_K B_K^T.  Everything in
+// those systems except q, k themselves is fixed once step t-1 has finished
+// (its selection Omega_{t-1} and its B update), because
+//     (q K_res^T) A_res = q (A_res^T K_res)^T = q Y^T.
+// So the work is split in two kernels:
+//   compress_prepare (K2p, after step t-1's selection; off the critical
+//     path, on a side stream in the captured engine step):
+//       Y = A_res^T K_res, G = A_res^T A_res over Omega_{t-1};
+//       P, R, their inverses (Gauss-Jordan; P, R kept for the fallback);
+//       W = B_Q + l2 Y,  Z_Q = P^-1 W,  Z_K = R^-1 B_K.
+//   compress (K2c, per token, critical path):
+//       y_q = q Z_Q^T = m P^-1 (m = q W^T),  y_k = k Z_K^T = k_hat0 (decode.py:79-81),
+//       then the alternation through the closed form of the rank-1-updated
+//       systems  x (S + l1 v^T v) = b + l1 qk v
+//           =>   x = y + u * l1 (qk - y.v) / (1 + l1 v.u),   u = v S^-1,
+//       the exact line-search B update and the appends.
+// Algebraically this is the reference's computation; the Gauss-Jordan sweep
+// (no pivoting) succeeds exactly when the matrix is numerically SPD, i.e.
+// when the reference's Cholesky does.  If P or R is not SPD, K2c solves each
+// full system directly with the reference's jitter retry (linalg.py:80-91).
 #include <algorithm>
 
 #include "common.cuh"
@@ -31,7 +35,7 @@
 namespace lrqk {
 
 constexpr int kCompressThreads = 256;
-constexpr int kMaxElems = 16;  // GJ elements per thread: r^2 / 256 for r <= 64
+constexpr int kSub = 64;  // rows staged per sub-chunk in the prepare reduction
 
 struct CompressArgs {
     lrqk_layer_t L;
@@ -39,113 +43,124 @@ struct CompressArgs {
     int update_b;
 };
 
-// Per-head prep area inside red_scratch, after the chunk partials.
-struct PrepLayout {
-    int RQ, Rinv, bq, bk, yk, misc, total;
+// Per-head precompute ("pre" buffer) written by K2p, read by K2c.
+struct PreLayout {
+    int Pinv, Rinv, P, R, ZQ, ZK, W, flags, total;
 };
-__host__ __device__ inline PrepLayout prep_layout(int R) {
-    PrepLayout p;
+__host__ __device__ inline PreLayout pre_layout(int R, int d) {
+    PreLayout p;
     int o = 0;
-    p.RQ = o; o += R * R;
+    p.Pinv = o; o += R * R;
     p.Rinv = o; o += R * R;
-    p.bq = o; o += R;
-    p.bk = o; o += R;
-    p.yk = o; o += R;
-    p.misc = o; o += 4;  // qk, R-is-SPD flag, non-finite flag
-    p.total = o;
+    p.P = o; o += R * R;
+    p.R = o; o += R * R;
+    p.ZQ = o; o += R * d;
+    p.ZK = o; o += R * d;
+    p.W = o; o += R * d;
+    p.flags = o; o += 4;   // okP, okR
+    p.total = (o + 3) & ~3;
     return p;
 }
-__host__ __device__ inline size_t red_head_floats(int R, int nchunks) {
-    return (size_t)nchunks * (R * R + R) + prep_layout(R).total;
+// Per-head reduction scratch of K2p: chunk partials [Y (R*d) | G (R*R)] + the
+// prep block's B_Q B_Q^T.
+__host__ __device__ inline size_t red_head_floats(int R, int d, int nchunks) {
+    return (size_t)nchunks * (R * d + R * R) + R * R;
 }
 
 // ---------------------------------------------------------------------------
-// An n x n matrix (n <= 64) spread over the block's registers: slot s of a
-// thread holds element e = tid + s*blockDim.x (row-major); its (row, col) is
-// decoded once into `ij` (-1 marks an unused slot).
-// Gauss-Jordan inversion in place: row k and column k travel through
-// double-buffered shared vectors, so each pivot costs one barrier.  inverse()
-// returns false (uniformly) if a pivot is not > 0, i.e. exactly when the
-// matrix is not numerically SPD.
+// Block-wide Gauss-Jordan inverse of an R x R SPD matrix in shared memory
+// (R = rank_stride, a power of two; rows/columns beyond the true rank hold
+// the identity, which leaves the leading block's inverse and its SPD-ness
+// unchanged).  Thread t owns E consecutive elements of one row; the matrix
+// ping-pongs between b0 and b1 so each pivot costs a single barrier.  No
+// pivoting: every pivot is > 0 exactly when the matrix is numerically SPD,
+// i.e. when the reference's Cholesky succeeds (linalg.py:81).  Returns false
+// (block-uniformly) otherwise.  R is even, so the inverse ends up in b0.
 // ---------------------------------------------------------------------------
-struct RegMat {
-    float a[kMaxElems];
-    int ij[kMaxElems];  // (i << 8) | j, or -1
-
-    __device__ void init(int n) {
+template <int E>
+__device__ bool block_gj_t(float *M, int R, int ld, float *s_rc) {
+    const int tid = threadIdx.x;
+    const int e0 = tid * E;
+    const bool act = e0 < R * R;
+    const int i = act ? e0 / R : 0, c0 = act ? e0 - (e0 / R) * R : 0;
+    float own[E];
 #pragma unroll
-        for (int s = 0; s < kMaxElems; ++s) {
-            const int e = threadIdx.x + s * blockDim.x;
-            ij[s] = e < n * n ? (((e / n) << 8) | (e % n)) : -1;
-        }
-    }
-    __device__ void load(const float *M, int ld, float diag_add = 0.f) {
+    for (int e = 0; e < E; ++e) own[e] = act ? M[i * ld + c0 + e] : 0.f;
+    __syncthreads();
+    for (int k = 0; k < R; ++k) {
+        float *rowb = s_rc + (k & 1) * 128;
+        float *colb = rowb + 64;
+        if (act) {
+            if (i == k) {
 #pragma unroll
-        for (int s = 0; s < kMaxElems; ++s) {
-            if (ij[s] < 0) break;
-            const int i = ij[s] >> 8, j = ij[s] & 255;
-            a[s] = M[i * ld + j] + (i == j ? diag_add : 0.f);
-        }
-    }
-    __device__ void store(float *M, int ld) const {
-#pragma unroll
-        for (int s = 0; s < kMaxElems; ++s) {
-            if (ij[s] < 0) break;
-            M[(ij[s] >> 8) * ld + (ij[s] & 255)] = a[s];
-        }
-    }
-    __device__ bool inverse(int n, float *s_rc /* 256 floats */) {
-        for (int k = 0; k < n; ++k) {
-            float *row = s_rc + (k & 1) * 128;
-            float *col = row + 64;
-#pragma unroll
-            for (int s = 0; s < kMaxElems; ++s) {
-                if (ij[s] < 0) break;
-                const int i = ij[s] >> 8, j = ij[s] & 255;
-                if (i == k) row[j] = a[s];
-                if (j == k) col[i] = a[s];
+                for (int e = 0; e < E; ++e) rowb[c0 + e] = own[e];
             }
-            __syncthreads();
-            const float p = row[k];
-            if (!(p > 0.f) || !isfinite(p)) return false;
-            const float ip = 1.f / p;
 #pragma unroll
-            for (int s = 0; s < kMaxElems; ++s) {
-                if (ij[s] < 0) break;
-                const int i = ij[s] >> 8, j = ij[s] & 255;
-                if (i == k && j == k) a[s] = ip;
-                else if (i == k) a[s] *= ip;
-                else if (j == k) a[s] = -a[s] * ip;
-                else a[s] = fmaf(-col[i] * ip, row[j], a[s]);
-            }
+            for (int e = 0; e < E; ++e)
+                if (c0 + e == k) colb[i] = own[e];
         }
         __syncthreads();
-        return true;
+        const float p = rowb[k];
+        if (!(p > 0.f) || !isfinite(p)) return false;  // block-uniform
+        if (act) {
+            const float ip = __frcp_rn(p);
+            const float f = colb[i] * ip;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int j = c0 + e;
+                const float piv = rowb[j];
+                if (i == k) own[e] = (j == k) ? ip : own[e] * ip;
+                else own[e] = (j == k) ? -f : fmaf(-f, piv, own[e]);
+            }
+        }
     }
-};
+    if (act) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) M[i * ld + c0 + e] = own[e];
+    }
+    __syncthreads();
+    return true;
+}
 
-// Solve x M = rhs directly (M SPD n x n, row stride ld) with the reference's
-// single jitter retry.  Returns 0 ok, 1 ok after jitter, 2 failed.
-__device__ int solve_spd_direct(const float *M, int n, int ld, const float *rhs, float *x, float *work,
-                                float *s_rc) {
-    RegMat m;
-    m.init(n);
+// In-place inverse of the padded R x R matrix in M (row stride ld); on
+// failure M is left in an undefined state.
+__device__ bool block_gj(float *M, int R, int ld, float *s_rc) {
+    const int nn = R * R;
+    if (nn >= 16 * kCompressThreads) return block_gj_t<16>(M, R, ld, s_rc);
+    if (nn >= 4 * kCompressThreads) return block_gj_t<4>(M, R, ld, s_rc);
+    return block_gj_t<1>(M, R, ld, s_rc);
+}
+
+// Fill b0 with M (r x r, row stride ldm) + jit on the diagonal, padded with
+// the identity to R x R (stride ld).  Whole block; ends with a barrier.
+__device__ void fill_padded(float *b0, const float *M, int ldm, int r, int R, int ld, float jit) {
+    for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+        const int i = e / R, j = e - i * R;
+        float v;
+        if (i < r && j < r) v = M[i * ldm + j] + (i == j ? jit : 0.f);
+        else v = (i == j) ? 1.f : 0.f;
+        b0[i * ld + j] = v;
+    }
+    __syncthreads();
+}
+
+// Solve x M = rhs directly (M SPD r x r) with the reference's single jitter
+// retry (linalg.py:80-91).  Returns 0 ok, 1 ok after jitter, 2 failed.
+__device__ int solve_spd_direct(const float *M, int ldm, int r, int R, int ld, const float *rhs, float *x,
+                                float *b0, float *s_rc) {
     for (int attempt = 0; attempt < 2; ++attempt) {
         float jit = 0.f;
         if (attempt == 1) {
             float tr = 0.f, dmax = 0.f;
-            for (int i = 0; i < n; ++i) { tr += M[i * ld + i]; dmax = fmaxf(dmax, fabsf(M[i * ld + i])); }
-            // 1e-10 (tr/n + 1) as the reference, floored at fp32 resolution
-            jit = fmaxf(1e-10f * (tr / n + 1.f), dmax * 1.2e-7f);
+            for (int i = 0; i < r; ++i) { tr += M[i * ldm + i]; dmax = fmaxf(dmax, fabsf(M[i * ldm + i])); }
+            // 1e-10 (tr/r + 1) as the reference, floored at fp32 resolution
+            jit = fmaxf(1e-10f * (tr / r + 1.f), dmax * 1.2e-7f);
         }
-        m.load(M, ld, jit);
-        __syncthreads();
-        if (m.inverse(n, s_rc)) {
-            m.store(work, n);
-            __syncthreads();
-            for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        fill_padded(b0, M, ldm, r, R, ld, jit);
+        if (block_gj(b0, R, ld, s_rc)) {
+            for (int j = threadIdx.x; j < r; j += blockDim.x) {
                 float acc = 0.f;
-                for (int i = 0; i < n; ++i) acc = fmaf(rhs[i], work[i * n + j], acc);
+                for (int i = 0; i < r; ++i) acc = fmaf(rhs[i], b0[i * ld + j], acc);
                 x[j] = acc;
             }
             __syncthreads();
@@ -153,6 +168,30 @@ __device__ int solve_spd_direct(const float *M, int n, int ld, const float *rhs,
         }
     }
     return 2;
+}
+
+// Stage a [rows][d] fp32 matrix from global into shared (row stride ldx,
+// d and ldx multiples of 4) with all loads of a thread issued together.
+__device__ void stage_rows_f32(float *dst, int ldx, const float *src, int rows, int d) {
+    const int n4 = rows * d / 4;
+    const float4 *s4 = reinterpret_cast<const float4 *>(src);
+    constexpr int U = 8;
+    for (int base = threadIdx.x; base < n4; base += blockDim.x * U) {
+        float4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = base + u * blockDim.x;
+            if (e < n4) v[u] = __ldcg(s4 + e);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = base + u * blockDim.x;
+            if (e < n4) {
+                const int p = (e * 4) / d, i = e * 4 - p * d;
+                *reinterpret_cast<float4 *>(dst + p * ldx + i) = v[u];
+            }
+        }
+    }
 }
 
 // y[j] = sum_i v[i] * S[i*ld + j]   (one warp, n <= 64)
@@ -225,336 +264,421 @@ __device__ void gram_rows(const float *X, int r, int d, int ldx, float *out, int
 }
 
 // ---------------------------------------------------------------------------
-// reduce blocks: partial G_res (upper 4x4 tiles) and m_res of kRedRows rows
+// K2p: compress_prepare
 // ---------------------------------------------------------------------------
-template <typename T, int LPR, int PPL>
-__device__ void reduce_chunk(const lrqk_layer_t &L, const T *qrow, const T *kres_base, const T *proxy, bool host,
-                             int bh, int row0, int nrow, float *part_out, float *smem) {
+template <typename T>
+__global__ void __launch_bounds__(kCompressThreads, 2)
+prepare_kernel(const lrqk_layer_t L) {
+    extern __shared__ __align__(16) float smem[];
+    __shared__ int s_flag;
+    __shared__ float s_rc[256];
+    const int bh = blockIdx.y;
+    const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
+    const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int nchunks = gridDim.x - 1;
+    const int n_prev = L.res_cnt[bh];
+    const bool host = L.policy == LRQK_SLOW_HOST;
+    const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+    const T *proxy = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
+    const T *kbase = host ? reinterpret_cast<const T *>(L.slot_k) + (size_t)bh * L.n_slots * d
+                          : reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
+    float *hs = L.red_scratch + (size_t)bh * red_head_floats(R, d, nchunks);
+    float *pre = L.pre + (size_t)bh * pre_layout(R, d).total;
+    const PreLayout PL = pre_layout(R, d);
+    const float *BQg = L.B_Q + (size_t)bh * R * d;
+    const float *BKg = L.B_K + (size_t)bh * R * d;
+    const int ldB = d + 4, ldM = R + 4;
     constexpr int N = Pack<T>::N;
-    constexpr int RPW = 32 / LPR;
-    constexpr int NW = kCompressThreads / 32;
-    constexpr int STEPS = kRedRows / (NW * RPW);
-    constexpr int SR = STEPS < 8 ? STEPS : 8;  // rows in flight per lane group
-    const int d = L.dim_stride, R = L.rank_stride;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int sub = lane / LPR, sl = lane - sub * LPR;
-    const int ldA = R + 1;
-    float *sq = smem;                        // [d]
-    float *sS = sq + d;                      // [kRedRows]
-    float *sA = sS + kRedRows;               // [kRedRows][R+1]
-    int *sIdx = reinterpret_cast<int *>(sA + kRedRows * ldA);  // gather row (slot or index)
-    int *sPx = sIdx + kRedRows;              // proxy row (index)
-    float *sRed = reinterpret_cast<float *>(sPx + kRedRows);
-    for (int i = tid; i < d; i += blockDim.x) sq[i] = to_float<T>(qrow[i]);
-    const int *ridx = L.res_idx + (size_t)bh * L.s_cap + row0;
-    const int *rslot = L.res_slot + (size_t)bh * L.s_cap + row0;
-    for (int j = tid; j < nrow; j += blockDim.x) {
-        const int x = ridx[j];
-        sPx[j] = x;
-        sIdx[j] = host ? rslot[j] : x;
-    }
-    __syncthreads();
-    // A_res rows: issue the loads first, consume after the K dots
-    const int apacks = R / N;
-    constexpr int AU = 4;
-    uint4 ax[AU];
-    const int total_a = nrow * apacks;
+
+    if ((int)blockIdx.x < nchunks) {
+        // ---- reduce: Y = A^T K and G = A^T A over this chunk of Omega ------
+        const int row0 = blockIdx.x * kRedRows;
+        const int nrow = max(0, min(kRedRows, n_prev - row0));
+        const int ldA = R + 1;
+        float *sK = smem;                    // [kSub][ldB]
+        float *sA = sK + kSub * ldB;         // [kSub][ldA]
+        float *sRed = sA + kSub * ldA;       // gram groups
+        const int *ridx = L.res_idx + (size_t)bh * L.s_cap + row0;
+        const int *rslot = L.res_slot + (size_t)bh * L.s_cap + row0;
+        // Y tiles (4 p x 4 i) owned by this thread
+        const int nYt = (R / 4) * (d / 4);
+        float yacc[4][16];
 #pragma unroll
-    for (int u = 0; u < AU; ++u) {
-        const int e = tid + u * kCompressThreads;
-        if (e < total_a) {
-            const int j = e / apacks, p = e - j * apacks;
-            ax[u] = *reinterpret_cast<const uint4 *>(proxy + proxy_pack_offset(sPx[j], p, apacks) * N);
-        }
-    }
-    // K_res rows: q . K_res[j]
-    for (int s0 = 0; s0 < STEPS; s0 += SR) {
-        uint4 kx[SR][PPL];
+        for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int s = 0; s < SR; ++s) {
-            const int j = ((s0 + s) * NW + warp) * RPW + sub;
-            if (j < nrow) {
-                const T *kr = kres_base + (size_t)sIdx[j] * d;
+            for (int e = 0; e < 16; ++e) yacc[a][e] = 0.f;
+        const int RB = R / 4, NP = RB * (RB + 1) / 2;
+        const int NG = max(1, kCompressThreads / NP);
+        float gacc[16];
 #pragma unroll
-                for (int pp = 0; pp < PPL; ++pp)
-                    kx[s][pp] = *reinterpret_cast<const uint4 *>(kr + (sl + pp * LPR) * N);
-            } else {
+        for (int e = 0; e < 16; ++e) gacc[e] = 0.f;
+        for (int s0 = 0; s0 < nrow; s0 += kSub) {
+            const int ns = min(kSub, nrow - s0);
+            __syncthreads();
+            // stage K rows and A rows (all loads of a thread issued together)
+            const int kp = d / N, ap = R / N;
+            const int tot = ns * (kp + ap);
+            constexpr int U = 8;
+            for (int base = tid; base < tot; base += kCompressThreads * U) {
+                uint4 v[U];
+                int dst[U];
 #pragma unroll
-                for (int pp = 0; pp < PPL; ++pp) kx[s][pp] = make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < U; ++u) {
+                    const int e = base + u * kCompressThreads;
+                    dst[u] = -1;
+                    if (e < tot) {
+                        if (e < ns * kp) {
+                            const int j = e / kp, pk = e - j * kp;
+                            const int src = host ? rslot[s0 + j] : ridx[s0 + j];
+                            v[u] = *reinterpret_cast<const uint4 *>(kbase + (size_t)src * d + pk * N);
+                            dst[u] = j * ldB + pk * N;
+                        } else {
+                            const int e2 = e - ns * kp;
+                            const int j = e2 / ap, pk = e2 - j * ap;
+                            v[u] = *reinterpret_cast<const uint4 *>(proxy + proxy_pack_offset(ridx[s0 + j], pk, ap) * N);
+                            dst[u] = (1 << 30) | (j * ldA + pk * N);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (dst[u] < 0) continue;
+                    float x[N];
+                    unpack16<T>(v[u], x);
+                    float *o = (dst[u] & (1 << 30)) ? sA + (dst[u] & ~(1 << 30)) : sK + dst[u];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) o[i] = x[i];
+                }
+            }
+            __syncthreads();
+            // Y += A^T K
+            for (int a = 0; a < 4; ++a) {
+                const int tI = tid + a * kCompressThreads;
+                if (tI >= nYt) break;
+                const int p0 = (tI / (d / 4)) * 4, i0 = (tI % (d / 4)) * 4;
+                for (int j = 0; j < ns; ++j) {
+                    const float4 kv = *reinterpret_cast<const float4 *>(sK + j * ldB + i0);
+                    const float ks[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const float ap2 = sA[j * ldA + p0 + u];
+#pragma unroll
+                        for (int w2 = 0; w2 < 4; ++w2) yacc[a][u * 4 + w2] = fmaf(ap2, ks[w2], yacc[a][u * 4 + w2]);
+                    }
+                }
+            }
+            // G += A^T A (upper 4x4 tiles, row groups)
+            if (tid < NP * NG) {
+                const int pair = tid % NP, grp = tid / NP;
+                int pb = 0, rem = pair;
+                while (rem >= RB - pb) { rem -= RB - pb; ++pb; }
+                const int qb = pb + rem;
+                for (int j = grp; j < ns; j += NG) {
+                    const float *arow = sA + j * ldA;
+                    float a4[4], b4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { a4[u] = arow[pb * 4 + u]; b4[u] = arow[qb * 4 + u]; }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int w2 = 0; w2 < 4; ++w2) gacc[u * 4 + w2] = fmaf(a4[u], b4[w2], gacc[u * 4 + w2]);
+                }
             }
         }
-#pragma unroll
-        for (int s = 0; s < SR; ++s) {
-            const int j = ((s0 + s) * NW + warp) * RPW + sub;
-            float part = 0.f;
-#pragma unroll
-            for (int pp = 0; pp < PPL; ++pp) {
-                float x[N];
-                unpack16<T>(kx[s][pp], x);
-                const float *qq = sq + (sl + pp * LPR) * N;
-#pragma unroll
-                for (int e = 0; e < N; ++e) part = fmaf(x[e], qq[e], part);
-            }
-            part = group_sum<LPR>(part);
-            if (j < nrow && sl == 0) sS[j] = part;
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < AU; ++u) {
-        const int e = tid + u * kCompressThreads;
-        if (e < total_a) {
-            const int j = e / apacks, p = e - j * apacks;
-            float x[N];
-            unpack16<T>(ax[u], x);
-#pragma unroll
-            for (int i = 0; i < N; ++i) sA[j * ldA + p * N + i] = x[i];
-        }
-    }
-    for (int e = tid + AU * kCompressThreads; e < total_a; e += kCompressThreads) {
-        const int j = e / apacks, p = e - j * apacks;
-        float x[N];
-        Pack<T>::load(proxy + proxy_pack_offset(sPx[j], p, apacks) * N, x);
-#pragma unroll
-        for (int i = 0; i < N; ++i) sA[j * ldA + p * N + i] = x[i];
-    }
-    __syncthreads();
-    // upper-triangular 4x4 tiles of G over the chunk's rows
-    const int RB = R / 4;
-    const int NP = RB * (RB + 1) / 2;
-    const int NG = max(1, kCompressThreads / NP);
-    if (tid < NP * NG) {
-        const int pair = tid % NP, grp = tid / NP;
-        int pb = 0, rem = pair;
-        while (rem >= RB - pb) { rem -= RB - pb; ++pb; }
-        const int qb = pb + rem;
-        float acc[16] = {};
-        for (int j = grp; j < nrow; j += NG) {
-            const float *a = sA + j * ldA;
-            float ap[4], aq[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { ap[u] = a[pb * 4 + u]; aq[u] = a[qb * 4 + u]; }
+        float *part = hs + (size_t)blockIdx.x * (R * d + R * R);
+        for (int a = 0; a < 4; ++a) {
+            const int tI = tid + a * kCompressThreads;
+            if (tI >= nYt) break;
+            const int p0 = (tI / (d / 4)) * 4, i0 = (tI % (d / 4)) * 4;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int w2 = 0; w2 < 4; ++w2) acc[u * 4 + w2] = fmaf(ap[u], aq[w2], acc[u * 4 + w2]);
+                *reinterpret_cast<float4 *>(part + (p0 + u) * d + i0) =
+                    make_float4(yacc[a][u * 4], yacc[a][u * 4 + 1], yacc[a][u * 4 + 2], yacc[a][u * 4 + 3]);
         }
+        __syncthreads();
+        if (tid < NP * NG) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e) sRed[(grp * NP + pair) * 16 + e] = acc[e];
+            for (int e = 0; e < 16; ++e) sRed[tid * 16 + e] = gacc[e];
+        }
+        __syncthreads();
+        for (int e = tid; e < NP * 16; e += kCompressThreads) {
+            float acc = 0.f;
+            for (int gI = 0; gI < NG; ++gI) acc += sRed[(gI * NP) * 16 + e];
+            const int pair = e / 16, uw = e - pair * 16;
+            int pb = 0, rem = pair;
+            while (rem >= RB - pb) { rem -= RB - pb; ++pb; }
+            const int qb = pb + rem;
+            part[R * d + (pb * 4 + uw / 4) * R + qb * 4 + (uw & 3)] = acc;  // tiles with pb <= qb
+        }
+    } else {
+        // ---- prep: R = B_K B_K^T, R^-1, Z_K = R^-1 B_K, B_Q B_Q^T -----------
+        float *sBQ = smem;                   // [R][ldB]
+        float *sBK = sBQ + R * ldB;          // [R][ldB]
+        float *b0 = sBK + R * ldB;           // [R][ldM]
+        float *tmp = b0 + R * ldM;           // gram scratch
+        stage_rows_f32(sBQ, ldB, BQg, R, d);
+        stage_rows_f32(sBK, ldB, BKg, R, d);
+        for (int e = tid; e < R * R; e += blockDim.x) {  // identity padding
+            const int i = e / R, j = e - i * R;
+            if (i >= r || j >= r) b0[i * ldM + j] = (i == j) ? 1.f : 0.f;
+        }
+        __syncthreads();
+        gram_rows(sBK, r, d, ldB, b0, ldM, tmp);                       // R (exactly symmetric)
+        gram_rows(sBQ, r, d, ldB, hs + (size_t)nchunks * (R * d + R * R), R, tmp);  // B_Q B_Q^T
+        for (int e = tid; e < R * R; e += blockDim.x) {
+            const int i = e / R, j = e - i * R;
+            pre[PL.R + e] = (i < r && j < r) ? b0[i * ldM + j] : 0.f;
+        }
+        __syncthreads();
+        const bool ok = block_gj(b0, R, ldM, s_rc);
+        if (ok) {
+            for (int e = tid; e < R * R; e += blockDim.x) {
+                const int i = e / R, j = e - i * R;
+                pre[PL.Rinv + e] = (i < r && j < r) ? b0[i * ldM + j] : 0.f;
+            }
+            // Z_K = R^-1 B_K  (r x d)
+            for (int e = tid; e < R * d; e += blockDim.x) {
+                const int p = e / d, i = e - p * d;
+                float acc = 0.f;
+                if (p < r)
+                    for (int q = 0; q < r; ++q) acc = fmaf(b0[p * ldM + q], sBK[q * ldB + i], acc);
+                pre[PL.ZK + e] = acc;
+            }
+        }
+        if (tid == 0) pre[PL.flags + 1] = ok ? 1.f : 0.f;
     }
-    for (int p = tid; p < R; p += kCompressThreads) {
-        float acc0 = 0.f, acc1 = 0.f;
-        int j = 0;
-        for (; j + 1 < nrow; j += 2) {
-            acc0 = fmaf(sS[j], sA[j * ldA + p], acc0);
-            acc1 = fmaf(sS[j + 1], sA[(j + 1) * ldA + p], acc1);
+    if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_PREPARE, gridDim.x, &s_flag)) return;
+
+    // ---- finish: P, P^-1, W, Z_Q ---------------------------------------------
+    float *sW = smem;                    // [R][ldB]   W = B_Q + l2 Y
+    float *b0 = sW + R * ldB;            // [R][ldM]
+    const float l2 = L.lambda_2;
+    const bool have_res = n_prev > 0;
+    {
+        const float4 *bq4 = reinterpret_cast<const float4 *>(BQg);
+        const int n4 = R * d / 4;
+        for (int e4 = tid; e4 < n4; e4 += blockDim.x) {
+            float4 acc = __ldcg(bq4 + e4);
+            if (have_res) {
+                float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4 *>(hs + (size_t)ch * (R * d + R * R)) + e4);
+                    y.x += v.x; y.y += v.y; y.z += v.z; y.w += v.w;
+                }
+                acc.x = fmaf(l2, y.x, acc.x); acc.y = fmaf(l2, y.y, acc.y);
+                acc.z = fmaf(l2, y.z, acc.z); acc.w = fmaf(l2, y.w, acc.w);
+            }
+            const int p = (e4 * 4) / d, i = e4 * 4 - p * d;
+            *reinterpret_cast<float4 *>(sW + p * ldB + i) = acc;
+            *reinterpret_cast<float4 *>(pre + PL.W + e4 * 4) = acc;
         }
-        if (j < nrow) acc0 = fmaf(sS[j], sA[j * ldA + p], acc0);
-        part_out[R * R + p] = acc0 + acc1;
+        const float *RQ = hs + (size_t)nchunks * (R * d + R * R);
+        for (int e = tid; e < R * R; e += blockDim.x) {
+            const int pi = e / R, qi = e - pi * R;
+            float v;
+            if (pi < r && qi < r) {
+                const int a0 = min(pi, qi), c0 = max(pi, qi);
+                float gs = 0.f;
+                if (have_res)
+                    for (int ch = 0; ch < nchunks; ++ch)
+                        gs += __ldcg(hs + (size_t)ch * (R * d + R * R) + R * d + a0 * R + c0);
+                v = __ldcg(RQ + pi * R + qi) + (have_res ? l2 * gs : 0.f);
+                pre[PL.P + e] = v;
+            } else {
+                v = (pi == qi) ? 1.f : 0.f;
+                pre[PL.P + e] = 0.f;
+            }
+            b0[pi * ldM + qi] = v;
+        }
     }
     __syncthreads();
-    for (int e = tid; e < NP * 16; e += kCompressThreads) {
-        float acc = 0.f;
-        for (int gI = 0; gI < NG; ++gI) acc += sRed[(gI * NP) * 16 + e];
-        const int pair = e / 16, uw = e - pair * 16;
-        int pb = 0, rem = pair;
-        while (rem >= RB - pb) { rem -= RB - pb; ++pb; }
-        const int qb = pb + rem;
-        part_out[(pb * 4 + uw / 4) * R + qb * 4 + (uw & 3)] = acc;  // tiles with pb <= qb
+    const bool okP = block_gj(b0, R, ldM, s_rc);
+    if (okP) {
+        for (int e = tid; e < R * R; e += blockDim.x) {
+            const int i = e / R, j = e - i * R;
+            pre[PL.Pinv + e] = (i < r && j < r) ? b0[i * ldM + j] : 0.f;
+        }
+        for (int e = tid; e < R * d; e += blockDim.x) {  // Z_Q = P^-1 W
+            const int p = e / d, i = e - p * d;
+            float acc = 0.f;
+            if (p < r)
+                for (int q = 0; q < r; ++q) acc = fmaf(b0[p * ldM + q], sW[q * ldB + i], acc);
+            pre[PL.ZQ + e] = acc;
+        }
     }
+    if (tid == 0) pre[PL.flags + 0] = okP ? 1.f : 0.f;
+    (void)warp;
 }
 
 // ---------------------------------------------------------------------------
-// the kernel
+// K2c: compress (one block per head)
 // ---------------------------------------------------------------------------
-template <typename T, int LPR, int PPL>
+template <typename T>
 __global__ void __launch_bounds__(kCompressThreads)
 compress_kernel(const CompressArgs args) {
     const lrqk_layer_t &L = args.L;
     extern __shared__ __align__(16) float smem[];
-    __shared__ int s_flag;
-    __shared__ float s_rc[256];
     __shared__ float s_scalar[8];
     __shared__ int s_bad;
-
-    const int bh = blockIdx.y;
+    __shared__ float s_rc[256];
+    const int bh = blockIdx.x;
     const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
-    const int G = L.n_q_heads / L.n_kv_heads;
-    const int g = h / G;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
     const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int t = L.ctx_len[b];
     if (t >= L.t_max) {
-        if (blockIdx.x == 0 && tid == 0) set_status(L.status, LRQK_ST_CAPACITY);
+        if (tid == 0) set_status(L.status, LRQK_ST_CAPACITY);
         return;
     }
-    const int nchunks = gridDim.x - 1;
-    const int n_prev = L.res_cnt[bh];
+    trace(0);
+    const PreLayout PL = pre_layout(R, d);
+    const float *pre = L.pre + (size_t)bh * PL.total;
     const size_t head_rows = (size_t)bh * L.t_max;
     const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
-    const T *proxy = reinterpret_cast<const T *>(L.proxy) + head_rows * R;
-    const bool host = (L.policy == LRQK_SLOW_HOST);
-    const T *kres_base = host ? reinterpret_cast<const T *>(L.slot_k) + (size_t)bh * L.n_slots * d
-                              : reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
     const T *qrow = reinterpret_cast<const T *>(args.q) + (size_t)bh * d;
     const T *krow = reinterpret_cast<const T *>(args.k) + ((size_t)b * L.n_kv_heads + g) * d;
     const T *vrow = reinterpret_cast<const T *>(args.v) + ((size_t)b * L.n_kv_heads + g) * d;
-    float *hs = L.red_scratch + (size_t)bh * red_head_floats(R, nchunks);
-    const PrepLayout PL = prep_layout(R);
-    float *prep = hs + (size_t)nchunks * (R * R + R);
-    const int ldM = R + 1;
-
-    if ((int)blockIdx.x < nchunks) {
-        const int row0 = blockIdx.x * kRedRows;
-        const int nrow = max(0, min(kRedRows, n_prev - row0));
-        reduce_chunk<T, LPR, PPL>(L, qrow, kres_base, proxy, host, bh, row0, nrow,
-                                  hs + (size_t)blockIdx.x * (R * R + R), smem);
-    } else {
-        // ---------------- prep block: the Omega-independent algebra ---------
-        float *sBQ = smem;                   // [R][d+1]
-        float *sBK = sBQ + R * (d + 1);      // [R][d+1]
-        float *sR = sBK + R * (d + 1);       // [R][ldM]
-        float *vq = sR + R * ldM;            // [d]
-        float *vk = vq + d;                  // [d]
-        float *bk = vk + d;                  // [R]
-        float *tmp = bk + R;                 // gram scratch
-        const float *BQg = L.B_Q + (size_t)bh * R * d;
-        const float *BKg = L.B_K + (size_t)bh * R * d;
-        for (int e = tid; e < R * d; e += blockDim.x) {
-            const int p = e / d, i = e - p * d;
-            sBQ[p * (d + 1) + i] = BQg[e];
-            sBK[p * (d + 1) + i] = BKg[e];
-        }
-        if (tid == 0) s_bad = 0;
-        __syncthreads();
-        for (int i = tid; i < d; i += blockDim.x) {
-            vq[i] = to_float<T>(qrow[i]);
-            vk[i] = to_float<T>(krow[i]);
-            if (!isfinite(vq[i]) || !isfinite(vk[i]) || !isfinite(to_float<T>(vrow[i]))) s_bad = 1;
-        }
-        __syncthreads();
-        gram_rows(sBK, r, d, d + 1, sR, ldM, tmp);            // R = B_K B_K^T
-        gram_rows(sBQ, r, d, d + 1, prep + PL.RQ, R, tmp);    // B_Q B_Q^T
-        for (int o = tid; o < 2 * r + 1; o += blockDim.x) {    // q B_Q^T, k B_K^T, q.k
-            const float *x = o < r ? sBQ + o * (d + 1) : (o < 2 * r ? sBK + (o - r) * (d + 1) : vq);
-            const float *y = o < r ? vq : vk;
-            float a0 = 0.f, a1 = 0.f;
-            for (int i = 0; i < d; i += 2) {
-                a0 = fmaf(x[i], y[i], a0);
-                a1 = fmaf(x[i + 1], y[i + 1], a1);
-            }
-            const float s = a0 + a1;
-            if (o < r) prep[PL.bq + o] = s;
-            else if (o < 2 * r) { prep[PL.bk + o - r] = s; bk[o - r] = s; }
-            else prep[PL.misc + 0] = s;
-        }
-        __syncthreads();
-        RegMat m;
-        m.init(r);
-        m.load(sR, ldM);
-        const bool ok = m.inverse(r, s_rc);
-        if (ok) {
-            m.store(prep + PL.Rinv, R);
-            m.store(sR, ldM);
-        }
-        __syncthreads();
-        if (ok && warp == 0) warp_vecmat(bk, sR, r, ldM, prep + PL.yk);  // k_hat0
-        if (tid == 0) {
-            prep[PL.misc + 1] = ok ? 1.f : 0.f;
-            prep[PL.misc + 2] = s_bad ? 1.f : 0.f;
-        }
-    }
-    if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_COMPRESS, gridDim.x, &s_flag)) return;
-
-    // ================= finish (one block per head) ==========================
-    float *sP = smem;                    // [R][ldM]  P, then P^-1
-    float *sRi = sP + R * ldM;           // [R][ldM]  R^-1 (R in the fallback)
-    float *vq = sRi + R * ldM;           // [d]
+    const int ldB = d + 4, ldM = R + 4;
+    float *sBQ = smem;                   // [R][ldB]
+    float *sBK = sBQ + R * ldB;          // [R][ldB]
+    float *sZQ = sBK + R * ldB;          // [R][ldB]  Z_Q (or W in the fallback)
+    float *sZK = sZQ + R * ldB;          // [R][ldB]  Z_K
+    float *sPi = sZK + R * ldB;          // [R][ldM]  P^-1 (P in the fallback)
+    float *sRi = sPi + R * ldM;          // [R][ldM]  R^-1 (R in the fallback)
+    float *b0 = sRi + R * ldM;           // [R][ldM]  fallback scratch
+    float *sM = b0 + R * ldM;            // [R][ldM]  fallback system
+    float *vq = sM + R * ldM;            // [d]
     float *vk = vq + d;                  // [d]
-    float *bk = vk + d;                  // [R]
-    float *mres = bk + R;                // [R]
-    float *yq = mres + R;                // [R]
+    float *yq = vk + d;                  // [R]
     float *yk = yq + R;                  // [R]
     float *qh = yk + R;                  // [R]
     float *kh = qh + R;                  // [R]
     float *u = kh + R;                   // [R]
     float *prevc = u + R;                // [2R]
     float *resid = prevc + 2 * R;        // [2][d]
-    float *work = resid + 2 * d;         // [R*(R+1)] fallback
-    float *sM = work + R * (R + 1);      // [R][ldM] fallback system
-    const float l1 = L.lambda_1, l2 = L.lambda_2;
-    if (__ldcg(prep + PL.misc + 2) != 0.f) {  // ref: linalg.py:32-33 via as_row (session.py:94)
-        if (tid == 0) set_status(L.status, LRQK_ST_NONFINITE);
-        return;
+    const bool okP = __ldcg(pre + PL.flags + 0) != 0.f;
+    const bool okR = __ldcg(pre + PL.flags + 1) != 0.f;
+    const bool fast = okP && okR;
+    // ---- stage: B_Q, B_K, Z_Q, Z_K (or W, P, R), q, k ----------------------
+    stage_rows_f32(sBQ, ldB, L.B_Q + (size_t)bh * R * d, R, d);
+    stage_rows_f32(sBK, ldB, L.B_K + (size_t)bh * R * d, R, d);
+    stage_rows_f32(sZQ, ldB, pre + (fast ? PL.ZQ : PL.W), R, d);
+    if (fast) stage_rows_f32(sZK, ldB, pre + PL.ZK, R, d);
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int i = e / R, j = e - i * R;
+        sPi[i * ldM + j] = __ldcg(pre + (fast ? PL.Pinv : PL.P) + e);
+        sRi[i * ldM + j] = __ldcg(pre + (fast ? PL.Rinv : PL.R) + e);
     }
-    const bool have_res = n_prev > 0;
-    const float qk = __ldcg(prep + PL.misc + 0);
-    const bool okR = __ldcg(prep + PL.misc + 1) != 0.f;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
     for (int i = tid; i < d; i += blockDim.x) {
         vq[i] = to_float<T>(qrow[i]);
         vk[i] = to_float<T>(krow[i]);
+        if (!isfinite(vq[i]) || !isfinite(vk[i]) || !isfinite(to_float<T>(vrow[i]))) s_bad = 1;
     }
-    // P = B_Q B_Q^T + l2 G_res ; m = q B_Q^T + l2 m_res
-    for (int e = tid; e < r * r; e += blockDim.x) {
-        const int pi = e / r, qi = e - pi * r;
-        const int a0 = min(pi, qi), c0 = max(pi, qi);
-        float g0 = 0.f, g1 = 0.f;
-        if (have_res) {
-            int ch = 0;
-            for (; ch + 1 < nchunks; ch += 2) {
-                g0 += __ldcg(hs + (size_t)ch * (R * R + R) + a0 * R + c0);
-                g1 += __ldcg(hs + (size_t)(ch + 1) * (R * R + R) + a0 * R + c0);
-            }
-            if (ch < nchunks) g0 += __ldcg(hs + (size_t)ch * (R * R + R) + a0 * R + c0);
-        }
-        sP[pi * ldM + qi] = __ldcg(prep + PL.RQ + pi * R + qi) + (have_res ? l2 * (g0 + g1) : 0.f);
-    }
-    for (int p = tid; p < r; p += blockDim.x) {
-        float m0 = 0.f, m1 = 0.f;
-        if (have_res) {
-            int ch = 0;
-            for (; ch + 1 < nchunks; ch += 2) {
-                m0 += __ldcg(hs + (size_t)ch * (R * R + R) + R * R + p);
-                m1 += __ldcg(hs + (size_t)(ch + 1) * (R * R + R) + R * R + p);
-            }
-            if (ch < nchunks) m0 += __ldcg(hs + (size_t)ch * (R * R + R) + R * R + p);
-        }
-        mres[p] = __ldcg(prep + PL.bq + p) + (have_res ? l2 * (m0 + m1) : 0.f);
-        bk[p] = __ldcg(prep + PL.bk + p);
-        yk[p] = okR ? __ldcg(prep + PL.yk + p) : 0.f;
-    }
-    if (okR)
-        for (int e = tid; e < r * r; e += blockDim.x) {
-            const int pi = e / r, qi = e - pi * r;
-            sRi[pi * ldM + qi] = __ldcg(prep + PL.Rinv + pi * R + qi);
-        }
     __syncthreads();
-    bool okP = false;
-    if (okR) {
-        RegMat m;
-        m.init(r);
-        m.load(sP, ldM);
-        okP = m.inverse(r, s_rc);
-        if (okP) m.store(sP, ldM);  // on failure sP still holds P
-        __syncthreads();
+    if (s_bad) {  // ref: linalg.py:32-33 via as_row (session.py:94)
+        if (tid == 0) set_status(L.status, LRQK_ST_NONFINITE);
+        return;
     }
+    trace(1);
+    // ---- y_q = Z_Q q (or m = W q), y_k = Z_K k (or k B_K^T), qk -------------
+    // one 8-lane group per output row; 32 groups per block
+    {
+        const int grp = tid >> 3, gl = tid & 7;
+        // trip count is uniform across each warp (the shuffles below need all lanes)
+        for (int o0 = 0; o0 < 2 * r + 1; o0 += kCompressThreads / 8) {
+            const int o = o0 + grp;
+            const bool valid = o < 2 * r + 1;
+            float acc = 0.f;
+            if (valid) {
+                const float *x = o < r ? sZQ + o * ldB : (o < 2 * r ? (fast ? sZK : sBK) + (o - r) * ldB : vq);
+                const float *y = o < r ? vq : vk;
+                for (int i = gl * 4; i < d; i += 32) {
+                    const float4 xv = *reinterpret_cast<const float4 *>(x + i);
+                    const float4 yv = *reinterpret_cast<const float4 *>(y + i);
+                    acc = fmaf(xv.x, yv.x, fmaf(xv.y, yv.y, fmaf(xv.z, yv.z, fmaf(xv.w, yv.w, acc))));
+                }
+            }
+            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            if (valid && gl == 0) {
+                if (o < r) yq[o] = acc;
+                else if (o < 2 * r) yk[o - r] = acc;
+                else s_scalar[0] = acc;
+            }
+        }
+    }
+    __syncthreads();
+    trace(2);
+    const float qk = s_scalar[0];
+    const float l1 = L.lambda_1;
     const int max_iter = L.max_iter;
-    if (okP) {
+    if (fast && r <= 32) {
+        // the alternation, one warp: lane j keeps column j of P^-1 and R^-1 in
+        // registers, vectors are distributed one component per lane
         if (warp == 0) {
-            warp_vecmat(mres, sP, r, ldM, yq);     // y_q = m P^-1
+            float pc[32], rc2[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                pc[i] = (i < r && lane < r) ? sPi[i * ldM + lane] : 0.f;
+                rc2[i] = (i < r && lane < r) ? sRi[i * ldM + lane] : 0.f;
+            }
+            const float yqv = lane < r ? yq[lane] : 0.f;
+            const float ykv = lane < r ? yk[lane] : 0.f;
+            float khv = ykv, qhv = 0.f, pq = 0.f, pk = 0.f;
+            for (int it = 0; it < max_iter; ++it) {
+                float uv = 0.f;                      // u = k_hat P^-1
+#pragma unroll
+                for (int i = 0; i < 32; ++i) uv = fmaf(__shfl_sync(0xffffffffu, khv, i), pc[i], uv);
+                float alpha = yqv * khv, c = uv * khv;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    alpha += __shfl_xor_sync(0xffffffffu, alpha, o);
+                    c += __shfl_xor_sync(0xffffffffu, c, o);
+                }
+                qhv = fmaf(l1 * (qk - alpha) / (1.f + l1 * c), uv, yqv);   // decode.py:84-108
+                float wv = 0.f;                      // w = q_hat R^-1
+#pragma unroll
+                for (int i = 0; i < 32; ++i) wv = fmaf(__shfl_sync(0xffffffffu, qhv, i), rc2[i], wv);
+                float beta = ykv * qhv, e2 = wv * qhv;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    beta += __shfl_xor_sync(0xffffffffu, beta, o);
+                    e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+                }
+                khv = fmaf(l1 * (qk - beta) / (1.f + l1 * e2), wv, ykv);   // decode.py:111-119
+                const float dq = qhv - pq, dk = khv - pk;
+                const float dsum = warp_sum(dq * dq + dk * dk);
+                pq = qhv;
+                pk = khv;
+                if (it > 0 && dsum / (2.f * r) <= L.tol) break;            // decode.py:143-146
+            }
+            qh[lane] = lane < r ? qhv : 0.f;
+            kh[lane] = lane < r ? khv : 0.f;
+            for (int i = 32 + lane; i < R; i += 32) { qh[i] = 0.f; kh[i] = 0.f; }
+        }
+        __syncthreads();
+    } else if (fast) {
+        if (warp == 0) {
             for (int i = lane; i < r; i += 32) kh[i] = yk[i];
             __syncwarp();
             for (int it = 0; it < max_iter; ++it) {
-                warp_vecmat(kh, sP, r, ldM, u);    // q_hat (decode.py:84-108)
+                warp_vecmat(kh, sPi, r, ldM, u);
                 const float alpha = warp_dot(yq, kh, r), c = warp_dot(u, kh, r);
                 const float coef = l1 * (qk - alpha) / (1.f + l1 * c);
                 for (int i = lane; i < r; i += 32) qh[i] = fmaf(coef, u[i], yq[i]);
                 __syncwarp();
-                warp_vecmat(qh, sRi, r, ldM, u);   // k_hat (decode.py:111-119)
+                warp_vecmat(qh, sRi, r, ldM, u);
                 const float beta = warp_dot(yk, qh, r), e2 = warp_dot(u, qh, r);
                 const float coef2 = l1 * (qk - beta) / (1.f + l1 * e2);
                 for (int i = lane; i < r; i += 32) kh[i] = fmaf(coef2, u[i], yk[i]);
                 __syncwarp();
-                float dsum = 0.f;                  // stop rule (decode.py:143-146)
+                float dsum = 0.f;
                 for (int i = lane; i < r; i += 32) {
                     const float dq = qh[i] - prevc[i], dk = kh[i] - prevc[r + i];
                     dsum += dq * dq + dk * dk;
@@ -565,45 +689,36 @@ compress_kernel(const CompressArgs args) {
                 __syncwarp();
                 if (stop) break;
             }
+            for (int i = r + lane; i < R; i += 32) { qh[i] = 0.f; kh[i] = 0.f; }
         }
         __syncthreads();
     } else {
         // ---- fallback: the reference's direct solves with jitter retry -----
-        const float *BKg = L.B_K + (size_t)bh * R * d;
-        for (int o = warp; o < r * r; o += nwarps) {  // R = B_K B_K^T again
-            const int pi = o / r, qi = o - pi * r;
-            float acc = 0.f;
-            for (int i = lane; i < d; i += 32) acc = fmaf(BKg[pi * d + i], BKg[qi * d + i], acc);
-            acc = warp_sum(acc);
-            if (lane == 0) sRi[pi * ldM + qi] = acc;
-        }
-        __syncthreads();
+        // sZQ holds W, so yq = m = q W^T;  yk = k B_K^T;  sPi = P, sRi = R
         int jitter = 0;
-        int rc = solve_spd_direct(sRi, r, ldM, bk, kh, work, s_rc);  // k_hat0
+        int rc = solve_spd_direct(sRi, ldM, r, R, ldM, yk, kh, b0, s_rc);  // k_hat0
         if (rc == 2) { if (tid == 0) set_status(L.status, LRQK_ST_SOLVE_FAILED); return; }
         jitter |= rc;
         for (int it = 0; it < max_iter; ++it) {
-            __syncthreads();
             for (int e = tid; e < r * r; e += blockDim.x) {
                 const int pi = e / r, qi = e - pi * r;
-                sM[pi * ldM + qi] = sP[pi * ldM + qi] + l1 * kh[pi] * kh[qi];
+                sM[pi * ldM + qi] = sPi[pi * ldM + qi] + l1 * kh[pi] * kh[qi];
             }
-            for (int p = tid; p < r; p += blockDim.x) u[p] = mres[p] + l1 * qk * kh[p];
+            for (int p = tid; p < r; p += blockDim.x) u[p] = yq[p] + l1 * qk * kh[p];
             __syncthreads();
-            rc = solve_spd_direct(sM, r, ldM, u, qh, work, s_rc);
+            rc = solve_spd_direct(sM, ldM, r, R, ldM, u, qh, b0, s_rc);
             if (rc == 2) { if (tid == 0) set_status(L.status, LRQK_ST_SOLVE_FAILED); return; }
             jitter |= rc;
-            __syncthreads();
             for (int e = tid; e < r * r; e += blockDim.x) {
                 const int pi = e / r, qi = e - pi * r;
                 sM[pi * ldM + qi] = sRi[pi * ldM + qi] + l1 * qh[pi] * qh[qi];
             }
-            for (int p = tid; p < r; p += blockDim.x) u[p] = bk[p] + l1 * qk * qh[p];
+            for (int p = tid; p < r; p += blockDim.x) u[p] = yk[p] + l1 * qk * qh[p];
             __syncthreads();
-            rc = solve_spd_direct(sM, r, ldM, u, kh, work, s_rc);
+            // note: yk here is k B_K^T (the rhs), not k_hat0
+            rc = solve_spd_direct(sM, ldM, r, R, ldM, u, kh, b0, s_rc);
             if (rc == 2) { if (tid == 0) set_status(L.status, LRQK_ST_SOLVE_FAILED); return; }
             jitter |= rc;
-            __syncthreads();
             if (tid == 0) {
                 float dsum = 0.f;
                 for (int i = 0; i < r; ++i) {
@@ -616,23 +731,26 @@ compress_kernel(const CompressArgs args) {
             __syncthreads();
             if (s_scalar[1] != 0.f) break;
         }
+        for (int i = r + tid; i < R; i += blockDim.x) { qh[i] = 0.f; kh[i] = 0.f; }
         if (tid == 0) set_status(L.status, LRQK_ST_FALLBACK | (jitter ? LRQK_ST_JITTERED : 0u));
+        __syncthreads();
     }
-    __syncthreads();
-    for (int i = r + tid; i < R; i += blockDim.x) { qh[i] = 0.f; kh[i] = 0.f; }
-    __syncthreads();
+    trace(3);
 
     // ---------------- line-search B update (decode.py:150-184), both sides --
     // resid = x_hat B - x ; s = x_hat grad = |x_hat|^2 resid ; eta = (resid.s)/(s.s)
-    const float *BQg = L.B_Q + (size_t)bh * R * d;
-    const float *BKg = L.B_K + (size_t)bh * R * d;
     for (int w = tid; w < 2 * d; w += blockDim.x) {
         const int side = w / d, i = w - side * d;
         const float *xh = side ? kh : qh;
-        const float *Bm = side ? BKg : BQg;
-        float acc = 0.f;
-        for (int p = 0; p < r; ++p) acc = fmaf(xh[p], __ldcg(Bm + p * d + i), acc);
-        resid[w] = acc - (side ? vk[i] : vq[i]);
+        const float *Bm = side ? sBK : sBQ;
+        float a0 = 0.f, a1 = 0.f;
+        int p = 0;
+        for (; p + 1 < r; p += 2) {
+            a0 = fmaf(xh[p], Bm[p * ldB + i], a0);
+            a1 = fmaf(xh[p + 1], Bm[(p + 1) * ldB + i], a1);
+        }
+        if (p < r) a0 = fmaf(xh[p], Bm[p * ldB + i], a0);
+        resid[w] = a0 + a1 - (side ? vk[i] : vq[i]);
     }
     __syncthreads();
     if (warp < 2) {
@@ -655,16 +773,25 @@ compress_kernel(const CompressArgs args) {
     }
     __syncthreads();
     if (args.update_b) {
-        for (int w = tid; w < 2 * r * d; w += blockDim.x) {
-            const int side = w / (r * d), e = w - side * r * d;
+        const int n4 = r * d / 4;
+        for (int w = tid; w < 2 * n4; w += blockDim.x) {
+            const int side = w / n4, e4 = w - side * n4;
             const float eta = s_scalar[2 + side];
             if (eta == 0.f) continue;
-            const int p = e / d, i = e - p * d;
-            float *Bg = (side ? L.B_K : L.B_Q) + (size_t)bh * R * d;
+            const int p = (e4 * 4) / d, i = e4 * 4 - p * d;
+            const float *Bm = side ? sBK : sBQ;
             const float *xh = side ? kh : qh;
-            Bg[p * d + i] = __ldcg(Bg + p * d + i) - eta * (xh[p] * resid[side * d + i]);
+            const float c = eta * xh[p];
+            const float *rs = resid + side * d + i;
+            float4 o;
+            o.x = Bm[p * ldB + i] - c * rs[0];
+            o.y = Bm[p * ldB + i + 1] - c * rs[1];
+            o.z = Bm[p * ldB + i + 2] - c * rs[2];
+            o.w = Bm[p * ldB + i + 3] - c * rs[3];
+            *reinterpret_cast<float4 *>((side ? L.B_K : L.B_Q) + (size_t)bh * R * d + p * d + i) = o;
         }
     }
+    trace(4);
 
     // ---------------- outputs and appends ---------------------------------
     for (int i = tid; i < R; i += blockDim.x) {
@@ -687,68 +814,65 @@ compress_kernel(const CompressArgs args) {
         T *dv = reinterpret_cast<T *>(L.slow_v) + (kv_rows + t) * d;
         for (int i = tid; i < d; i += blockDim.x) { dk[i] = krow[i]; dv[i] = vrow[i]; }
     }
-    if (host) {  // the new row also lands in this head's spare slot
+    if (L.policy == LRQK_SLOW_HOST) {  // the new row also lands in this head's spare slot
         const int slot = L.spare_slot[bh];
         T *sk = reinterpret_cast<T *>(L.slot_k) + ((size_t)bh * L.n_slots + slot) * d;
         T *sv = reinterpret_cast<T *>(L.slot_v) + ((size_t)bh * L.n_slots + slot) * d;
         for (int i = tid; i < d; i += blockDim.x) { sk[i] = krow[i]; sv[i] = vrow[i]; }
     }
+    (void)nwarps;
 }
 
 int compress_chunks(const lrqk_layer_t &L) { return (L.s_cap + kRedRows - 1) / kRedRows; }
 
 size_t compress_scratch_floats_per_head(const lrqk_layer_t &L) {
-    return red_head_floats(L.rank_stride, compress_chunks(L));
+    return red_head_floats(L.rank_stride, L.dim_stride, compress_chunks(L));
+}
+size_t compress_pre_floats_per_head(const lrqk_layer_t &L) {
+    return pre_layout(L.rank_stride, L.dim_stride).total;
 }
 
-size_t compress_smem_bytes(const lrqk_layer_t &L) {
+static size_t prepare_smem_bytes(const lrqk_layer_t &L) {
     const size_t d = L.dim_stride, R = L.rank_stride;
     const size_t RB = R / 4, NP = RB * (RB + 1) / 2;
     const size_t NG = NP >= (size_t)kCompressThreads ? 1 : kCompressThreads / NP;
-    const size_t a = (d + kRedRows + (size_t)kRedRows * (R + 1) + 2 * kRedRows + NG * NP * 16) * sizeof(float);
-    const size_t p = (2 * R * (d + 1) + R * (R + 1) + 2 * d + R + 2 * NP * 16) * sizeof(float);
-    const size_t f = (4 * R * (R + 1) + 4 * d + 9 * R) * sizeof(float);
+    const size_t ldB = d + 4, ldM = R + 4;
+    const size_t a = ((size_t)kSub * ldB + (size_t)kSub * (R + 1) + NG * NP * 16) * sizeof(float);
+    const size_t p = (2 * R * ldB + R * ldM + 2 * NP * 16) * sizeof(float);
+    const size_t f = (R * ldB + R * ldM) * sizeof(float);
     return std::max(a, std::max(p, f));
 }
+static size_t compress_smem_bytes(const lrqk_layer_t &L) {
+    const size_t d = L.dim_stride, R = L.rank_stride;
+    const size_t ldB = d + 4, ldM = R + 4;
+    return (4 * R * ldB + 4 * R * ldM + 4 * d + 7 * R) * sizeof(float);
+}
 
-template <typename T>
-static int launch_compress_t(const CompressArgs &a, cudaStream_t st) {
-    const lrqk_layer_t &L = a.L;
-    constexpr int N = Pack<T>::N;
-    const int packs = L.dim_stride / N;
-    const int lpr = packs < 32 ? packs : 32;
-    const int ppl = packs / lpr;
+int launch_prepare(const lrqk_layer_t &L, cudaStream_t st) {
     dim3 grid(compress_chunks(L) + 1, L.batch * L.n_q_heads);
-    const size_t smem = compress_smem_bytes(L);
-#define LRQK_CMP(LP, PP)                                                                   \
-    do {                                                                                   \
-        auto fn = compress_kernel<T, LP, PP>;                                              \
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-        fn<<<grid, kCompressThreads, smem, st>>>(a);                                       \
-    } while (0)
-    if (ppl == 1) {
-        switch (lpr) {
-            case 1: LRQK_CMP(1, 1); break;
-            case 2: LRQK_CMP(2, 1); break;
-            case 4: LRQK_CMP(4, 1); break;
-            case 8: LRQK_CMP(8, 1); break;
-            case 16: LRQK_CMP(16, 1); break;
-            case 32: LRQK_CMP(32, 1); break;
-            default: return LRQK_EUNSUPPORTED;
-        }
-    } else if (ppl == 2 && lpr == 32) {
-        LRQK_CMP(32, 2);
+    const size_t smem = prepare_smem_bytes(L);
+    if (L.dtype == LRQK_BF16) {
+        cudaFuncSetAttribute(prepare_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        prepare_kernel<__nv_bfloat16><<<grid, kCompressThreads, smem, st>>>(L);
     } else {
-        return LRQK_EUNSUPPORTED;
+        cudaFuncSetAttribute(prepare_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        prepare_kernel<float><<<grid, kCompressThreads, smem, st>>>(L);
     }
-#undef LRQK_CMP
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
 int launch_compress(const lrqk_layer_t &L, const void *q, const void *k, const void *v, int update_b,
                     cudaStream_t st) {
     CompressArgs a{L, q, k, v, update_b};
-    return L.dtype == LRQK_BF16 ? launch_compress_t<__nv_bfloat16>(a, st) : launch_compress_t<float>(a, st);
+    const size_t smem = compress_smem_bytes(L);
+    if (L.dtype == LRQK_BF16) {
+        cudaFuncSetAttribute(compress_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        compress_kernel<__nv_bfloat16><<<L.batch * L.n_q_heads, kCompressThreads, smem, st>>>(a);
+    } else {
+        cudaFuncSetAttribute(compress_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        compress_kernel<float><<<L.batch * L.n_q_heads, kCompressThreads, smem, st>>>(a);
+    }
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
 }  // namespace lrqk

@@ -56,6 +56,7 @@ calls = [lambda: lib.lrqk_decode_compress(L.ptr, q.data_ptr(), k.data_ptr(), v.d
 times = {n: [] for n in names}
 for s in range(a.steps):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+    torch.cuda._sleep(200000)  # let the host enqueue every launch before timing
     evs[0].record()
     for i, c in enumerate(calls):
         _lib.check(c(), names[i])
@@ -64,6 +65,19 @@ for s in range(a.steps):
     for i, n in enumerate(names):
         times[n].append(evs[i].elapsed_time(evs[i + 1]) * 1e3)
 st = int(L.view("status").item())
+import numpy as np
+lib.lrqk_trace_enable(1)
+_lib.check(calls[0](), "compress")
+torch.cuda.synchronize()
+buf = np.zeros((65536, 2), dtype=np.uint64)
+n = lib.lrqk_trace_read(buf.ctypes.data, 65536)
+lib.lrqk_trace_enable(0)
+rec = buf[:n]
+t0 = rec[:, 1].min()
+tags = (rec[:, 0] >> 48).astype(int)
+for tag in sorted(set(tags)):
+    ts = (rec[tags == tag, 1] - t0) / 1e3
+    print(f"trace tag {tag}: n={len(ts)} min={ts.min():.1f}us med={np.median(ts):.1f}us max={ts.max():.1f}us")
 res = {n: round(sum(v[1:]) / max(1, len(v) - 1), 2) for n, v in times.items()}
 print(json.dumps(dict(us=res, status=st, prefill_ms=round(pf_ms, 1), miss=int(L.view("step_miss").sum()),
                       total=int(L.view("step_total").sum()), args=vars(a))))
