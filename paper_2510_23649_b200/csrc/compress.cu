@@ -292,23 +292,26 @@ prepare_kernel(const lrqk_layer_t L) {
     const int ldB = d + 4, ldM = R + 4;
     constexpr int N = Pack<T>::N;
 
+    trace(10);
     if ((int)blockIdx.x < nchunks) {
         // ---- reduce: Y = A^T K and G = A^T A over this chunk of Omega ------
         const int row0 = blockIdx.x * kRedRows;
         const int nrow = max(0, min(kRedRows, n_prev - row0));
-        const int ldA = R + 1;
+        const int ldA = R + 4;
         float *sK = smem;                    // [kSub][ldB]
         float *sA = sK + kSub * ldB;         // [kSub][ldA]
         float *sRed = sA + kSub * ldA;       // gram groups
         const int *ridx = L.res_idx + (size_t)bh * L.s_cap + row0;
         const int *rslot = L.res_slot + (size_t)bh * L.s_cap + row0;
-        // Y tiles (4 p x 4 i) owned by this thread
-        const int nYt = (R / 4) * (d / 4);
-        float yacc[4][16];
+        // Y = A^T K: 8 (p) x 4 (i) register tiles; rows split over RG groups
+        const int ntl = (R / 8) * (d / 4);
+        const int RG = ntl >= kCompressThreads ? 1 : kCompressThreads / ntl;
+        const int tgrp = tid / ntl;                  // row group (RG > 1)
+        float yacc[2][32];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-            for (int e = 0; e < 16; ++e) yacc[a][e] = 0.f;
+            for (int e = 0; e < 32; ++e) yacc[a][e] = 0.f;
         const int RB = R / 4, NP = RB * (RB + 1) / 2;
         const int NG = max(1, kCompressThreads / NP);
         float gacc[16];
@@ -353,20 +356,21 @@ prepare_kernel(const lrqk_layer_t L) {
                 }
             }
             __syncthreads();
-            // Y += A^T K
-            for (int a = 0; a < 4; ++a) {
-                const int tI = tid + a * kCompressThreads;
-                if (tI >= nYt) break;
-                const int p0 = (tI / (d / 4)) * 4, i0 = (tI % (d / 4)) * 4;
-                for (int j = 0; j < ns; ++j) {
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const int tI = (RG > 1) ? tid % ntl : tid + a * kCompressThreads;
+                if ((RG > 1 && a > 0) || tI >= ntl) break;
+                const int p0 = (tI / (d / 4)) * 8, i0 = (tI % (d / 4)) * 4;
+                for (int j = (RG > 1 ? tgrp : 0); j < ns; j += RG) {
                     const float4 kv = *reinterpret_cast<const float4 *>(sK + j * ldB + i0);
+                    const float4 a0 = *reinterpret_cast<const float4 *>(sA + j * ldA + p0);
+                    const float4 a1 = *reinterpret_cast<const float4 *>(sA + j * ldA + p0 + 4);
                     const float ks[4] = {kv.x, kv.y, kv.z, kv.w};
+                    const float as[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float ap2 = sA[j * ldA + p0 + u];
+                    for (int u = 0; u < 8; ++u)
 #pragma unroll
-                        for (int w2 = 0; w2 < 4; ++w2) yacc[a][u * 4 + w2] = fmaf(ap2, ks[w2], yacc[a][u * 4 + w2]);
-                    }
+                        for (int w2 = 0; w2 < 4; ++w2) yacc[a][u * 4 + w2] = fmaf(as[u], ks[w2], yacc[a][u * 4 + w2]);
                 }
             }
             // G += A^T A (upper 4x4 tiles, row groups)
@@ -387,15 +391,38 @@ prepare_kernel(const lrqk_layer_t L) {
                 }
             }
         }
+        trace(11);
         float *part = hs + (size_t)blockIdx.x * (R * d + R * R);
-        for (int a = 0; a < 4; ++a) {
-            const int tI = tid + a * kCompressThreads;
-            if (tI >= nYt) break;
-            const int p0 = (tI / (d / 4)) * 4, i0 = (tI % (d / 4)) * 4;
+        if (RG == 1) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                *reinterpret_cast<float4 *>(part + (p0 + u) * d + i0) =
-                    make_float4(yacc[a][u * 4], yacc[a][u * 4 + 1], yacc[a][u * 4 + 2], yacc[a][u * 4 + 3]);
+            for (int a = 0; a < 2; ++a) {
+                const int tI = tid + a * kCompressThreads;
+                if (tI >= ntl) break;
+                const int p0 = (tI / (d / 4)) * 8, i0 = (tI % (d / 4)) * 4;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    *reinterpret_cast<float4 *>(part + (p0 + u) * d + i0) =
+                        make_float4(yacc[a][u * 4], yacc[a][u * 4 + 1], yacc[a][u * 4 + 2], yacc[a][u * 4 + 3]);
+            }
+        } else {
+            // sum the RG row groups through shared memory (reuses the staging area)
+            __syncthreads();
+            float *red = smem;  // [RG][R*d]
+            const int tI = tid % ntl;
+            const int p0 = (tI / (d / 4)) * 8, i0 = (tI % (d / 4)) * 4;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                *reinterpret_cast<float4 *>(red + (size_t)tgrp * R * d + (p0 + u) * d + i0) =
+                    make_float4(yacc[0][u * 4], yacc[0][u * 4 + 1], yacc[0][u * 4 + 2], yacc[0][u * 4 + 3]);
+            __syncthreads();
+            for (int e4 = tid; e4 < R * d / 4; e4 += kCompressThreads) {
+                float4 acc = reinterpret_cast<const float4 *>(red)[e4];
+                for (int gI = 1; gI < RG; ++gI) {
+                    const float4 v = reinterpret_cast<const float4 *>(red + (size_t)gI * R * d)[e4];
+                    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                }
+                reinterpret_cast<float4 *>(part)[e4] = acc;
+            }
         }
         __syncthreads();
         if (tid < NP * NG) {
@@ -449,7 +476,9 @@ prepare_kernel(const lrqk_layer_t L) {
         }
         if (tid == 0) pre[PL.flags + 1] = ok ? 1.f : 0.f;
     }
+    trace((int)blockIdx.x < nchunks ? 12 : 13);
     if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_PREPARE, gridDim.x, &s_flag)) return;
+    trace(14);
 
     // ---- finish: P, P^-1, W, Z_Q ---------------------------------------------
     float *sW = smem;                    // [R][ldB]   W = B_Q + l2 Y
@@ -494,6 +523,7 @@ prepare_kernel(const lrqk_layer_t L) {
         }
     }
     __syncthreads();
+    trace(15);
     const bool okP = block_gj(b0, R, ldM, s_rc);
     if (okP) {
         for (int e = tid; e < R * R; e += blockDim.x) {
@@ -508,6 +538,7 @@ prepare_kernel(const lrqk_layer_t L) {
             pre[PL.ZQ + e] = acc;
         }
     }
+    trace(16);
     if (tid == 0) pre[PL.flags + 0] = okP ? 1.f : 0.f;
     (void)warp;
 }
@@ -837,7 +868,8 @@ static size_t prepare_smem_bytes(const lrqk_layer_t &L) {
     const size_t RB = R / 4, NP = RB * (RB + 1) / 2;
     const size_t NG = NP >= (size_t)kCompressThreads ? 1 : kCompressThreads / NP;
     const size_t ldB = d + 4, ldM = R + 4;
-    const size_t a = ((size_t)kSub * ldB + (size_t)kSub * (R + 1) + NG * NP * 16) * sizeof(float);
+    const size_t a = std::max(((size_t)kSub * ldB + (size_t)kSub * (R + 4) + NG * NP * 16) * sizeof(float),
+                              (size_t)8192 * sizeof(float));
     const size_t p = (2 * R * ldB + R * ldM + 2 * NP * 16) * sizeof(float);
     const size_t f = (R * ldB + R * ldM) * sizeof(float);
     return std::max(a, std::max(p, f));

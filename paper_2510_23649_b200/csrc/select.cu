@@ -222,6 +222,173 @@ score_kernel(const ScoreArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// K3 (main path): the proxy store streamed through a TMA bulk-copy pipeline.
+// One producer warp keeps kStages 1-D bulk copies (cp.async.bulk, completion
+// on an mbarrier) in flight; eight consumer warps each score one 32-row tile
+// per stage straight out of shared memory (lane = row).  Every byte of the
+// proxy store is read exactly once, with no register staging.
+// ---------------------------------------------------------------------------
+constexpr int kCW = 8;  // consumer warps
+
+LRQK_DEV uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+LRQK_DEV void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+LRQK_DEV void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+LRQK_DEV void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+LRQK_DEV void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    } while (!ok);
+}
+LRQK_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int NPK> struct ScoreStages {
+    static constexpr int kTileBytes = NPK * 512;
+    static constexpr int kStageBytes = kCW * kTileBytes;
+    static constexpr int kStages = (96 * 1024 / kStageBytes) < 2 ? 2 : ((96 * 1024 / kStageBytes) > 6 ? 6 : 96 * 1024 / kStageBytes);
+    static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
+};
+
+template <typename T, int NPK>
+__global__ void __launch_bounds__(32 * (kCW + 1))
+score_tma_kernel(const ScoreArgs a) {
+    using SS = ScoreStages<NPK>;
+    const lrqk_layer_t &L = a.L;
+    constexpr int N = Pack<T>::N;
+    constexpr int R = NPK * N;
+    extern __shared__ __align__(128) uint8_t tsm[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(tsm + SS::kStages * SS::kStageBytes);
+    uint64_t *empty = full + SS::kStages;
+    __shared__ int s_hist[kHistBins];
+    __shared__ int s_scan[32];
+    __shared__ int s_flag;
+    __shared__ int s_out[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int P = a.parts;
+    const int bh = blockIdx.x / P, part = blockIdx.x - bh * P;
+    const int b = bh / L.n_q_heads;
+    const int t = L.ctx_len[b];
+    if (t >= L.t_max) return;
+    const int n = t + 1;
+    const int lite_start = max(0, n - L.lite_budget);
+    const int tiles = (n + 31) >> 5;
+    const int tpp = (tiles + P - 1) / P;
+    const int tile0 = min(tiles, part * tpp), tile1 = min(tiles, tile0 + tpp);
+    const int stride = sample_stride(lite_start);
+    const int n_stage_iters = (tile1 - tile0 + kCW - 1) / kCW;
+    for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = 0;
+    if (tid == 0) {
+        for (int s2 = 0; s2 < SS::kStages; ++s2) {
+            mbar_init(full + s2, 1);
+            mbar_init(empty + s2, kCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint8_t *src = reinterpret_cast<const uint8_t *>(reinterpret_cast<const T *>(L.proxy) +
+                                                           (size_t)bh * L.t_max * R);
+    uint32_t *keys = L.keys + (size_t)bh * L.t_max;
+    if (warp == kCW) {
+        // ---------------- producer ----------------
+        if (lane == 0) {
+            for (int it = 0; it < n_stage_iters; ++it) {
+                const int s2 = it % SS::kStages;
+                if (it >= SS::kStages) mbar_wait(empty + s2, ((it / SS::kStages) - 1) & 1);
+                const int nt = min(kCW, tile1 - tile0 - it * kCW);
+                const uint32_t bytes = (uint32_t)nt * SS::kTileBytes;
+                mbar_expect_tx(full + s2, bytes);
+                bulk_g2s(tsm + s2 * SS::kStageBytes, src + (size_t)(tile0 + it * kCW) * SS::kTileBytes, bytes,
+                         full + s2);
+            }
+        }
+    } else {
+        // ---------------- consumers ----------------
+        float qv[R];
+        const float *qh = L.q_hat + (size_t)bh * L.rank_stride;
+#pragma unroll
+        for (int e = 0; e < R; ++e) qv[e] = qh[e];
+        for (int it = 0; it < n_stage_iters; ++it) {
+            const int s2 = it % SS::kStages;
+            mbar_wait(full + s2, (it / SS::kStages) & 1);
+            const int tile = tile0 + it * kCW + warp;
+            if (tile < tile1) {
+                const uint4 *p4 = reinterpret_cast<const uint4 *>(tsm + s2 * SS::kStageBytes + warp * SS::kTileBytes) + lane;
+                float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+                for (int pk = 0; pk < NPK; ++pk) {
+                    float f[N];
+                    unpack16<T>(p4[pk * 32], f);
+#pragma unroll
+                    for (int e = 0; e < N; e += 2) {
+                        s0 = fmaf(f[e], qv[pk * N + e], s0);
+                        s1 = fmaf(f[e + 1], qv[pk * N + e + 1], s1);
+                    }
+                }
+                const int row = tile * 32 + lane;
+                const uint32_t key = score_key(s0 + s1);
+                if (row < n) keys[row] = key;
+                if (row < lite_start && (tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s2);
+        }
+    }
+    __syncthreads();
+    uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;
+    for (int i = tid; i < kHistBins; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(ghist + i, (uint32_t)s_hist[i]);
+    int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
+    if (!last_arrival(cnt, P, &s_flag)) return;
+    // ---- last block of this head: candidate bins ----------------------------
+    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+    const int k_eff = min(L.k_budget, lite_start);
+    if (lite_start == 0 || k_eff >= lite_start) {
+        if (tid == 0) {
+            meta[M_MODE] = 1; meta[M_K_EFF] = k_eff; meta[M_LITE] = lite_start;
+            meta[M_SURE] = 0; meta[M_CAND] = 0;
+        }
+        return;
+    }
+    for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = (int)__ldcg(ghist + i);
+    __syncthreads();
+    int b_hi, b_lo;
+    if (stride == 1) {
+        find_crossing(s_hist, kHistBins, k_eff, s_scan, s_out);
+        b_hi = b_lo = s_out[0];
+    } else {
+        const int m_hi = max(1, (int)(0.8f * k_eff / stride));
+        find_crossing(s_hist, kHistBins, m_hi, s_scan, s_out);
+        b_hi = s_out[0] < 0 ? kHistBins - 1 : s_out[0];
+        const int m_lo = (int)ceilf(1.25f * k_eff / stride) + 8;
+        find_crossing(s_hist, kHistBins, m_lo, s_scan, s_out);
+        b_lo = s_out[0] < 0 ? 0 : s_out[0];
+    }
+    if (tid == 0) {
+        meta[M_B_HI] = b_hi;
+        meta[M_B_LO] = b_lo;
+        meta[M_STRIDE] = stride;
+        int s2 = 0;
+        while (s2 < 32 - kHistBits && ((b_hi - b_lo + 1) << (s2 + 1)) <= kHistBins) ++s2;
+        meta[M_S2] = s2;
+        meta[M_K_EFF] = k_eff;
+        meta[M_LITE] = lite_start;
+        meta[M_SURE] = 0;
+        meta[M_CAND] = 0;
+        meta[M_MODE] = 0;
+    }
+}
+
 // Radix select over unique composites (exact fallback): returns thr such that
 // exactly m elements have comp >= thr.
 template <class Get>
@@ -595,7 +762,36 @@ static int launch_score_t(const ScoreArgs &a, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
+template <typename T, int NPK>
+static void launch_score_tma_t(const ScoreArgs &a, int grid, cudaStream_t st) {
+    using SS = ScoreStages<NPK>;
+    auto fn = score_tma_kernel<T, NPK>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::kSmem);
+    fn<<<grid, 32 * (kCW + 1), SS::kSmem, st>>>(a);
+}
+
+template <typename T>
+static int launch_score_tma(const lrqk_layer_t &L, cudaStream_t st) {
+    const int BH = L.batch * L.n_q_heads;
+    const int tiles = L.t_max / 32;
+    const int P = max(1, min((2 * num_sms()) / BH, max(1, tiles / 64)));
+    ScoreArgs a{L, nullptr, P};
+    const int grid = BH * P;
+    const int npk = L.rank_stride * (int)sizeof(T) / 16;
+    switch (npk) {
+        case 1: launch_score_tma_t<T, 1>(a, grid, st); break;
+        case 2: launch_score_tma_t<T, 2>(a, grid, st); break;
+        case 4: launch_score_tma_t<T, 4>(a, grid, st); break;
+        case 8: launch_score_tma_t<T, 8>(a, grid, st); break;
+        case 16: launch_score_tma_t<T, 16>(a, grid, st); break;
+        default: return LRQK_EUNSUPPORTED;
+    }
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
 int launch_score(const lrqk_layer_t &L, const float *ext_scores, cudaStream_t st) {
+    if (ext_scores == nullptr)
+        return L.dtype == LRQK_BF16 ? launch_score_tma<__nv_bfloat16>(L, st) : launch_score_tma<float>(L, st);
     ScoreArgs a{L, ext_scores, score_parts(L)};
     return L.dtype == LRQK_BF16 ? launch_score_t<__nv_bfloat16>(a, st) : launch_score_t<float>(a, st);
 }

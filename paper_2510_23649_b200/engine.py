@@ -379,22 +379,48 @@ class Engine:
         return self.ctx_len[: 4 * self.shape.batch].view(torch.int32)
 
     def launches_per_step(self):
-        """Kernels one decode step launches (compress, score, scan, finalize,
-        [gather], attention per layer, plus the ctx advance)."""
+        """Kernels one decode step launches: per layer compress, score,
+        select, [gather], attention and the next step's compress_prepare,
+        plus the ctx advance."""
         per = 5 + (1 if self.shape.policy == "host" else 0)
         return self.n_layers * per + 1
 
-    def decode_step(self, q=None, k=None, v=None, out=None, stream=None):
+    def decode_step(self, q=None, k=None, v=None, out=None, stream=None, overlap=True):
+        """One token for every sequence through all layers.  With overlap,
+        each layer's compress_prepare (the q/k-independent half of the next
+        step's compression) runs on a side stream concurrently with the rest
+        of the step and is joined before the step ends."""
         q = self.q_buf if q is None else q
         k = self.k_buf if k is None else k
         v = self.v_buf if v is None else v
         out = self.out_buf if out is None else out
         lib = _lib.lib()
-        sp = _lib.stream_ptr(stream)
+        main = stream if stream is not None else torch.cuda.current_stream()
+        sp = _lib.stream_ptr(main)
+        if overlap:
+            if getattr(self, "_side", None) is None:
+                self._side = torch.cuda.Stream(device=self.device)
+            side = self._side
+            side.wait_stream(main)
+            ssp = _lib.stream_ptr(side)
         for i, layer in enumerate(self.layers):
-            _lib.check(lib.lrqk_decode_step(layer.ptr, q[i].data_ptr(), k[i].data_ptr(), v[i].data_ptr(),
-                                            out[i].data_ptr(), 0, sp), "lrqk_decode_step")
+            lp = layer.ptr
+            _lib.check(lib.lrqk_decode_compress(lp, q[i].data_ptr(), k[i].data_ptr(), v[i].data_ptr(), 1, sp),
+                       "lrqk_decode_compress")
+            _lib.check(lib.lrqk_score(lp, sp), "lrqk_score")
+            _lib.check(lib.lrqk_select(lp, sp), "lrqk_select")
+            _lib.check(lib.lrqk_gather_misses(lp, sp), "lrqk_gather_misses")
+            if overlap:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                side.wait_event(ev)
+                _lib.check(lib.lrqk_compress_prepare(lp, ssp), "lrqk_compress_prepare")
+            _lib.check(lib.lrqk_attention(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_attention")
+            if not overlap:
+                _lib.check(lib.lrqk_compress_prepare(lp, sp), "lrqk_compress_prepare")
         _lib.check(lib.lrqk_advance(self.ctx.data_ptr(), self.shape.batch, sp), "lrqk_advance")
+        if overlap:
+            main.wait_stream(side)
         return out
 
     def capture(self, warmup_steps=0):

@@ -18,6 +18,7 @@ p.add_argument("--steps", type=int, default=6)
 p.add_argument("--dtype", default="bf16")
 p.add_argument("--policy", default="hbm")
 p.add_argument("--no-prefill", action="store_true")
+p.add_argument("--trace", default="compress")
 a = p.parse_args()
 dev = torch.device("cuda")
 B, Hq, Hkv, d, r, l = a.batch, a.hq, a.hkv, 128, a.rank, a.ctx
@@ -47,11 +48,12 @@ q = torch.randn(B, Hq, d, device=dev, generator=g).to(sdt)
 k = torch.randn(B, Hkv, d, device=dev, generator=g).to(sdt)
 v = torch.randn(B, Hkv, d, device=dev, generator=g).to(sdt)
 out = torch.zeros(B, Hq, d, device=dev)
-names = ["compress", "score", "select", "gather", "attention", "advance"]
+names = ["compress", "score", "select", "gather", "attention", "prepare", "advance"]
 calls = [lambda: lib.lrqk_decode_compress(L.ptr, q.data_ptr(), k.data_ptr(), v.data_ptr(), 1, sp),
          lambda: lib.lrqk_score(L.ptr, sp), lambda: lib.lrqk_select(L.ptr, sp),
          lambda: lib.lrqk_gather_misses(L.ptr, sp),
          lambda: lib.lrqk_attention(L.ptr, q.data_ptr(), out.data_ptr(), sp),
+         lambda: lib.lrqk_compress_prepare(L.ptr, sp),
          lambda: lib.lrqk_advance(L.view("ctx_len").data_ptr(), B, sp)]
 times = {n: [] for n in names}
 for s in range(a.steps):
@@ -67,7 +69,8 @@ for s in range(a.steps):
 st = int(L.view("status").item())
 import numpy as np
 lib.lrqk_trace_enable(1)
-_lib.check(calls[0](), "compress")
+ti = names.index(a.trace)
+_lib.check(calls[ti](), a.trace)
 torch.cuda.synchronize()
 buf = np.zeros((65536, 2), dtype=np.uint64)
 n = lib.lrqk_trace_read(buf.ctypes.data, 65536)
