@@ -25,7 +25,7 @@ attention_kernel(const AttnArgs a) {
     const lrqk_layer_t &L = a.L;
     constexpr int N = Pack<T>::N;
     constexpr int RPW = 32 / LPR;
-    constexpr int U = 4;
+    constexpr int U = 8;
     constexpr int NW = kAttnThreads / 32;
     __shared__ float s_m[NW * RPW], s_l[NW * RPW];
     __shared__ int s_flag;
@@ -64,23 +64,26 @@ attention_kernel(const AttnArgs a) {
         for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
     const int r0 = split * kAttnRows, r1 = min(S, r0 + kAttnRows);
     const int step = NW * RPW;
+    // the split's row offsets, staged once (one dependent round trip)
+    __shared__ int s_src[kAttnRows];
+    for (int j = tid; j < r1 - r0; j += blockDim.x) s_src[j] = src[r0 + j];
+    __syncthreads();
+    // scores of U rows per lane group in flight, K and V kept packed until used
     for (int base = r0 + warp * RPW + sub; base < r1 + sub; base += step * U) {
-        float kx[U][PPL][N], vx[U][PPL][N];
+        uint4 kx[U][PPL], vx[U][PPL];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = base + u * step;
             if (j < r1) {
-                const size_t row = (size_t)src[j] * d;
+                const size_t row = (size_t)s_src[j - r0] * d;
 #pragma unroll
                 for (int pp = 0; pp < PPL; ++pp) {
-                    Pack<T>::load(kb + row + (sl + pp * LPR) * N, kx[u][pp]);
-                    Pack<T>::load(vb + row + (sl + pp * LPR) * N, vx[u][pp]);
+                    kx[u][pp] = *reinterpret_cast<const uint4 *>(kb + row + (sl + pp * LPR) * N);
+                    vx[u][pp] = *reinterpret_cast<const uint4 *>(vb + row + (sl + pp * LPR) * N);
                 }
             } else {
 #pragma unroll
-                for (int pp = 0; pp < PPL; ++pp)
-#pragma unroll
-                    for (int e = 0; e < N; ++e) { kx[u][pp][e] = 0.f; vx[u][pp][e] = 0.f; }
+                for (int pp = 0; pp < PPL; ++pp) { kx[u][pp] = make_uint4(0, 0, 0, 0); vx[u][pp] = make_uint4(0, 0, 0, 0); }
             }
         }
         float x[U];
@@ -88,12 +91,20 @@ attention_kernel(const AttnArgs a) {
         for (int u = 0; u < U; ++u) {
             float s = 0.f;
 #pragma unroll
-            for (int pp = 0; pp < PPL; ++pp)
+            for (int pp = 0; pp < PPL; ++pp) {
+                float f[N];
+                unpack16<T>(kx[u][pp], f);
 #pragma unroll
-                for (int e = 0; e < N; ++e) s = fmaf(kx[u][pp][e], qv[pp][e], s);
-            s = group_sum<LPR>(s);
-            x[u] = (base + u * step < r1) ? s * c : -INFINITY;
+                for (int e = 0; e < N; ++e) s = fmaf(f[e], qv[pp][e], s);
+            }
+            x[u] = s;
         }
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], o);
+#pragma unroll
+        for (int u = 0; u < U; ++u) x[u] = (base + u * step < r1) ? x[u] * c : -INFINITY;
         float mx = m;
 #pragma unroll
         for (int u = 0; u < U; ++u) mx = fmaxf(mx, x[u]);
@@ -109,9 +120,12 @@ attention_kernel(const AttnArgs a) {
             const float p = exp2f(x[u] - mx);
             l += p;
 #pragma unroll
-            for (int pp = 0; pp < PPL; ++pp)
+            for (int pp = 0; pp < PPL; ++pp) {
+                float f[N];
+                unpack16<T>(vx[u][pp], f);
 #pragma unroll
-                for (int e = 0; e < N; ++e) acc[pp][e] = fmaf(p, vx[u][pp][e], acc[pp][e]);
+                for (int e = 0; e < N; ++e) acc[pp][e] = fmaf(p, f[e], acc[pp][e]);
+            }
         }
         m = mx;
     }

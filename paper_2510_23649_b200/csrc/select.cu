@@ -424,6 +424,7 @@ __device__ uint64_t radix_top_m(Get get, int n, int m, int nbits, int *s_hist, i
 // ---------------------------------------------------------------------------
 constexpr int kLocSure = 1024;  // block-local append buffers (spill to global beyond)
 constexpr int kLocCand = 2048;
+constexpr int kCritCap = 4096;  // critical fine bin sorted in shared memory (larger -> exact fallback)
 
 __global__ void __launch_bounds__(kSelThreads)
 select_kernel(const lrqk_layer_t L, int parts) {
@@ -453,53 +454,71 @@ select_kernel(const lrqk_layer_t L, int parts) {
         // ---- scan part: certain winners, candidates, fine histogram ----------
         if (mode0 == 0) {
             const int b_hi = meta[M_B_HI], b_lo = meta[M_B_LO], s2 = meta[M_S2];
-            const int per = (lite_start + parts - 1) / parts;
-            const int row0 = part * per, row1 = min(lite_start, row0 + per);
+            const int per = ((lite_start + parts - 1) / parts + 3) & ~3;  // 16-byte aligned parts
+            const int row0 = min(lite_start, part * per), row1 = min(lite_start, row0 + per);
             int *loc_sure = reinterpret_cast<int *>(fsm);
             uint64_t *loc_cand = reinterpret_cast<uint64_t *>(fsm + kLocSure);
             for (int i = tid; i < kHistBins; i += nt) s_hist[i] = 0;
             if (tid < 4) s_cnt[tid] = 0;
             __syncthreads();
-            for (int base = row0; base < row1; base += nt * 4) {
-                uint32_t kv[4];
+            constexpr int U = 4;  // 16-byte key loads in flight per thread
+            for (int base = row0; base < row1; base += nt * 4 * U) {
+                uint4 kv4[U];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = base + u * nt + tid;
-                    kv[u] = i < row1 ? __ldcg(keys + i) : 0u;
+                for (int u = 0; u < U; ++u) {
+                    const int i = base + (u * nt + tid) * 4;
+                    kv4[u] = i < row1 ? __ldcg(reinterpret_cast<const uint4 *>(keys + i)) : make_uint4(0, 0, 0, 0);
                 }
+                // classify, count, one warp scan per list
+                uint32_t sure_m = 0, cand_m = 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = base + u * nt + tid;
-                    const int bin = (int)(kv[u] >> (32 - kHistBits));
-                    const bool is_sure = i < row1 && bin > b_hi;
-                    const bool is_cand = i < row1 && bin >= b_lo && bin <= b_hi;
-                    const unsigned ms = __ballot_sync(0xffffffffu, is_sure);
-                    const unsigned mc = __ballot_sync(0xffffffffu, is_cand);
-                    if (ms) {
-                        int basei = 0;
-                        if (lane == 0) basei = atomicAdd(&s_cnt[0], __popc(ms));
-                        basei = __shfl_sync(0xffffffffu, basei, 0);
-                        const int pos = basei + __popc(ms & ((1u << lane) - 1u));
-                        if (is_sure) {
-                            if (pos < kLocSure) loc_sure[pos] = i;
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t kk[4] = {kv4[u].x, kv4[u].y, kv4[u].z, kv4[u].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int i = base + (u * nt + tid) * 4 + c;
+                        const int bin = (int)(kk[c] >> (32 - kHistBits));
+                        if (i < row1 && bin > b_hi) sure_m |= 1u << (u * 4 + c);
+                        else if (i < row1 && bin >= b_lo) cand_m |= 1u << (u * 4 + c);
+                    }
+                }
+                if (!__any_sync(0xffffffffu, (sure_m | cand_m) != 0)) continue;
+                const int ns_t = __popc(sure_m), nc_t = __popc(cand_m);
+                int xs = ns_t, xc = nc_t;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int ys = __shfl_up_sync(0xffffffffu, xs, o), yc = __shfl_up_sync(0xffffffffu, xc, o);
+                    if (lane >= o) { xs += ys; xc += yc; }
+                }
+                int bs = 0, bc = 0;
+                if (lane == 31) {
+                    bs = xs ? atomicAdd(&s_cnt[0], xs) : 0;
+                    bc = xc ? atomicAdd(&s_cnt[1], xc) : 0;
+                }
+                bs = __shfl_sync(0xffffffffu, bs, 31) + xs - ns_t;
+                bc = __shfl_sync(0xffffffffu, bc, 31) + xc - nc_t;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t kk[4] = {kv4[u].x, kv4[u].y, kv4[u].z, kv4[u].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int bit = u * 4 + c;
+                        const int i = base + (u * nt + tid) * 4 + c;
+                        if (sure_m & (1u << bit)) {
+                            if (bs < kLocSure) loc_sure[bs] = i;
                             else {  // rare spill: straight to the global list
                                 const int g = atomicAdd(meta + M_SURE, 1);
                                 if (g < L.k_budget) sure[g] = i;
                             }
-                        }
-                    }
-                    if (mc) {
-                        int basei = 0;
-                        if (lane == 0) basei = atomicAdd(&s_cnt[1], __popc(mc));
-                        basei = __shfl_sync(0xffffffffu, basei, 0);
-                        const int pos = basei + __popc(mc & ((1u << lane) - 1u));
-                        if (is_cand) {
-                            atomicAdd(&s_hist[fine_bin(kv[u], b_lo, s2)], 1);
-                            if (pos < kLocCand) loc_cand[pos] = make_comp(kv[u], i);
+                            ++bs;
+                        } else if (cand_m & (1u << bit)) {
+                            atomicAdd(&s_hist[fine_bin(kk[c], b_lo, s2)], 1);
+                            if (bc < kLocCand) loc_cand[bc] = make_comp(kk[c], i);
                             else {
                                 const int g = atomicAdd(meta + M_CAND, 1);
-                                if (g < L.cand_cap) cand[g] = make_comp(kv[u], i);
+                                if (g < L.cand_cap) cand[g] = make_comp(kk[c], i);
                             }
+                            ++bc;
                         }
                     }
                 }
@@ -556,7 +575,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
                     const int n_crit = fstar >= 0 ? s_hist[fstar] : 0;
                     int M = 1;
                     while (M < n_crit) M <<= 1;
-                    if (fstar < 0 || M > L.cand_cap) ok = false;  // uniform
+                    if (fstar < 0 || M > kCritCap) ok = false;  // uniform
                     if (ok) {
                         for (int i = tid; i < n_cand; i += nt) {
                             const uint64_t c = __ldcg(cand + i);
@@ -799,8 +818,7 @@ int launch_score(const lrqk_layer_t &L, const float *ext_scores, cudaStream_t st
 size_t finalize_smem_bytes(const lrqk_layer_t &L) {
     const size_t n_words = ((size_t)L.t_max + 31) / 32;
     const size_t slot_words = ((size_t)L.n_slots + 31) / 32;
-    size_t cand_pow2 = 1;
-    while (cand_pow2 < (size_t)L.cand_cap) cand_pow2 <<= 1;
+    const size_t cand_pow2 = kCritCap;
     const size_t fin = ((n_words + 3) & ~(size_t)3) * 4 + 4 * (size_t)L.s_cap * 4 +
                        ((slot_words + 3) & ~(size_t)3) * 4 + cand_pow2 * 8;
     const size_t scan = (size_t)kLocSure * 4 + (size_t)kLocCand * 8;
