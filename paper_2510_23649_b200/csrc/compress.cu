@@ -264,8 +264,162 @@ __device__ void gram_rows(const float *X, int r, int d, int ldx, float *out, int
 }
 
 // ---------------------------------------------------------------------------
+// K2p reduce on tensor cores (bf16 storage): per 64-row sub-chunk of Omega,
+//     Y += A_sub^T K_sub   (M = r, N = d, K = 64)      G += A_sub^T A_sub
+// with mma.sync m16n8k16 bf16 x bf16 -> fp32.  Products of bf16 values are
+// exact in fp32, so this equals the fp32 CUDA-core accumulation up to
+// summation order.  Rows are gathered into shared memory with cp.async
+// (16-byte LDGSTS) into two buffers, so the next sub-chunk's gather overlaps
+// the current sub-chunk's MMAs; fragments come from ldmatrix.trans.
+// ---------------------------------------------------------------------------
+LRQK_DEV void cp_async16(void *dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src) : "memory");
+}
+LRQK_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> LRQK_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+LRQK_DEV void ldsm_x4_trans(uint32_t (&r)[4], const void *p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+LRQK_DEV void ldsm_x2_trans(uint32_t (&r)[2], const void *p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1]) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+LRQK_DEV void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+constexpr int kMmaRows = 64;  // rows per sub-chunk
+
+// smem bytes of the two gather buffers (row strides padded by 16 bytes)
+__host__ __device__ inline int mma_stage_bytes(int R, int d) { return kMmaRows * ((d * 2 + 16) + (R * 2 + 16)); }
+
+__device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int nrow, const __nv_bfloat16 *kbase,
+                                   const __nv_bfloat16 *proxy, bool host, float *part, uint8_t *smem) {
+    const int d = L.dim_stride, R = L.rank_stride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ldk = d * 2 + 16, lda = R * 2 + 16;  // bytes
+    const int stage = mma_stage_bytes(R, d);
+    const int *ridx = L.res_idx + (size_t)bh * L.s_cap + row0;
+    const int *rslot = L.res_slot + (size_t)bh * L.s_cap + row0;
+    const int MT = R / 16;            // m tiles (rank rows)
+    const int NTW = d / 64;           // n tiles of 8 columns per warp (d / 8 / 8 warps)
+    const int GT = (R / 16) * (R / 8);  // G tiles
+    float yacc[4][4][4];              // [m tile][n tile of this warp][frag]
+    float gacc[4][4];                 // up to 4 G tiles per warp
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) { yacc[a][b2][c] = 0.f; gacc[a][c] = 0.f; }
+    const int nsub = (nrow + kMmaRows - 1) / kMmaRows;
+    auto issue = [&](int sub) {
+        uint8_t *buf = smem + (sub & 1) * stage;
+        uint8_t *kb_s = buf, *ab_s = buf + kMmaRows * ldk;
+        const int s0 = sub * kMmaRows;
+        const int ns = min(kMmaRows, nrow - s0);
+        const int kp = d / 8, ap = R / 8;  // 16-byte packs per row
+        for (int e = tid; e < kMmaRows * (kp + ap); e += blockDim.x) {
+            if (e < kMmaRows * kp) {
+                const int j = e / kp, pk = e - j * kp;
+                if (j < ns) {
+                    const int src = host ? rslot[s0 + j] : ridx[s0 + j];
+                    cp_async16(kb_s + j * ldk + pk * 16, kbase + (size_t)src * d + pk * 8);
+                } else {
+                    *reinterpret_cast<uint4 *>(kb_s + j * ldk + pk * 16) = make_uint4(0, 0, 0, 0);
+                }
+            } else {
+                const int e2 = e - kMmaRows * kp;
+                const int j = e2 / ap, pk = e2 - j * ap;
+                if (j < ns) cp_async16(ab_s + j * lda + pk * 16, proxy + proxy_pack_offset(ridx[s0 + j], pk, ap) * 8);
+                else *reinterpret_cast<uint4 *>(ab_s + j * lda + pk * 16) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        cp_async_commit();
+    };
+    if (nsub > 0) issue(0);
+    for (int sub = 0; sub < nsub; ++sub) {
+        if (sub + 1 < nsub) { issue(sub + 1); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        __syncthreads();
+        const uint8_t *buf = smem + (sub & 1) * stage;
+        const uint8_t *kb_s = buf, *ab_s = buf + kMmaRows * ldk;
+        const int q = lane >> 3, i8 = lane & 7;
+#pragma unroll
+        for (int ks = 0; ks < kMmaRows; ks += 16) {
+            // A fragments (A_mat[m][k] = A_sm[k][m]) for every m tile
+            uint32_t af[4][4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                if (mt >= MT) break;
+                const int m0 = mt * 16 + ((q & 1) ? 8 : 0), k0 = ks + ((q & 2) ? 8 : 0);
+                ldsm_x4_trans(af[mt], ab_s + (k0 + i8) * lda + m0 * 2);
+            }
+            // Y: this warp's n tiles (columns warp*8*NTW ...)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+                if (nt >= NTW) break;
+                const int n0 = (warp * NTW + nt) * 8;
+                uint32_t bfr[2];
+                const int k0 = ks + ((lane >> 3) & 1) * 8;  // lanes 0-7: k 0-7, 8-15: k 8-15
+                ldsm_x2_trans(bfr, kb_s + (k0 + i8) * ldk + n0 * 2);
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) {
+                    if (mt >= MT) break;
+                    mma_bf16_16816(yacc[mt][nt], af[mt], bfr);
+                }
+            }
+            // G tiles owned by this warp: tile g = warp + 8*w2
+#pragma unroll
+            for (int w2 = 0; w2 < 4; ++w2) {
+                const int gtile = warp + 8 * w2;
+                if (gtile >= GT) break;
+                const int mt = gtile / (R / 8), n0 = (gtile % (R / 8)) * 8;
+                uint32_t bfr[2];
+                const int k0 = ks + ((lane >> 3) & 1) * 8;
+                ldsm_x2_trans(bfr, ab_s + (k0 + i8) * lda + n0 * 2);
+                mma_bf16_16816(gacc[w2], af[mt], bfr);
+            }
+        }
+        __syncthreads();
+    }
+    // accumulator fragments -> partial (Y row-major R x d, then G R x R)
+    const int fr = lane >> 2, fc = (lane & 3) * 2;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+        if (mt >= MT) break;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+            if (nt >= NTW) break;
+            const int n0 = (warp * NTW + nt) * 8;
+            float *y = part + (mt * 16 + fr) * d + n0 + fc;
+            *reinterpret_cast<float2 *>(y) = make_float2(yacc[mt][nt][0], yacc[mt][nt][1]);
+            *reinterpret_cast<float2 *>(y + 8 * d) = make_float2(yacc[mt][nt][2], yacc[mt][nt][3]);
+        }
+    }
+#pragma unroll
+    for (int w2 = 0; w2 < 4; ++w2) {
+        const int gtile = warp + 8 * w2;
+        if (gtile >= GT) break;
+        const int mt = gtile / (R / 8), n0 = (gtile % (R / 8)) * 8;
+        float *gp = part + R * d + (mt * 16 + fr) * R + n0 + fc;
+        *reinterpret_cast<float2 *>(gp) = make_float2(gacc[w2][0], gacc[w2][1]);
+        *reinterpret_cast<float2 *>(gp + 8 * R) = make_float2(gacc[w2][2], gacc[w2][3]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K2p: compress_prepare
 // ---------------------------------------------------------------------------
+template <typename T> constexpr bool kUseMma = false;
+template <> constexpr bool kUseMma<__nv_bfloat16> = true;
+
 template <typename T>
 __global__ void __launch_bounds__(kCompressThreads, 2)
 prepare_kernel(const lrqk_layer_t L) {
@@ -293,7 +447,14 @@ prepare_kernel(const lrqk_layer_t L) {
     constexpr int N = Pack<T>::N;
 
     trace(10);
-    if ((int)blockIdx.x < nchunks) {
+    if ((int)blockIdx.x < nchunks && kUseMma<T> && R >= 16 && d >= 64) {
+        const int row0 = blockIdx.x * kRedRows;
+        const int nrow = max(0, min(kRedRows, n_prev - row0));
+        prepare_reduce_mma(L, bh, row0, nrow, reinterpret_cast<const __nv_bfloat16 *>(kbase),
+                           reinterpret_cast<const __nv_bfloat16 *>(proxy), host,
+                           hs + (size_t)blockIdx.x * (R * d + R * R), reinterpret_cast<uint8_t *>(smem));
+        trace(11);
+    } else if ((int)blockIdx.x < nchunks) {
         // ---- reduce: Y = A^T K and G = A^T A over this chunk of Omega ------
         const int row0 = blockIdx.x * kRedRows;
         const int nrow = max(0, min(kRedRows, n_prev - row0));
@@ -868,8 +1029,9 @@ static size_t prepare_smem_bytes(const lrqk_layer_t &L) {
     const size_t RB = R / 4, NP = RB * (RB + 1) / 2;
     const size_t NG = NP >= (size_t)kCompressThreads ? 1 : kCompressThreads / NP;
     const size_t ldB = d + 4, ldM = R + 4;
-    const size_t a = std::max(((size_t)kSub * ldB + (size_t)kSub * (R + 4) + NG * NP * 16) * sizeof(float),
-                              (size_t)8192 * sizeof(float));
+    const size_t a = std::max(std::max(((size_t)kSub * ldB + (size_t)kSub * (R + 4) + NG * NP * 16) * sizeof(float),
+                                       (size_t)8192 * sizeof(float)),
+                              (size_t)2 * mma_stage_bytes((int)R, (int)d));
     const size_t p = (2 * R * ldB + R * ldM + 2 * NP * 16) * sizeof(float);
     const size_t f = (R * ldB + R * ldM) * sizeof(float);
     return std::max(a, std::max(p, f));

@@ -537,7 +537,9 @@ select_kernel(const lrqk_layer_t L, int parts) {
             for (int i = tid; i < kHistBins; i += nt)
                 if (s_hist[i]) atomicAdd(hist2 + i, (uint32_t)s_hist[i]);
         }
+        trace(21);
         if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_SELECT, parts, &s_flag)) continue;
+        trace(22);
 
         // ================= finalize (one block per head) =====================
         const int n_words = (lite_start + 31) >> 5;
@@ -620,6 +622,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
                 for (int i = tid; i < lite_start; i += nt)
                     if (make_comp(__ldcg(keys + i), i) >= thr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
             }
+            trace(23);
             __syncthreads();
             // ascending compaction of the bitmap
             const int per = (n_words + nt - 1) / nt;
@@ -640,6 +643,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
         }
         for (int i = tid; i < t + 1 - lite_start; i += nt) newl[k_eff + i] = lite_start + i;  // omega_l
 
+        trace(24);
         // ---- K5: hit/miss against Omega_{t-1} U {t} ---------------------------
         const int n_prev = L.res_cnt[bh];
         int *res_idx = L.res_idx + (size_t)bh * L.s_cap;
@@ -652,6 +656,16 @@ select_kernel(const lrqk_layer_t L, int parts) {
         __syncthreads();
         const int spare = host ? L.spare_slot[bh] : 0;
         int hits_local = 0;
+        if (!host) {
+            // |Omega_t ∩ (Omega_{t-1} ∪ {t})| = 1 + #{x in Omega_{t-1} : x in Omega_t}, with
+            // membership read straight off the selection bitmap (t is never in Omega_{t-1})
+            if (tid == 0) hits_local = 1;
+            for (int i = tid; i < n_prev; i += nt) {
+                const int x = prevl[i];
+                const bool in_new = mode0 == 1 || x >= lite_start || ((bitmap[x >> 5] >> (x & 31)) & 1u);
+                hits_local += in_new ? 1 : 0;
+            }
+        } else
         for (int i = tid; i < S; i += nt) {
             const int x = newl[i];
             int pos = -1;
@@ -737,6 +751,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
             meta[M_SURE] = 0;
             meta[M_CAND] = 0;
         }
+        trace(25);
         uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;  // both levels, ready for the next step
         for (int i = tid; i < 2 * kHistBins; i += nt) ghist[i] = 0u;
         __syncthreads();
@@ -827,7 +842,7 @@ size_t finalize_smem_bytes(const lrqk_layer_t &L) {
 
 int launch_select(const lrqk_layer_t &L, cudaStream_t st) {
     const int BH = L.batch * L.n_q_heads;
-    const int parts = max(1, min((num_sms() * 2 + BH - 1) / BH, max(1, L.t_max / 4096)));
+    const int parts = max(1, min((num_sms() * 2) / BH, max(1, L.t_max / 4096)));
     const int grid = max(1, min(BH * parts, num_sms() * 2));
     const size_t smem = finalize_smem_bytes(L);
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
