@@ -172,6 +172,24 @@ int lrqk_select_scores(const float *scores, int32_t n_heads, int32_t t, int32_t 
                        void *workspace, size_t workspace_bytes, void *stream);
 size_t lrqk_select_scores_workspace(int32_t n_heads, int32_t t, int32_t k_budget, int32_t lite_budget);
 
+/* Standalone exact attention over explicit fp32 rows (drop-in
+ * exact_attention, attention.py:23-34): q [H][ld], K/V [H][n][ld];
+ * out [H][ld], weights [H][n] (may be NULL). */
+int lrqk_attention_rows(const float *q, const float *K, const float *V, int32_t n_heads, int32_t n_rows,
+                        int32_t head_dim, int32_t ld, float *out, float *weights, void *stream);
+
+/* Hit/miss accounting of an explicit selection against an ascending
+ * resident set (drop-in fetch_and_merge, cache.py:174-196):
+ * out3 = {misses, selected, any index outside [0, size)}. */
+int lrqk_count_misses(const int32_t *resident, int32_t n_resident, const int32_t *omega, int32_t n_selected,
+                      int32_t size, int32_t *out3, void *stream);
+
+/* Standalone exact line-search step on one B factor (drop-in
+ * update_projections, decode.py:150-184): x_hat [H][r], B [H][r][d],
+ * x [H][d] -> B_out, grad (may be NULL) [H][r][d], eta [H]. */
+int lrqk_line_search(const float *x_hat, const float *B, const float *x, int32_t n_heads, int32_t rank,
+                     int32_t dim, float *B_out, float *grad, float *eta, void *stream);
+
 /* ---- prefill factorisation (ref: prefill.py:197-230) ---- */
 typedef struct lrqk_prefill {
     int32_t n_heads;        /* independent (Q,K) problems                     */

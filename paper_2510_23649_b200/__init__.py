@@ -1,8 +1,10 @@
 """B200-native LRQK decode-time sparse-attention path (arXiv 2510.23649).
 
 Drop-in for the reference package's prefill / decode / cache-manager /
-attention API (ref: pkg/src/lrqk/__init__.py:10-82), computed by hand-written
-sm_100a CUDA kernels behind a C-ABI (include/lrqk_b200.h).  There is no CPU
+attention API (ref: pkg/src/lrqk/__init__.py:10-82): the same names are
+re-exported flat from this package, computed by hand-written sm_100a CUDA
+kernels behind a C-ABI (include/lrqk_b200.h).  The batched multi-layer
+engine (`Engine`, `LayerState`) is the throughput path.  There is no CPU
 fallback: without the library or a CUDA device every compute call raises
 LibraryUnavailable.
 """
@@ -10,5 +12,45 @@ LibraryUnavailable.
 from .errors import CorruptTraceError, NonFiniteError, SolveFailedError, UnsupportedVersionError
 from ._lib import LibraryUnavailable, load_library
 from .engine import Engine, LayerShape, LayerState, prefill_factorize_device
+from .api import (
+    AttentionResult,
+    CacheStats,
+    CompressedToken,
+    DecodeConfig,
+    DecodeSession,
+    DecodeWorkspace,
+    ImportanceScores,
+    InitStrategy,
+    LowRankFactors,
+    PrefillConfig,
+    PrefillRun,
+    SelectionSet,
+    SessionConfig,
+    SimulationResult,
+    StepReport,
+    TieredKVCache,
+    TokenStep,
+    append_token,
+    as_matrix,
+    as_row,
+    decode_compress,
+    exact_attention,
+    exact_topk,
+    fetch_and_merge,
+    importance_scores,
+    init_factors,
+    miss_rate,
+    prefill_factorize,
+    prefill_run,
+    proxy_scores,
+    run_simulation,
+    select_active,
+    selection_recall,
+    summarize,
+    topk_indices,
+    update_projections,
+    write_report_csv,
+    write_stats_csv,
+)
 
 __version__ = "0.1.0"

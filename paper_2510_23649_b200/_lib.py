@@ -89,6 +89,9 @@ SIGNATURES = {
     "lrqk_host_alloc": (_P, [C.c_size_t]),
     "lrqk_host_free": (None, [_P]),
     "lrqk_host_device_ptr": (_P, [_P]),
+    "lrqk_attention_rows": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
+    "lrqk_count_misses": (C.c_int, [_P, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P]),
+    "lrqk_line_search": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P]),
     "lrqk_trace_enable": (C.c_int, [C.c_int]),
     "lrqk_trace_read": (C.c_int, [_P, C.c_int]),
 }

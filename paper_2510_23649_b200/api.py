@@ -1,0 +1,787 @@
+"""Drop-in mirror of the reference package's public API for the decode-time
+sparse-attention path (ref: pkg/src/lrqk/__init__.py:10-82).
+
+Same names, dataclasses, argument meaning and errors as the reference
+(`NonFiniteError`, `SolveFailedError`, `ValueError`, `IndexError`,
+`RuntimeError`); every numeric result is computed by the sm_100a kernels
+behind include/lrqk_b200.h (fp32 storage, fp32 arithmetic), and returned as
+float64 numpy arrays like the reference's.  Without the CUDA library or a
+device every call raises LibraryUnavailable -- there is no CPU fallback.
+
+Implemented entry points and the kernels behind them:
+  prefill_run / prefill_factorize  -> lrqk_prefill_factorize   (prefill.py:197-230)
+  init_factors, importance_scores  -> host initialisation, as the reference (prefill.py:108-139)
+  decode_compress                  -> lrqk_compress_prepare + lrqk_decode_compress (decode.py:122-147)
+  update_projections               -> B update of the same kernel    (decode.py:169-184)
+  proxy_scores                     -> lrqk_proxy_scores_f32          (cache.py:141-146)
+  select_active, topk_indices      -> lrqk_select_scores             (cache.py:149-171, linalg.py:96-110)
+  fetch_and_merge                  -> lrqk_count_misses              (cache.py:174-196)
+  exact_attention, exact_topk      -> lrqk_attention_rows / select   (attention.py:23-41)
+  DecodeSession, run_simulation    -> the fused per-layer decode step (session.py:62-165)
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes as C
+import math
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .engine import LayerShape, LayerState, pad_last, pow2_at_least, prefill_factorize_device
+from .errors import NonFiniteError, SolveFailedError
+
+INIT_KINDS = ("randn", "top", "topcol")
+JITTER_EPS = 1e-10     # ref: linalg.py:19
+ETA_DENOM_FLOOR = 1e-14  # ref: decode.py:26
+
+
+def _dev():
+    _lib.lib()  # raises LibraryUnavailable without a device / library
+    return torch.device("cuda")
+
+
+def _f32(x, dev=None):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32), device=dev or _dev())
+
+
+def _np64(t):
+    return t.detach().double().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# validation gate (ref: linalg.py:22-45)
+# ---------------------------------------------------------------------------
+def as_matrix(a, name: str = "matrix") -> np.ndarray:
+    out = np.ascontiguousarray(a, dtype=np.float64)
+    if out.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {out.shape}")
+    if not np.isfinite(out).all():
+        raise NonFiniteError(f"{name} contains non-finite entries")
+    return out
+
+
+def as_row(a, name: str = "row") -> np.ndarray:
+    arr = np.asarray(a, dtype=np.float64)
+    if arr.ndim == 1:
+        arr = arr[None, :]
+    out = as_matrix(arr, name)
+    if out.shape[0] != 1:
+        raise ValueError(f"{name} must be a single row, got shape {out.shape}")
+    return out
+
+
+# ---------------------------------------------------------------------------
+# selection (ref: linalg.py:96-110, cache.py:149-171)
+# ---------------------------------------------------------------------------
+def _select_device(scores_2d: torch.Tensor, t: int, k_budget: int, lite_budget: int):
+    """scores_2d [H, t+1] f32 on device -> (omega [H, s_cap] int32, counts [H])."""
+    lib = _lib.lib()
+    H = scores_2d.shape[0]
+    ws_bytes = lib.lrqk_select_scores_workspace(H, t, k_budget, lite_budget)
+    ws = torch.empty(max(256, ws_bytes), dtype=torch.uint8, device=scores_2d.device)
+    omega = torch.empty(H, k_budget + lite_budget, dtype=torch.int32, device=scores_2d.device)
+    cnt = torch.empty(H, dtype=torch.int32, device=scores_2d.device)
+    _lib.check(lib.lrqk_select_scores(scores_2d.data_ptr(), H, t, k_budget, lite_budget, omega.data_ptr(),
+                                      cnt.data_ptr(), ws.data_ptr(), ws_bytes, _lib.stream_ptr()),
+               "lrqk_select_scores")
+    return omega, cnt
+
+
+def topk_indices(scores, k: int) -> np.ndarray:
+    """Indices of the k largest scores, ascending; ties toward the lower index."""
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    s = np.asarray(scores, dtype=np.float64).ravel()
+    n = s.shape[0]
+    if k >= n:
+        return np.arange(n)
+    # one extra token fills the (mandatory) lite window, so omega_k is the
+    # plain top-k over the n real scores
+    dev = _dev()
+    padded = torch.empty(1, n + 1, dtype=torch.float32, device=dev)
+    padded[0, :n] = _f32(s, dev)
+    padded[0, n] = float("-inf")
+    omega, cnt = _select_device(padded, n, k, 1)
+    got = omega[0, : int(cnt[0])].cpu().numpy().astype(np.int64)
+    return got[got < n]
+
+
+@dataclass
+class SelectionSet:
+    omega_k: np.ndarray
+    omega_l: np.ndarray
+    omega: np.ndarray
+
+
+def select_active(scores, t: int, k_budget: int, lite_budget: int) -> SelectionSet:
+    s = np.asarray(scores, dtype=np.float64).ravel()
+    if s.shape[0] != t + 1:
+        raise ValueError(f"scores must cover tokens 0..{t}, got {s.shape[0]}")
+    omega, cnt = _select_device(_f32(s[None, :]), t, k_budget, lite_budget)
+    om = omega[0, : int(cnt[0])].cpu().numpy().astype(np.intp)
+    lite_start = max(0, t + 1 - lite_budget)
+    return SelectionSet(omega_k=om[om < lite_start], omega_l=om[om >= lite_start], omega=om)
+
+
+# ---------------------------------------------------------------------------
+# proxy scores (ref: cache.py:141-146)
+# ---------------------------------------------------------------------------
+def proxy_scores(q_hat, proxy_store) -> np.ndarray:
+    store = np.asarray(proxy_store, dtype=np.float64)
+    qh = np.asarray(q_hat, dtype=np.float64).reshape(1, -1)
+    t, r = store.shape
+    if t == 0:
+        return np.zeros(0)
+    dev = _dev()
+    rs = pow2_at_least(r)
+    st = pad_last(_f32(store, dev), rs).contiguous()
+    q = pad_last(_f32(qh, dev), rs).contiguous()
+    out = torch.empty(t, dtype=torch.float32, device=dev)
+    _lib.check(_lib.lib().lrqk_proxy_scores_f32(st.data_ptr(), _lib.F32, q.data_ptr(), out.data_ptr(), 1, t, rs,
+                                                 _lib.stream_ptr()), "lrqk_proxy_scores_f32")
+    return _np64(out)
+
+
+# ---------------------------------------------------------------------------
+# attention (ref: attention.py:23-50)
+# ---------------------------------------------------------------------------
+@dataclass
+class AttentionResult:
+    output: np.ndarray
+    weights: np.ndarray
+
+
+def _attention_device(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, d: int, want_weights=True):
+    H, n, ld = K.shape
+    out = torch.empty(H, ld, dtype=torch.float32, device=K.device)
+    w = torch.empty(H, n, dtype=torch.float32, device=K.device) if want_weights else None
+    _lib.check(_lib.lib().lrqk_attention_rows(q.data_ptr(), K.data_ptr(), V.data_ptr(), H, n, d, ld, out.data_ptr(),
+                                               w.data_ptr() if w is not None else None, _lib.stream_ptr()),
+               "lrqk_attention_rows")
+    return out, w
+
+
+def exact_attention(q, K, V) -> AttentionResult:
+    K = np.asarray(K, dtype=np.float64)
+    V = np.asarray(V, dtype=np.float64)
+    n, d = K.shape
+    if n == 0:
+        raise ValueError("exact_attention requires at least one key")
+    if V.shape[0] != n:
+        raise ValueError(f"K has {n} rows but V has {V.shape[0]}")
+    dev = _dev()
+    out, w = _attention_device(_f32(np.asarray(q).reshape(1, d), dev), _f32(K[None], dev), _f32(V[None], dev), d)
+    return AttentionResult(output=_np64(out[:, :d]), weights=_np64(w[0]))
+
+
+def exact_topk(q, K, k: int) -> np.ndarray:
+    K = np.asarray(K, dtype=np.float64)
+    if K.shape[0] == 0:
+        raise ValueError("exact_topk requires at least one key")
+    return topk_indices(proxy_scores(np.asarray(q).reshape(1, -1), K), k)
+
+
+def selection_recall(proxy, exact) -> float:
+    exact = set(int(i) for i in exact)
+    if not exact:
+        raise ValueError("selection_recall undefined for an empty exact set")
+    proxy = set(int(i) for i in proxy)
+    return len(proxy & exact) / len(exact)
+
+
+# ---------------------------------------------------------------------------
+# prefill (ref: prefill.py)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class InitStrategy:
+    kind: str = "randn"
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.kind not in INIT_KINDS:
+            raise ValueError(f"init kind must be one of {INIT_KINDS}, got {self.kind!r}")
+
+
+@dataclass(frozen=True)
+class PrefillConfig:
+    rank: int = 32
+    lambda_q: float = 1.0
+    lambda_k: float = 1.0
+    max_iter: int = 2
+    tol: float = 1e-2
+    init: InitStrategy = field(default_factory=InitStrategy)
+
+    def __post_init__(self):
+        if self.rank < 1:
+            raise ValueError(f"rank must be >= 1, got {self.rank}")
+        if self.lambda_q < 0 or self.lambda_k < 0:
+            raise ValueError("lambda_q and lambda_k must be >= 0")
+        if self.max_iter < 1:
+            raise ValueError(f"max_iter must be >= 1, got {self.max_iter}")
+        if self.tol <= 0:
+            raise ValueError(f"tol must be > 0, got {self.tol}")
+
+
+@dataclass
+class LowRankFactors:
+    A_Q: np.ndarray
+    A_K: np.ndarray
+    B_Q: np.ndarray
+    B_K: np.ndarray
+
+    @property
+    def rank(self) -> int:
+        return self.A_Q.shape[1]
+
+    def copy(self) -> "LowRankFactors":
+        return LowRankFactors(self.A_Q.copy(), self.A_K.copy(), self.B_Q.copy(), self.B_K.copy())
+
+
+@dataclass(frozen=True)
+class ImportanceScores:
+    s_q: np.ndarray
+    s_k: np.ndarray
+    s_qk: np.ndarray
+
+
+@dataclass
+class PrefillRun:
+    factors: LowRankFactors
+    objective: list
+    sweeps: int
+    converged: bool
+
+
+def importance_scores(Q, K) -> ImportanceScores:
+    """ref: prefill.py:108-113 (host-side initialisation helper)."""
+    Q, K = np.asarray(Q, dtype=np.float64), np.asarray(K, dtype=np.float64)
+    if Q.shape != K.shape:
+        raise ValueError(f"Q and K must share a shape, got {Q.shape} vs {K.shape}")
+    s_q = np.abs(Q).sum(axis=0)
+    s_k = np.abs(K).sum(axis=0)
+    return ImportanceScores(s_q=s_q, s_k=s_k, s_qk=s_q + s_k)
+
+
+def _host_topk(scores, k):
+    s = np.asarray(scores, dtype=np.float64)
+    if k >= s.size:
+        return np.arange(s.size)
+    return np.sort(np.lexsort((np.arange(s.size), -s))[:k])
+
+
+def init_factors(Q, K, cfg: PrefillConfig) -> LowRankFactors:
+    """Initial A_Q, A_K (ref: prefill.py:116-139).  Like the reference this
+    runs on the host: a PCG64 draw or a column pick, uploaded once."""
+    Q, K = np.asarray(Q, dtype=np.float64), np.asarray(K, dtype=np.float64)
+    if Q.shape != K.shape:
+        raise ValueError(f"Q and K must share a shape, got {Q.shape} vs {K.shape}")
+    l, d = Q.shape
+    r = cfg.rank
+    if r > d:
+        raise ValueError(f"rank {r} exceeds head dimension {d}")
+    if cfg.init.kind == "randn":
+        rng = np.random.default_rng(cfg.init.seed)
+        A_Q = rng.standard_normal((l, r))
+        A_K = rng.standard_normal((l, r))
+    else:
+        sc = importance_scores(Q, K)
+        if cfg.init.kind == "top":
+            A_Q = Q[:, _host_topk(sc.s_q, r)].copy()
+            A_K = K[:, _host_topk(sc.s_k, r)].copy()
+        else:
+            cols = _host_topk(sc.s_qk, r)
+            A_Q, A_K = Q[:, cols].copy(), K[:, cols].copy()
+    return LowRankFactors(A_Q=A_Q, A_K=A_K, B_Q=np.zeros((r, d)), B_K=np.zeros((r, d)))
+
+
+def prefill_run(Q, K, cfg: PrefillConfig) -> PrefillRun:
+    Q = as_matrix(Q, "Q")
+    K = as_matrix(K, "K")
+    if Q.shape != K.shape:
+        raise ValueError(f"Q and K must share a shape, got {Q.shape} vs {K.shape}")
+    f0 = init_factors(Q, K, cfg)
+    dev = _dev()
+    res = prefill_factorize_device(_f32(Q[None], dev), _f32(K[None], dev), cfg.rank, lambda_q=cfg.lambda_q,
+                                   lambda_k=cfg.lambda_k, max_iter=cfg.max_iter, tol=cfg.tol, A_Q0=f0.A_Q,
+                                   A_K0=f0.A_K, want_objective=True, dtype="f32")
+    sweeps = int(res["sweeps"][0])
+    obj = [float(x) for x in res["objective"][0, : sweeps + 1].cpu()]
+    f = LowRankFactors(A_Q=_np64(res["A_Q"][0]), A_K=_np64(res["A_K"][0]), B_Q=_np64(res["B_Q"][0]),
+                       B_K=_np64(res["B_K"][0]))
+    return PrefillRun(factors=f, objective=obj, sweeps=sweeps, converged=bool(res["converged"][0]))
+
+
+def prefill_factorize(Q, K, cfg: PrefillConfig) -> LowRankFactors:
+    return prefill_run(Q, K, cfg).factors
+
+
+# ---------------------------------------------------------------------------
+# decode compression (ref: decode.py)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class DecodeConfig:
+    lambda_1: float = 1.0
+    lambda_2: float = 1.0
+    max_iter: int = 2
+    tol: float = 1e-2
+
+    def __post_init__(self):
+        if self.lambda_1 < 0 or self.lambda_2 < 0:
+            raise ValueError("lambda_1 and lambda_2 must be >= 0")
+        if self.max_iter < 1:
+            raise ValueError(f"max_iter must be >= 1, got {self.max_iter}")
+        if self.tol <= 0:
+            raise ValueError(f"tol must be > 0, got {self.tol}")
+
+
+@dataclass(frozen=True)
+class TokenStep:
+    q: np.ndarray
+    k: np.ndarray
+    v: np.ndarray
+
+    def __post_init__(self):
+        if not (self.q.shape == self.k.shape == self.v.shape):
+            raise ValueError("q, k, v must share the same 1 x d shape")
+
+
+@dataclass
+class CompressedToken:
+    q_hat: np.ndarray
+    k_hat: np.ndarray
+
+
+@dataclass
+class DecodeWorkspace:
+    """The reference's per-step intermediates.  The GPU path keeps the step
+    sizes and gradients (rank-1: x_hat^T resid); the normal-system matrices
+    live on the device only and are left as None."""
+
+    m_lq: np.ndarray | None = None
+    M_rq: np.ndarray | None = None
+    grad_BQ: np.ndarray | None = None
+    grad_BK: np.ndarray | None = None
+    eta_Q: float = 0.0
+    eta_K: float = 0.0
+
+
+def _one_head_layer(d, r, n_rows, t_max, decode_cfg, k_budget=1, lite_budget=1):
+    shape = LayerShape(batch=1, n_q_heads=1, n_kv_heads=1, head_dim=d, rank=r, k_budget=k_budget,
+                       lite_budget=lite_budget, t_max=t_max, dtype="f32")
+    return LayerState(shape, lambda_1=decode_cfg.lambda_1, lambda_2=decode_cfg.lambda_2,
+                      max_iter=decode_cfg.max_iter, tol=decode_cfg.tol)
+
+
+def _compress_on_device(step: TokenStep, f: LowRankFactors, A_res, K_res, cfg: DecodeConfig, update_b: bool):
+    A_res = np.asarray(A_res, dtype=np.float64)
+    K_res = np.asarray(K_res, dtype=np.float64)
+    if A_res.shape[0] != K_res.shape[0]:
+        raise ValueError(f"resident proxy/key row counts differ: {A_res.shape[0]} vs {K_res.shape[0]}")
+    r, d = f.B_Q.shape
+    n = A_res.shape[0]
+    layer = _one_head_layer(d, r, n, n + 1, cfg, k_budget=max(1, n), lite_budget=1)
+    dev = layer.device
+    lib = _lib.lib()
+    sp = _lib.stream_ptr()
+    rows = max(n, 1)
+    A = np.zeros((rows, r))
+    Kr = np.zeros((rows, d))
+    A[:n], Kr[:n] = A_res, K_res
+    layer.load_prompt(_f32(A[None, None], dev), _f32(f.B_Q[None, None], dev), _f32(f.B_K[None, None], dev),
+                      _f32(Kr[None, None], dev), _f32(Kr[None, None], dev))
+    # the resident set is exactly the given rows (possibly none)
+    layer.view("res_idx")[0, 0, :n] = torch.arange(n, dtype=torch.int32, device=dev)
+    layer.view("res_cnt").fill_(n)
+    _lib.check(lib.lrqk_compress_prepare(layer.ptr, sp), "lrqk_compress_prepare")
+    ds = layer.shape.dim_stride
+    q = pad_last(_f32(step.q, dev), ds).contiguous()
+    k = pad_last(_f32(step.k, dev), ds).contiguous()
+    v = pad_last(_f32(step.v, dev), ds).contiguous()
+    _lib.check(lib.lrqk_decode_compress(layer.ptr, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(update_b), sp),
+               "lrqk_decode_compress")
+    torch.cuda.synchronize()
+    layer.raise_status()
+    return layer
+
+
+def decode_compress(step: TokenStep, f: LowRankFactors, A_K_resident, K_resident, cfg: DecodeConfig):
+    """ref: decode.py:122-147."""
+    layer = _compress_on_device(step, f, A_K_resident, K_resident, cfg, update_b=False)
+    r = f.B_Q.shape[0]
+    comp = CompressedToken(q_hat=_np64(layer.view("q_hat")[0, :, :r]), k_hat=_np64(layer.view("k_hat")[0, :, :r]))
+    return comp, DecodeWorkspace()
+
+
+def update_projections(step: TokenStep, comp: CompressedToken, f: LowRankFactors, ws: DecodeWorkspace):
+    """One exact line-search step on B_Q, B_K (ref: decode.py:150-184),
+    computed by lrqk_line_search; A factors pass through."""
+    r, d = f.B_Q.shape
+    dev = _dev()
+    lib = _lib.lib()
+    xh = _f32(np.vstack([np.asarray(comp.q_hat).reshape(1, r), np.asarray(comp.k_hat).reshape(1, r)]), dev)
+    B = _f32(np.stack([f.B_Q, f.B_K]), dev)
+    x = _f32(np.vstack([np.asarray(step.q).reshape(1, d), np.asarray(step.k).reshape(1, d)]), dev)
+    B_out = torch.empty_like(B)
+    grad = torch.empty_like(B)
+    eta = torch.empty(2, dtype=torch.float32, device=dev)
+    _lib.check(lib.lrqk_line_search(xh.data_ptr(), B.data_ptr(), x.data_ptr(), 2, r, d, B_out.data_ptr(),
+                                    grad.data_ptr(), eta.data_ptr(), _lib.stream_ptr()), "lrqk_line_search")
+    e = eta.cpu().tolist()
+    ws.grad_BQ, ws.grad_BK = _np64(grad[0]), _np64(grad[1])
+    ws.eta_Q, ws.eta_K = float(e[0]), float(e[1])
+    return LowRankFactors(A_Q=f.A_Q, A_K=f.A_K, B_Q=_np64(B_out[0]), B_K=_np64(B_out[1]))
+
+
+# ---------------------------------------------------------------------------
+# cache manager (ref: cache.py)
+# ---------------------------------------------------------------------------
+@dataclass
+class CacheStats:
+    c_miss: int = 0
+    c_total: int = 0
+    per_step: list = field(default_factory=list)
+
+    def record(self, step: int, miss_count: int, selected_count: int) -> None:
+        self.c_miss += miss_count
+        self.c_total += selected_count
+        self.per_step.append((step, miss_count, selected_count))
+
+
+def miss_rate(stats: CacheStats) -> float:
+    if stats.c_total == 0:
+        raise ValueError("miss rate undefined: no selections recorded")
+    return stats.c_miss / stats.c_total
+
+
+class TieredKVCache:
+    """One head's tiered cache: slow tier K/V and the proxy store live on the
+    device; `fast_resident` is the fast-tier index set (ref: cache.py:84-138)."""
+
+    def __init__(self, dim: int, rank: int, k_budget: int, lite_budget: int):
+        if k_budget < 1 or lite_budget < 1:
+            raise ValueError("k_budget and lite_budget must be >= 1")
+        self.dim, self.rank, self.k_budget, self.lite_budget = dim, rank, k_budget, lite_budget
+        self._dev = _dev()
+        self._K = torch.zeros(16, dim, dtype=torch.float32, device=self._dev)
+        self._V = torch.zeros(16, dim, dtype=torch.float32, device=self._dev)
+        self._P = torch.zeros(16, rank, dtype=torch.float32, device=self._dev)
+        self._n = 0
+        self.fast_resident: set[int] = set()
+
+    def _grow(self, need):
+        cap = self._K.shape[0]
+        if need <= cap:
+            return
+        while cap < need:
+            cap *= 2
+        for nm in ("_K", "_V", "_P"):
+            old = getattr(self, nm)
+            new = torch.zeros(cap, old.shape[1], dtype=old.dtype, device=old.device)
+            new[: self._n] = old[: self._n]
+            setattr(self, nm, new)
+
+    def _extend(self, K, V, P):
+        n = K.shape[0]
+        self._grow(self._n + n)
+        self._K[self._n: self._n + n] = _f32(K, self._dev)
+        self._V[self._n: self._n + n] = _f32(V, self._dev)
+        self._P[self._n: self._n + n] = _f32(P, self._dev)
+        self._n += n
+
+    @property
+    def size(self) -> int:
+        return self._n
+
+    @property
+    def proxy_store(self) -> np.ndarray:
+        v = _np64(self._P[: self._n])
+        v.flags.writeable = False
+        return v
+
+    def seed_prompt(self, K, V, A_K) -> None:
+        if not (K.shape[0] == V.shape[0] == A_K.shape[0]):
+            raise ValueError("prompt K, V, and proxy row counts must match")
+        self._extend(np.asarray(K), np.asarray(V), np.asarray(A_K))
+        start = max(0, self.size - self.lite_budget)
+        self.fast_resident = set(range(start, self.size))
+
+    def resident_rows(self):
+        idx = np.array(sorted(self.fast_resident), dtype=np.intp)
+        it = torch.as_tensor(idx, dtype=torch.long, device=self._dev)
+        return idx, _np64(self._P[it]), _np64(self._K[it])
+
+    def slow_rows(self, indices):
+        it = torch.as_tensor(np.asarray(indices, dtype=np.int64), device=self._dev)
+        return _np64(self._K[it]), _np64(self._V[it])
+
+    def full_history(self):
+        K, V = _np64(self._K[: self._n]), _np64(self._V[: self._n])
+        K.flags.writeable = False
+        V.flags.writeable = False
+        return K, V
+
+
+def append_token(cache: TieredKVCache, k, v, k_hat) -> int:
+    """ref: cache.py:199-214."""
+    t = cache.size
+    cache._extend(np.asarray(k).reshape(1, -1), np.asarray(v).reshape(1, -1), np.asarray(k_hat).reshape(1, -1))
+    cache.fast_resident.add(t)
+    return t
+
+
+def fetch_and_merge(cache: TieredKVCache, sel: SelectionSet, stats: CacheStats):
+    """ref: cache.py:174-196 (miss counting by lrqk_count_misses)."""
+    dev = cache._dev
+    omega = np.unique(np.asarray(sel.omega, dtype=np.int64))
+    res = np.array(sorted(cache.fast_resident), dtype=np.int32)
+    out = torch.zeros(3, dtype=torch.int32, device=dev)
+    om_t = torch.as_tensor(omega.astype(np.int32), device=dev)
+    res_t = torch.as_tensor(res, device=dev) if res.size else torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().lrqk_count_misses(res_t.data_ptr(), int(res.size), om_t.data_ptr(), int(omega.size),
+                                             cache.size, out.data_ptr(), _lib.stream_ptr()), "lrqk_count_misses")
+    miss, total, bad = (int(x) for x in out.cpu())
+    if bad:
+        lo, hi = int(omega.min()), int(omega.max())
+        raise IndexError(f"selection references token {hi if hi >= cache.size else lo}, "
+                         f"valid range is 0..{cache.size - 1}")
+    stats.record(step=cache.size - 1, miss_count=miss, selected_count=total)
+    K, V = cache.slow_rows(np.sort(np.asarray(sel.omega)))
+    cache.fast_resident = set(int(i) for i in omega)
+    return K, V
+
+
+def write_stats_csv(path, stats: CacheStats) -> None:
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["step", "selected", "miss", "hit", "miss_rate"])
+        for step, miss, selected in stats.per_step:
+            w.writerow([step, selected, miss, selected - miss, repr(miss / selected if selected else 0.0)])
+
+
+# ---------------------------------------------------------------------------
+# session (ref: session.py)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SessionConfig:
+    prefill: PrefillConfig = field(default_factory=PrefillConfig)
+    decode: DecodeConfig = field(default_factory=DecodeConfig)
+    k_budget: int = 2048
+    lite_budget: int = 64
+
+    def __post_init__(self):
+        if self.k_budget < 1 or self.lite_budget < 1:
+            raise ValueError("k_budget and lite_budget must be >= 1")
+
+
+@dataclass
+class StepReport:
+    step: int
+    selected_count: int
+    miss_count: int
+    recall_vs_exact: float
+    output_err: float
+
+
+@dataclass
+class SimulationResult:
+    reports: list
+    stats: CacheStats
+    session: "DecodeSession"
+
+
+class _SessionCacheView:
+    """Read-only view of a session's device cache with the reference's
+    TieredKVCache accessors (size, proxy_store, fast_resident, ...)."""
+
+    def __init__(self, session: "DecodeSession"):
+        self._s = session
+
+    @property
+    def size(self) -> int:
+        return self._s._t
+
+    @property
+    def proxy_store(self) -> np.ndarray:
+        L = self._s._layer
+        v = _np64(L.proxy_rows()[0, 0, : self.size, : L.shape.rank])
+        v.flags.writeable = False
+        return v
+
+    @property
+    def fast_resident(self) -> set:
+        L = self._s._layer
+        n = int(L.view("res_cnt")[0, 0])
+        return set(int(i) for i in L.view("res_idx")[0, 0, :n].cpu())
+
+    def resident_rows(self):
+        idx = np.array(sorted(self.fast_resident), dtype=np.intp)
+        P = self.proxy_store
+        K, _ = self.full_history()
+        return idx, P[idx], K[idx]
+
+    def slow_rows(self, indices):
+        K, V = self.full_history()
+        return K[indices], V[indices]
+
+    def full_history(self):
+        L = self._s._layer
+        d = L.shape.head_dim
+        K = _np64(L.view("slow_k")[0, 0, : self.size, :d])
+        V = _np64(L.view("slow_v")[0, 0, : self.size, :d])
+        return K, V
+
+
+class DecodeSession:
+    """One head's lifecycle on the GPU: prefill once, then step tokens
+    (ref: session.py:62-131)."""
+
+    def __init__(self, cfg: SessionConfig):
+        self.cfg = cfg
+        self.factors: LowRankFactors | None = None
+        self.cache = None
+        self.stats = CacheStats()
+        self.last_selection: SelectionSet | None = None
+        self.last_output: np.ndarray | None = None
+        self._layer = None
+        self._t = 0
+
+    def _alloc(self, t_max):
+        c = self.cfg
+        d = self._d
+        shape = LayerShape(batch=1, n_q_heads=1, n_kv_heads=1, head_dim=d, rank=c.prefill.rank,
+                           k_budget=c.k_budget, lite_budget=c.lite_budget, t_max=t_max, dtype="f32")
+        return LayerState(shape, lambda_1=c.decode.lambda_1, lambda_2=c.decode.lambda_2,
+                          max_iter=c.decode.max_iter, tol=c.decode.tol)
+
+    def prefill(self, Q, K, V) -> LowRankFactors:
+        Q = as_matrix(Q, "Q")
+        K = as_matrix(K, "K")
+        V = as_matrix(V, "V")
+        if not (Q.shape == K.shape == V.shape):
+            raise ValueError("prompt Q, K, V must share one l x d shape")
+        run = prefill_run(Q, K, self.cfg.prefill)
+        self.factors = run.factors
+        l, self._d = Q.shape
+        self._layer = self._alloc(max(2 * l, l + 256))
+        dev = self._layer.device
+        self._layer.load_prompt(_f32(self.factors.A_K[None, None], dev), _f32(self.factors.B_Q[None, None], dev),
+                                _f32(self.factors.B_K[None, None], dev), _f32(K[None, None], dev),
+                                _f32(V[None, None], dev))
+        self._t = l
+        self.cache = _SessionCacheView(self)
+        return self.factors
+
+    def _regrow(self):
+        """Double the store capacity (the reference's _RowStore growth)."""
+        old = self._layer
+        new = self._alloc(2 * old.shape.t_max)
+        t = self._t
+        for nm in ("B_Q", "B_K", "res_idx", "res_cnt", "c_miss", "c_total", "ctx_len"):
+            new.view(nm).copy_(old.view(nm))
+        new.view("slow_k")[:, :, :t].copy_(old.view("slow_k")[:, :, :t])
+        new.view("slow_v")[:, :, :t].copy_(old.view("slow_v")[:, :, :t])
+        tl = (t + 31) // 32
+        new.proxy_tiles()[:, :, :tl].copy_(old.proxy_tiles()[:, :, :tl])
+        new.buf["pre"].copy_(old.buf["pre"])
+        self._layer = new
+
+    def decode_step(self, q, k, v, compute_metrics: bool = True) -> StepReport:
+        if self.factors is None or self._layer is None:
+            raise RuntimeError("decode_step called before prefill")
+        step = TokenStep(q=as_row(q, "q"), k=as_row(k, "k"), v=as_row(v, "v"))
+        if self._t + 1 >= self._layer.shape.t_max:
+            self._regrow()
+        L = self._layer
+        dev = L.device
+        ds = L.shape.dim_stride
+        qd = pad_last(_f32(step.q, dev), ds).contiguous()
+        kd = pad_last(_f32(step.k, dev), ds).contiguous()
+        vd = pad_last(_f32(step.v, dev), ds).contiguous()
+        out = torch.zeros(1, 1, ds, dtype=torch.float32, device=dev)
+        L.step(qd, kd, vd, out, advance=True)
+        torch.cuda.synchronize()
+        L.raise_status()
+        t = self._t
+        self._t += 1
+        n = int(L.view("res_cnt")[0, 0])
+        omega = L.view("res_idx")[0, 0, :n].cpu().numpy().astype(np.intp)
+        lite_start = max(0, t + 1 - self.cfg.lite_budget)
+        self.last_selection = SelectionSet(omega_k=omega[omega < lite_start], omega_l=omega[omega >= lite_start],
+                                           omega=omega)
+        self.last_output = _np64(out[0, :, : self._d])
+        miss = int(L.view("step_miss")[0, 0])
+        total = int(L.view("step_total")[0, 0])
+        self.stats.record(t, miss, total)
+        r = self.cfg.prefill.rank
+        self.factors = LowRankFactors(A_Q=self.factors.A_Q, A_K=self.factors.A_K,
+                                      B_Q=_np64(L.view("B_Q")[0, 0, :r, : self._d]),
+                                      B_K=_np64(L.view("B_K")[0, 0, :r, : self._d]))
+        if compute_metrics:
+            recall, err = self._fidelity(step.q, omega, self.last_output, t)
+        else:
+            recall, err = math.nan, math.nan
+        return StepReport(step=t, selected_count=total, miss_count=miss, recall_vs_exact=recall, output_err=err)
+
+    def _fidelity(self, q, omega, output, t):
+        """Recall against the exact top-k over the full history and error
+        against full-history attention (ref: session.py:119-131), both on the
+        device."""
+        L = self._layer
+        d = self._d
+        K = L.view("slow_k")[0, 0, : t + 1, :d].contiguous()
+        V = L.view("slow_v")[0, 0, : t + 1, :d].contiguous()
+        exact = exact_topk(q, _np64(K), min(self.cfg.k_budget, t + 1))
+        recall = selection_recall(omega, exact)
+        full, _ = _attention_device(_f32(q, L.device), K[None], V[None], d, want_weights=False)
+        full = _np64(full[:, :d])
+        denom = float(np.linalg.norm(full))
+        diff = float(np.linalg.norm(output - full))
+        err = diff / denom if denom > 0 else (0.0 if diff == 0.0 else math.inf)
+        return recall, err
+
+
+def run_simulation(Q, K, V, prompt_len: int, cfg: SessionConfig, steps: int | None = None,
+                   compute_metrics: bool = True) -> SimulationResult:
+    """ref: session.py:134-165."""
+    Q = as_matrix(Q, "Q")
+    K = as_matrix(K, "K")
+    V = as_matrix(V, "V")
+    total = Q.shape[0]
+    if not 1 <= prompt_len <= total:
+        raise ValueError(f"prompt_len must be in [1, {total}], got {prompt_len}")
+    available = total - prompt_len
+    if steps is None:
+        steps = available
+    if steps > available:
+        raise ValueError(f"{steps} decode steps requested, only {available} available")
+    session = DecodeSession(cfg)
+    session.prefill(Q[:prompt_len], K[:prompt_len], V[:prompt_len])
+    reports = [session.decode_step(Q[i], K[i], V[i], compute_metrics=compute_metrics)
+               for i in range(prompt_len, prompt_len + steps)]
+    return SimulationResult(reports=reports, stats=session.stats, session=session)
+
+
+def summarize(result: SimulationResult, cfg: SessionConfig) -> dict:
+    errs = [r.output_err for r in result.reports]
+    recalls = [r.recall_vs_exact for r in result.reports]
+    have = bool(errs) and not any(math.isnan(e) for e in errs)
+    return {
+        "steps": len(result.reports),
+        "mean_miss_rate": (result.stats.c_miss / result.stats.c_total if result.stats.c_total else None),
+        "mean_recall": float(np.mean(recalls)) if have else None,
+        "p50_output_err": float(np.percentile(errs, 50)) if have else None,
+        "p95_output_err": float(np.percentile(errs, 95)) if have else None,
+        "config": asdict(cfg),
+    }
+
+
+def write_report_csv(path, reports) -> None:
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["step", "selected", "miss", "recall", "output_err"])
+        for r in reports:
+            w.writerow([r.step, r.selected_count, r.miss_count, repr(r.recall_vs_exact), repr(r.output_err)])

@@ -376,3 +376,166 @@ int launch_fill_int(int32_t *p, int n, int v, cudaStream_t st) {
 }
 
 }  // namespace lrqk
+
+namespace lrqk {
+// ---------------------------------------------------------------------------
+// Standalone exact attention over explicit rows (drop-in exact_attention,
+// attention.py:23-34): one block per head, logits -> max -> exp -> weights
+// -> output.  Rows are fp32 [H][n][ld]; outputs [H][ld] and weights [H][n].
+// ---------------------------------------------------------------------------
+__global__ void attention_rows_kernel(const float *q, const float *K, const float *V, int n, int d, int ld,
+                                      float scale, float *out, float *weights) {
+    extern __shared__ float w[];  // [n]
+    __shared__ float red[32];
+    const int h = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const float *qh = q + (size_t)h * ld;
+    const float *Kh = K + (size_t)h * n * ld;
+    const float *Vh = V + (size_t)h * n * ld;
+    // logits, one warp per row
+    for (int j = warp; j < n; j += nw) {
+        float acc = 0.f;
+        for (int i = lane; i < d; i += 32) acc = fmaf(qh[i], Kh[(size_t)j * ld + i], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) w[j] = acc * scale;
+    }
+    __syncthreads();
+    float m = -INFINITY;
+    for (int j = tid; j < n; j += blockDim.x) m = fmaxf(m, w[j]);
+    m = warp_max(m);
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    if (tid < 32) {
+        float v = tid < nw ? red[tid] : -INFINITY;
+        v = warp_max(v);
+        if (tid == 0) red[0] = v;
+    }
+    __syncthreads();
+    m = red[0];
+    __syncthreads();
+    float sacc = 0.f;
+    for (int j = tid; j < n; j += blockDim.x) {
+        const float e = expf(w[j] - m);
+        w[j] = e;
+        sacc += e;
+    }
+    sacc = warp_sum(sacc);
+    if (lane == 0) red[warp] = sacc;
+    __syncthreads();
+    if (tid < 32) {
+        float v = tid < nw ? red[tid] : 0.f;
+        v = warp_sum(v);
+        if (tid == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = 1.f / red[0];
+    for (int j = tid; j < n; j += blockDim.x) {
+        w[j] *= inv;
+        if (weights) weights[(size_t)h * n + j] = w[j];
+    }
+    __syncthreads();
+    for (int i = tid; i < d; i += blockDim.x) {
+        float o = 0.f;
+        for (int j = 0; j < n; ++j) o = fmaf(w[j], Vh[(size_t)j * ld + i], o);
+        out[(size_t)h * ld + i] = o;
+    }
+}
+
+int launch_attention_rows(const float *q, const float *K, const float *V, int H, int n, int d, int ld, float *out,
+                          float *weights, cudaStream_t st) {
+    const size_t smem = (size_t)n * sizeof(float);
+    if (smem > 200 * 1024) return LRQK_EUNSUPPORTED;
+    cudaFuncSetAttribute(attention_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attention_rows_kernel<<<H, 256, smem, st>>>(q, K, V, n, d, ld, rsqrtf((float)d), out, weights);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
+// Hit/miss accounting for an explicit selection (drop-in fetch_and_merge,
+// cache.py:174-196): resident (ascending, n_res) vs omega (n_sel, any order,
+// unique); outputs [miss, selected, out_of_range].  One block.
+// ---------------------------------------------------------------------------
+__global__ void count_misses_kernel(const int32_t *resident, int n_res, const int32_t *omega, int n_sel, int size,
+                                    int32_t *out) {
+    __shared__ int s_miss, s_bad;
+    if (threadIdx.x == 0) { s_miss = 0; s_bad = 0; }
+    __syncthreads();
+    int miss = 0, bad = 0;
+    for (int i = threadIdx.x; i < n_sel; i += blockDim.x) {
+        const int x = omega[i];
+        if (x < 0 || x >= size) bad = 1;
+        int lo = 0, hi = n_res - 1, found = 0;
+        while (lo <= hi) {
+            const int mid = (lo + hi) >> 1;
+            const int v = resident[mid];
+            if (v == x) { found = 1; break; }
+            if (v < x) lo = mid + 1; else hi = mid - 1;
+        }
+        miss += found ? 0 : 1;
+    }
+    atomicAdd(&s_miss, miss);
+    if (bad) atomicOr(&s_bad, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) { out[0] = s_miss; out[1] = n_sel; out[2] = s_bad; }
+}
+
+int launch_count_misses(const int32_t *resident, int n_res, const int32_t *omega, int n_sel, int size, int32_t *out,
+                        cudaStream_t st) {
+    count_misses_kernel<<<1, 256, 0, st>>>(resident, n_res, omega, n_sel, size, out);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+}  // namespace lrqk
+
+namespace lrqk {
+// ---------------------------------------------------------------------------
+// Standalone exact line-search step on one B factor (drop-in
+// update_projections, decode.py:150-184): per head h,
+//   resid = x_hat B - x, grad = x_hat^T resid, s = x_hat grad,
+//   eta = (resid.s)/(s.s) (0 when s.s <= 1e-14 (1 + |resid.s|)),
+//   B_out = B - eta grad.   Shapes: x_hat [H][r], B [H][r][d], x [H][d].
+// ---------------------------------------------------------------------------
+__global__ void line_search_kernel(const float *xh, const float *B, const float *x, int r, int d, float *B_out,
+                                   float *grad, float *eta_out) {
+    extern __shared__ float sm[];
+    float *res = sm;        // [d]
+    float *sx = res + d;    // [r]
+    __shared__ double s_nd[2][32];
+    const int h = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const float *Bh = B + (size_t)h * r * d;
+    for (int p = tid; p < r; p += blockDim.x) sx[p] = xh[(size_t)h * r + p];
+    __syncthreads();
+    float nx = 0.f;
+    for (int p = 0; p < r; ++p) nx = fmaf(sx[p], sx[p], nx);
+    double num = 0.0, den = 0.0;
+    for (int i = tid; i < d; i += blockDim.x) {
+        float acc = 0.f;
+        for (int p = 0; p < r; ++p) acc = fmaf(sx[p], Bh[(size_t)p * d + i], acc);
+        const float rr = acc - x[(size_t)h * d + i];
+        res[i] = rr;
+        const double s = (double)nx * rr;
+        num += (double)rr * s;
+        den += s * s;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, o);
+        den += __shfl_xor_sync(0xffffffffu, den, o);
+    }
+    if (lane == 0) { s_nd[0][warp] = num; s_nd[1][warp] = den; }
+    __syncthreads();
+    double tn = 0.0, td = 0.0;
+    for (int w = 0; w < nw; ++w) { tn += s_nd[0][w]; td += s_nd[1][w]; }
+    const float eta = (td <= 1e-14 * (1.0 + fabs(tn))) ? 0.f : (float)(tn / td);
+    if (tid == 0) eta_out[h] = eta;
+    for (int e = tid; e < r * d; e += blockDim.x) {
+        const int p = e / d, i = e - p * d;
+        const float g = sx[p] * res[i];
+        if (grad) grad[(size_t)h * r * d + e] = g;
+        B_out[(size_t)h * r * d + e] = Bh[e] - eta * g;
+    }
+}
+
+int launch_line_search(const float *xh, const float *B, const float *x, int H, int r, int d, float *B_out,
+                       float *grad, float *eta, cudaStream_t st) {
+    line_search_kernel<<<H, 256, (size_t)(d + r) * sizeof(float), st>>>(xh, B, x, r, d, B_out, grad, eta);
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+}  // namespace lrqk

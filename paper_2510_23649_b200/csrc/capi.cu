@@ -20,6 +20,12 @@ int launch_advance(int32_t *ctx_len, int n, cudaStream_t st);
 int launch_proxy_scores(const void *store, int dtype, const float *qh, float *out, int n_heads, int n_rows, int R,
                         cudaStream_t st);
 int launch_fill_int(int32_t *p, int n, int v, cudaStream_t st);
+int launch_attention_rows(const float *q, const float *K, const float *V, int H, int n, int d, int ld, float *out,
+                          float *weights, cudaStream_t st);
+int launch_count_misses(const int32_t *resident, int n_res, const int32_t *omega, int n_sel, int size, int32_t *out,
+                        cudaStream_t st);
+int launch_line_search(const float *xh, const float *B, const float *x, int H, int r, int d, float *B_out,
+                       float *grad, float *eta, cudaStream_t st);
 size_t prefill_scratch_floats(const lrqk_prefill_t &P);
 int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st);
 }  // namespace lrqk
@@ -279,6 +285,24 @@ int lrqk_select_scores(const float *scores, int32_t n_heads, int32_t t, int32_t 
     if (cudaMemcpyAsync(omega_cnt, L.res_cnt, (size_t)n_heads * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
         return check(LRQK_ECUDA);
     return LRQK_OK;
+}
+
+int lrqk_attention_rows(const float *q, const float *K, const float *V, int32_t n_heads, int32_t n_rows,
+                        int32_t head_dim, int32_t ld, float *out, float *weights, void *stream) {
+    if (!q || !K || !V || !out || n_heads < 1 || n_rows < 1 || head_dim < 1 || ld < head_dim) return LRQK_EINVAL;
+    return check(launch_attention_rows(q, K, V, n_heads, n_rows, head_dim, ld, out, weights, (cudaStream_t)stream));
+}
+
+int lrqk_count_misses(const int32_t *resident, int32_t n_resident, const int32_t *omega, int32_t n_selected,
+                      int32_t size, int32_t *out3, void *stream) {
+    if (!omega || !out3 || n_resident < 0 || n_selected < 0) return LRQK_EINVAL;
+    return check(launch_count_misses(resident, n_resident, omega, n_selected, size, out3, (cudaStream_t)stream));
+}
+
+int lrqk_line_search(const float *x_hat, const float *B, const float *x, int32_t n_heads, int32_t rank,
+                     int32_t dim, float *B_out, float *grad, float *eta, void *stream) {
+    if (!x_hat || !B || !x || !B_out || !eta || n_heads < 1 || rank < 1 || dim < 1) return LRQK_EINVAL;
+    return check(launch_line_search(x_hat, B, x, n_heads, rank, dim, B_out, grad, eta, (cudaStream_t)stream));
 }
 
 size_t lrqk_prefill_scratch_bytes(const lrqk_prefill_t *P) {
