@@ -238,13 +238,17 @@ def run_ours(args, world, rank, local):
     eng.capture()
     gather_buf = None
     if world > 1:
-        gather_buf = torch.empty(world, B, Hq, shape.dim_stride, device=dev)
+        from paper_2510_23649_b200.shard import gather_outputs, plan_shards
+
+        plan = plan_shards(B * world, Hq, Hkv, world)
+        assert plan[rank].batch == B and plan[rank].n_q_heads == Hq
+        gather_buf = torch.empty(B * world, Hq, shape.dim_stride, device=dev)
 
     def one_step(i):
         load_inputs(i)
         eng.replay()
         if world > 1:  # final per-head output gather over NVLink (NCCL)
-            dist.all_gather_into_tensor(gather_buf, eng.out_buf[-1])
+            gather_outputs(eng.out_buf[-1], plan, out=gather_buf)
 
     step_i = 2
     for _ in range(args.warmup):
@@ -293,7 +297,7 @@ def run_ours(args, world, rank, local):
         eng.v_buf[..., :d].copy_(v_host[j], non_blocking=True)
         eng.replay()
         if world > 1:
-            dist.all_gather_into_tensor(gather_buf, eng.out_buf[-1])
+            gather_outputs(eng.out_buf[-1], plan, out=gather_buf)
         out_host.copy_(eng.out_buf, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()

@@ -315,7 +315,8 @@ def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter
         aq, ak = randn_init(l, rank, seed)
         A_Q0, A_K0 = aq, ak
     def prep(A):
-        A = torch.as_tensor(A, dtype=torch.float32, device=dev)
+        A = torch.as_tensor(np.array(A, dtype=np.float32) if isinstance(A, np.ndarray) else A,
+                            dtype=torch.float32, device=dev)
         if A.dim() == 2:
             A = A.unsqueeze(0).expand(H, l, A.shape[-1])
         return pad_last(A, rs).contiguous().clone()
