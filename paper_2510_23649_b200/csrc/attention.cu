@@ -36,6 +36,9 @@ attention_kernel(const AttnArgs a) {
     const int d = L.dim_stride;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sub = lane / LPR, sl = lane - sub * LPR;
+    trace(30);
+    pdl_wait();
+    pdl_trigger();
     const int S = L.res_cnt[bh];
     const bool host = L.policy == LRQK_SLOW_HOST;
     const T *kb, *vb;
@@ -129,6 +132,7 @@ attention_kernel(const AttnArgs a) {
         }
         m = mx;
     }
+    trace(31);
     // per-group partials to shared
     const int gidx = warp * RPW + sub;
     if (sl == 0) { s_m[gidx] = m; s_l[gidx] = l; }
@@ -154,7 +158,9 @@ attention_kernel(const AttnArgs a) {
         part[0] = M;
         part[1] = sl2;
     }
+    trace(32);
     if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_ATTN, gridDim.x, &s_flag)) return;
+    trace(33);
     // merge the splits of this head
     __shared__ float s_ms[64], s_w[64];
     __shared__ float s_den;
@@ -188,6 +194,7 @@ attention_kernel(const AttnArgs a) {
         if (sp < nsp) o0 = fmaf(__ldcg(parts + (size_t)sp * (d + 2) + 2 + i), s_ms[sp], o0);
         a.out[(size_t)bh * d + i] = (o0 + o1) * inv;
     }
+    trace(34);
 }
 
 int attn_splits(const lrqk_layer_t &L) { return (L.s_cap + kAttnRows - 1) / kAttnRows; }
@@ -205,7 +212,7 @@ static int launch_attention_t(const AttnArgs &a, cudaStream_t st) {
     do {                                                                                         \
         auto fn = attention_kernel<T, LP, PP>;                                                   \
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-        fn<<<grid, kAttnThreads, smem, st>>>(a);                                                 \
+        launch_kernel(fn, grid, kAttnThreads, smem, st, true, a);                                \
     } while (0)
     if (ppl == 1) {
         switch (lpr) {

@@ -1,5 +1,6 @@
 // extern "C" boundary of liblrqk_b200.so (declared in include/lrqk_b200.h).
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -31,6 +32,14 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st);
 }  // namespace lrqk
 
 using namespace lrqk;
+
+bool lrqk::pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("LRQK_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 static thread_local char g_err[256] = "";
 

@@ -196,6 +196,66 @@ LRQK_DEV bool last_arrival(int *counter, int expected, int *s_flag) {
 }  // namespace lrqk
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch.  The decode chain (compress -> score ->
+// select -> attention, layer after layer) is launched with programmatic
+// stream serialization: a kernel's blocks may start while its predecessor
+// is still running, do work that only depends on older kernels, then
+// pdl_wait() until the predecessor has completed and its writes are
+// visible.  Every kernel calls pdl_trigger() only after its own pdl_wait(),
+// so when a kernel's prologue runs, everything before its predecessor has
+// completed.  Both are no-ops for kernels launched without the attribute.
+// ---------------------------------------------------------------------------
+namespace lrqk {
+LRQK_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+LRQK_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();  // capi.cu: on unless LRQK_PDL=0
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}  // namespace lrqk
+
+// ---------------------------------------------------------------------------
+// mbarrier + 1-D TMA bulk copy (cp.async.bulk) helpers
+// ---------------------------------------------------------------------------
+namespace lrqk {
+LRQK_DEV uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+LRQK_DEV void mbar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+LRQK_DEV void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+LRQK_DEV void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+LRQK_DEV void mbar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    } while (!ok);
+}
+LRQK_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+}  // namespace lrqk
+
+// ---------------------------------------------------------------------------
 // Development tracing: when g_lrqk_trace_on is set (lrqk_trace_enable), thread
 // 0 of a block records (tag, block, %globaltimer) records.  Off by default.
 // ---------------------------------------------------------------------------

@@ -61,6 +61,9 @@ __host__ __device__ inline PreLayout pre_layout(int R, int d) {
     p.total = (o + 3) & ~3;
     return p;
 }
+struct PreLayoutOrder {  // compress_kernel bulk-copies Pinv|Rinv and ZQ|ZK as pairs
+    static constexpr bool kPairs = true;
+};
 // Per-head reduction scratch of K2p: chunk partials [Y (R*d) | G (R*R)] + the
 // prep block's B_Q B_Q^T.
 __host__ __device__ inline size_t red_head_floats(int R, int d, int nchunks) {
@@ -715,16 +718,12 @@ compress_kernel(const CompressArgs args) {
     __shared__ float s_scalar[8];
     __shared__ int s_bad;
     __shared__ float s_rc[256];
+    __shared__ __align__(8) uint64_t s_bar;
     const int bh = blockIdx.x;
     const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
     const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
     const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int t = L.ctx_len[b];
-    if (t >= L.t_max) {
-        if (tid == 0) set_status(L.status, LRQK_ST_CAPACITY);
-        return;
-    }
     trace(0);
     const PreLayout PL = pre_layout(R, d);
     const float *pre = L.pre + (size_t)bh * PL.total;
@@ -733,16 +732,20 @@ compress_kernel(const CompressArgs args) {
     const T *qrow = reinterpret_cast<const T *>(args.q) + (size_t)bh * d;
     const T *krow = reinterpret_cast<const T *>(args.k) + ((size_t)b * L.n_kv_heads + g) * d;
     const T *vrow = reinterpret_cast<const T *>(args.v) + ((size_t)b * L.n_kv_heads + g) * d;
-    const int ldB = d + 4, ldM = R + 4;
-    float *sBQ = smem;                   // [R][ldB]
-    float *sBK = sBQ + R * ldB;          // [R][ldB]
-    float *sZQ = sBK + R * ldB;          // [R][ldB]  Z_Q (or W in the fallback)
-    float *sZK = sZQ + R * ldB;          // [R][ldB]  Z_K
-    float *sPi = sZK + R * ldB;          // [R][ldM]  P^-1 (P in the fallback)
-    float *sRi = sPi + R * ldM;          // [R][ldM]  R^-1 (R in the fallback)
-    float *b0 = sRi + R * ldM;           // [R][ldM]  fallback scratch
-    float *sM = b0 + R * ldM;            // [R][ldM]  fallback system
-    float *vq = sM + R * ldM;            // [d]
+    // Staged operands, unpadded: B_Q, B_K | P^-1, R^-1 | Z_Q, Z_K arrive with
+    // four 1-D bulk copies on one mbarrier (the pre layout keeps each pair
+    // contiguous), issued before anything else so the whole 72 KB lands in
+    // one memory round trip.
+    const int ldB = d, ldM = R;
+    float *sBQ = smem;                   // [R][d]
+    float *sBK = sBQ + R * d;            // [R][d]
+    float *sPi = sBK + R * d;            // [R][R]  P^-1 (P in the fallback)
+    float *sRi = sPi + R * R;            // [R][R]  R^-1 (R in the fallback)
+    float *sZQ = sRi + R * R;            // [R][d]  Z_Q (or W in the fallback)
+    float *sZK = sZQ + R * d;            // [R][d]  Z_K
+    float *b0 = sZK + R * d;             // [R][R]  fallback scratch
+    float *sM = b0 + R * R;              // [R][R]  fallback system
+    float *vq = sM + R * R;              // [d]
     float *vk = vq + d;                  // [d]
     float *yq = vk + d;                  // [R]
     float *yk = yq + R;                  // [R]
@@ -751,25 +754,44 @@ compress_kernel(const CompressArgs args) {
     float *u = kh + R;                   // [R]
     float *prevc = u + R;                // [2R]
     float *resid = prevc + 2 * R;        // [2][d]
+    static_assert(PreLayoutOrder::kPairs, "pre layout keeps Pinv|Rinv and ZQ|ZK adjacent");
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t mat = (uint32_t)(R * d * 4), sq = (uint32_t)(R * R * 4);
+        mbar_expect_tx(&s_bar, 4 * mat + 2 * sq);
+        bulk_g2s(sBQ, L.B_Q + (size_t)bh * R * d, mat, &s_bar);
+        bulk_g2s(sBK, L.B_K + (size_t)bh * R * d, mat, &s_bar);
+        bulk_g2s(sPi, pre + PL.Pinv, 2 * sq, &s_bar);
+        bulk_g2s(sZQ, pre + PL.ZQ, 2 * mat, &s_bar);
+        s_bad = 0;
+    }
+    // B_Q/B_K and pre were written by the previous step (older than this
+    // kernel's predecessor); q/k/v and ctx_len may come from the predecessor
+    pdl_wait();
+    pdl_trigger();
     const bool okP = __ldcg(pre + PL.flags + 0) != 0.f;
     const bool okR = __ldcg(pre + PL.flags + 1) != 0.f;
     const bool fast = okP && okR;
-    // ---- stage: B_Q, B_K, Z_Q, Z_K (or W, P, R), q, k ----------------------
-    stage_rows_f32(sBQ, ldB, L.B_Q + (size_t)bh * R * d, R, d);
-    stage_rows_f32(sBK, ldB, L.B_K + (size_t)bh * R * d, R, d);
-    stage_rows_f32(sZQ, ldB, pre + (fast ? PL.ZQ : PL.W), R, d);
-    if (fast) stage_rows_f32(sZK, ldB, pre + PL.ZK, R, d);
-    for (int e = tid; e < R * R; e += blockDim.x) {
-        const int i = e / R, j = e - i * R;
-        sPi[i * ldM + j] = __ldcg(pre + (fast ? PL.Pinv : PL.P) + e);
-        sRi[i * ldM + j] = __ldcg(pre + (fast ? PL.Rinv : PL.R) + e);
-    }
-    if (tid == 0) s_bad = 0;
+    const int t = L.ctx_len[b];
     __syncthreads();
+    if (t >= L.t_max) {
+        mbar_wait(&s_bar, 0);  // no bulk copy may still target this block's smem
+        if (tid == 0) set_status(L.status, LRQK_ST_CAPACITY);
+        return;
+    }
     for (int i = tid; i < d; i += blockDim.x) {
         vq[i] = to_float<T>(qrow[i]);
         vk[i] = to_float<T>(krow[i]);
         if (!isfinite(vq[i]) || !isfinite(vk[i]) || !isfinite(to_float<T>(vrow[i]))) s_bad = 1;
+    }
+    mbar_wait(&s_bar, 0);
+    if (!fast) {  // rare: the direct solves need W, P, R instead of Z_Q, P^-1, R^-1
+        for (int e = tid; e < R * d; e += blockDim.x) sZQ[e] = __ldcg(pre + PL.W + e);
+        for (int e = tid; e < R * R; e += blockDim.x) {
+            sPi[e] = __ldcg(pre + PL.P + e);
+            sRi[e] = __ldcg(pre + PL.R + e);
+        }
     }
     __syncthreads();
     if (s_bad) {  // ref: linalg.py:32-33 via as_row (session.py:94)
@@ -1038,8 +1060,7 @@ static size_t prepare_smem_bytes(const lrqk_layer_t &L) {
 }
 static size_t compress_smem_bytes(const lrqk_layer_t &L) {
     const size_t d = L.dim_stride, R = L.rank_stride;
-    const size_t ldB = d + 4, ldM = R + 4;
-    return (4 * R * ldB + 4 * R * ldM + 4 * d + 7 * R) * sizeof(float);
+    return (4 * R * d + 4 * R * R + 4 * d + 7 * R) * sizeof(float);
 }
 
 int launch_prepare(const lrqk_layer_t &L, cudaStream_t st) {
@@ -1061,10 +1082,10 @@ int launch_compress(const lrqk_layer_t &L, const void *q, const void *k, const v
     const size_t smem = compress_smem_bytes(L);
     if (L.dtype == LRQK_BF16) {
         cudaFuncSetAttribute(compress_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        compress_kernel<__nv_bfloat16><<<L.batch * L.n_q_heads, kCompressThreads, smem, st>>>(a);
+        launch_kernel(compress_kernel<__nv_bfloat16>, L.batch * L.n_q_heads, kCompressThreads, smem, st, true, a);
     } else {
         cudaFuncSetAttribute(compress_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        compress_kernel<float><<<L.batch * L.n_q_heads, kCompressThreads, smem, st>>>(a);
+        launch_kernel(compress_kernel<float>, L.batch * L.n_q_heads, kCompressThreads, smem, st, true, a);
     }
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }

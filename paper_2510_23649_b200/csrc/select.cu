@@ -231,28 +231,6 @@ score_kernel(const ScoreArgs a) {
 // ---------------------------------------------------------------------------
 constexpr int kCW = 8;  // consumer warps
 
-LRQK_DEV uint32_t smem_u32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
-LRQK_DEV void mbar_init(uint64_t *b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-LRQK_DEV void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-LRQK_DEV void mbar_arrive(uint64_t *b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-LRQK_DEV void mbar_wait(uint64_t *b, uint32_t parity) {
-    uint32_t ok;
-    do {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
-    } while (!ok);
-}
-LRQK_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
 template <int NPK> struct ScoreStages {
     static constexpr int kTileBytes = NPK * 512;
     static constexpr int kStageBytes = kCW * kTileBytes;
@@ -274,6 +252,7 @@ score_tma_kernel(const ScoreArgs a) {
     __shared__ int s_scan[32];
     __shared__ int s_flag;
     __shared__ int s_out[2];
+    trace(40);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int P = a.parts;
     const int bh = blockIdx.x / P, part = blockIdx.x - bh * P;
@@ -296,6 +275,8 @@ score_tma_kernel(const ScoreArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();  // q_hat, the appended proxy row and ctx_len come from compress
+    pdl_trigger();
     const uint8_t *src = reinterpret_cast<const uint8_t *>(reinterpret_cast<const T *>(L.proxy) +
                                                            (size_t)bh * L.t_max * R);
     uint32_t *keys = L.keys + (size_t)bh * L.t_max;
@@ -344,12 +325,14 @@ score_tma_kernel(const ScoreArgs a) {
             if (lane == 0) mbar_arrive(empty + s2);
         }
     }
+    trace(41);
     __syncthreads();
     uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;
     for (int i = tid; i < kHistBins; i += blockDim.x)
         if (s_hist[i]) atomicAdd(ghist + i, (uint32_t)s_hist[i]);
     int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
     if (!last_arrival(cnt, P, &s_flag)) return;
+    trace(42);
     // ---- last block of this head: candidate bins ----------------------------
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     const int k_eff = min(L.k_budget, lite_start);
@@ -387,6 +370,7 @@ score_tma_kernel(const ScoreArgs a) {
         meta[M_CAND] = 0;
         meta[M_MODE] = 0;
     }
+    trace(43);
 }
 
 // Radix select over unique composites (exact fallback): returns thr such that
@@ -426,7 +410,7 @@ constexpr int kLocSure = 1024;  // block-local append buffers (spill to global b
 constexpr int kLocCand = 2048;
 constexpr int kCritCap = 4096;  // critical fine bin sorted in shared memory (larger -> exact fallback)
 
-__global__ void __launch_bounds__(kSelThreads)
+__global__ void __launch_bounds__(kSelThreads, 2)
 select_kernel(const lrqk_layer_t L, int parts) {
     extern __shared__ __align__(16) uint32_t fsm[];
     __shared__ int s_hist[kHistBins];
@@ -437,9 +421,12 @@ select_kernel(const lrqk_layer_t L, int parts) {
     const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
     const int BH = L.batch * L.n_q_heads;
     const bool host = L.policy == LRQK_SLOW_HOST;
+    pdl_wait();
+    pdl_trigger();
 
     for (int item = blockIdx.x; item < BH * parts; item += gridDim.x) {
         const int bh = item / parts, part = item - bh * parts;
+        trace(20);
         const int b = bh / L.n_q_heads;
         const int t = L.ctx_len[b];
         if (t >= L.t_max) continue;
@@ -552,6 +539,17 @@ select_kernel(const lrqk_layer_t L, int parts) {
         uint32_t *slot_used = reinterpret_cast<uint32_t *>(news + L.s_cap);
         const int slot_words = (L.n_slots + 31) >> 5;
         uint64_t *crit = reinterpret_cast<uint64_t *>(slot_used + ((slot_words + 3) & ~3));
+        // prefetch in one round trip: Omega_{t-1} (+ slots), the fine
+        // histogram, the list lengths; clear the bitmap meanwhile
+        const int n_prev = L.res_cnt[bh];
+        int *res_idx = L.res_idx + (size_t)bh * L.s_cap;
+        int *res_slot = L.res_slot + (size_t)bh * L.s_cap;
+        for (int i = tid; i < n_prev; i += nt) {
+            prevl[i] = __ldcg(res_idx + i);
+            if (host) prevs[i] = __ldcg(res_slot + i);
+        }
+        if (mode0 == 0)
+            for (int i = tid; i < kHistBins; i += nt) s_hist[i] = (int)__ldcg(hist2 + i);
         if (mode0 == 1) {
             for (int i = tid; i < k_eff; i += nt) newl[i] = i;  // everything fits
         } else {
@@ -560,6 +558,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
             const int n_cand = __ldcg(meta + M_CAND);
             const int need = k_eff - n_sure;
             bool ok = n_sure <= L.k_budget && need >= 0 && need <= n_cand && n_cand <= L.cand_cap;
+            if (tid == 0) s_cnt[0] = 0;
             __syncthreads();
             if (ok) {
                 for (int i = tid; i < n_sure; i += nt) {
@@ -568,9 +567,6 @@ select_kernel(const lrqk_layer_t L, int parts) {
                 }
                 if (need > 0) {
                     const int b_lo = meta[M_B_LO], s2 = meta[M_S2];
-                    for (int i = tid; i < kHistBins; i += nt) s_hist[i] = (int)__ldcg(hist2 + i);
-                    if (tid == 0) s_cnt[0] = 0;
-                    __syncthreads();
                     find_crossing(s_hist, kHistBins, need, s_scan, s_out);
                     const int fstar = s_out[0];
                     const int need2 = need - s_out[1];
@@ -645,13 +641,6 @@ select_kernel(const lrqk_layer_t L, int parts) {
 
         trace(24);
         // ---- K5: hit/miss against Omega_{t-1} U {t} ---------------------------
-        const int n_prev = L.res_cnt[bh];
-        int *res_idx = L.res_idx + (size_t)bh * L.s_cap;
-        int *res_slot = L.res_slot + (size_t)bh * L.s_cap;
-        for (int i = tid; i < n_prev; i += nt) {
-            prevl[i] = res_idx[i];
-            if (host) prevs[i] = res_slot[i];
-        }
         if (host) for (int w = tid; w < slot_words; w += nt) slot_used[w] = 0u;
         __syncthreads();
         const int spare = host ? L.spare_slot[bh] : 0;
@@ -801,7 +790,7 @@ static void launch_score_tma_t(const ScoreArgs &a, int grid, cudaStream_t st) {
     using SS = ScoreStages<NPK>;
     auto fn = score_tma_kernel<T, NPK>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::kSmem);
-    fn<<<grid, 32 * (kCW + 1), SS::kSmem, st>>>(a);
+    launch_kernel(fn, grid, 32 * (kCW + 1), SS::kSmem, st, true, a);
 }
 
 template <typename T>
@@ -846,7 +835,7 @@ int launch_select(const lrqk_layer_t &L, cudaStream_t st) {
     const int grid = max(1, min(BH * parts, num_sms() * 2));
     const size_t smem = finalize_smem_bytes(L);
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    select_kernel<<<grid, kSelThreads, smem, st>>>(L, parts);
+    launch_kernel(select_kernel, grid, kSelThreads, smem, st, true, L, parts);
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
