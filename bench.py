@@ -276,6 +276,14 @@ def run_ours(args, world, rank, local):
     ms = start.elapsed_time(stop)
     eng.raise_status()
     t_now = int(eng.ctx[0].item())
+    # selection path statistics (head-steps per mode, since the prompt)
+    mstat = np.zeros(7, dtype=np.int64)
+    for layer in eng.layers:
+        m = layer.buf["sel_meta"].view(torch.int32)[: B * Hq * 48].view(B * Hq, 48)
+        mstat += m[:, 33:40].sum(0).cpu().numpy()
+    sel_modes = dict(zip(["sampled_radix", "all_fit", "unused", "window_scan", "unused4", "window_direct",
+                          "exact_fallback"],
+                         [int(x) for x in mstat]))
 
     # ---- end to end: host inputs in, host outputs out, per step ------------
     q_host = q_pool[:4].cpu().pin_memory()
@@ -321,6 +329,7 @@ def run_ours(args, world, rank, local):
             _lib.check(lib.lrqk_score(layer.ptr, sp), "score")
             b_.record(stream)
             evs.append((a, b_))
+            _lib.check(lib.lrqk_select_attend(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "select_attend")
             _lib.check(lib.lrqk_select(layer.ptr, sp), "select")
             _lib.check(lib.lrqk_gather_misses(layer.ptr, sp), "gather")
             _lib.check(lib.lrqk_attention(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "attention")
@@ -374,6 +383,7 @@ def run_ours(args, world, rank, local):
         clocks=clock_info,
         prefill=dict(ms_total_gpu=round(prefill_ms, 2), heads=L * B * Hq, ctx=ctx, setup_s=round(setup_s, 2)),
         bytes_per_token_layer=byt,
+        select_paths=sel_modes,
     )
 
 

@@ -95,9 +95,9 @@ typedef struct lrqk_layer {
     float *q_hat, *k_hat;          /* [B,Hq,rank_stride]                      */
     float *eta;                    /* [B,Hq,2] line-search steps (eta_Q, eta_K) */
     uint32_t *keys;                /* [B,Hq,t_max] order-preserving score keys */
-    uint32_t *hist;                /* [B,Hq,2,2048] coarse + fine radix histograms (zero between steps) */
-    int32_t *sel_meta;             /* [B,Hq,16]                               */
-    int32_t *sure_idx;             /* [B,Hq,k_budget]                         */
+    uint32_t *hist;                /* [B,Hq,3,2048] coarse | fine / part counts | hint window (zero between steps) */
+    int32_t *sel_meta;             /* [B,Hq,32] selection state (incl. the persistent threshold hint) */
+    int32_t *sure_idx;             /* [B,Hq,select_parts,k_budget]            */
     uint64_t *cand;                /* [B,Hq,cand_cap]                          */
     float *red_scratch;            /* [B,Hq,red_chunks,rank_stride*(rank_stride+1)] */
     float *attn_scratch;           /* [B,Hq,attn_splits,dim_stride+2]          */
@@ -106,6 +106,13 @@ typedef struct lrqk_layer {
 
     /* ---- persistent precompute of the next step's compression (K2p) ---- */
     float *pre;                    /* [B,Hq,pre_floats]: P^-1, R^-1, P, R, Z_Q, Z_K, W, flags */
+
+    /* ---- per-step scratch of the fused score/selection path ---- */
+    uint64_t *fcand;               /* [B*Hq*score_parts, 1025] per-part window suffix counts (lrqk_score) */
+    int32_t *fcnt;                 /* [B*Hq*score_parts] certain winners before each part (offsets)  */
+
+    /* ---- persistent residency bitmap (HBM policy hit/miss accounting) ---- */
+    uint32_t *res_bits;            /* [B,Hq,ceil(t_max/32)] bit x set <=> x in the fast tier      */
 } lrqk_layer_t;
 
 /* Sizes (bytes) of every buffer in lrqk_layer_t for the given configuration,
@@ -144,6 +151,13 @@ int lrqk_score(const lrqk_layer_t *L, void *stream);
  * replacement.  ref: cache.py:149-196, linalg.py:96-110. */
 int lrqk_select(const lrqk_layer_t *L, void *stream);
 
+/* Fused selection + attention for the heads whose score pass located the
+ * k-th largest key in its threshold window (the common case, HBM policy):
+ * writes Omega_t to res_idx and the attention row to out for those heads;
+ * lrqk_select / lrqk_attention then skip them.  Launch it right after
+ * lrqk_score.  ref: cache.py:149-171, attention.py:23-34. */
+int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
+
 /* Host policy: copy this step's missed K/V rows from the pinned host slow
  * tier into their slots (zero-copy PCIe reads).  ref: cache.py:193-194. */
 int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);
@@ -152,8 +166,9 @@ int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);
  * ref: attention.py:23-34, session.py:101-102. */
 int lrqk_attention(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
-/* One whole decode step of one layer (the five calls above in the
- * reference's order, session.py:90-104); advance!=0 also bumps ctx_len. */
+/* One whole decode step of one layer (compress, score, select_attend,
+ * select, gather, attention, compress_prepare -- the reference's order,
+ * session.py:90-104); advance!=0 also bumps ctx_len. */
 int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const void *v,
                      float *out, int advance, void *stream);
 

@@ -32,7 +32,8 @@ _FLOAT_FIELDS = ("lambda_1", "lambda_2", "tol")
 BUFFER_NAMES = ("proxy", "B_Q", "B_K", "slow_k", "slow_v", "slot_k", "slot_v", "ctx_len", "res_idx",
                 "res_slot", "res_cnt", "spare_slot", "miss_idx", "miss_slot", "miss_cnt", "c_miss",
                 "c_total", "step_miss", "step_total", "q_hat", "k_hat", "eta", "keys", "hist",
-                "sel_meta", "sure_idx", "cand", "red_scratch", "attn_scratch", "counters", "status", "pre")
+                "sel_meta", "sure_idx", "cand", "red_scratch", "attn_scratch", "counters", "status", "pre",
+                "fcand", "fcnt", "res_bits")
 
 
 class LayerStruct(C.Structure):
@@ -77,6 +78,7 @@ SIGNATURES = {
     "lrqk_select": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_gather_misses": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_attention": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
+    "lrqk_select_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_decode_step": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P, _P, C.c_int, _P]),
     "lrqk_advance": (C.c_int, [_P, C.c_int32, _P]),
     "lrqk_proxy_scores_f32": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P]),

@@ -708,7 +708,7 @@ class DecodeSession:
         t = self._t
         self._t += 1
         n = int(L.view("res_cnt")[0, 0])
-        omega = L.view("res_idx")[0, 0, :n].cpu().numpy().astype(np.intp)
+        omega = np.sort(L.view("res_idx")[0, 0, :n].cpu().numpy().astype(np.intp))  # stored unordered
         lite_start = max(0, t + 1 - self.cfg.lite_budget)
         self.last_selection = SelectionSet(omega_k=omega[omega < lite_start], omega_l=omega[omega >= lite_start],
                                            omega=omega)

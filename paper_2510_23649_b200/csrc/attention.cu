@@ -39,6 +39,7 @@ attention_kernel(const AttnArgs a) {
     trace(30);
     pdl_wait();
     pdl_trigger();
+    if (L.sel_meta[(size_t)bh * kMetaInts + M_MODE] == 5) return;  // done by select_attend_kernel
     const int S = L.res_cnt[bh];
     const bool host = L.policy == LRQK_SLOW_HOST;
     const T *kb, *vb;
@@ -198,6 +199,8 @@ attention_kernel(const AttnArgs a) {
 }
 
 int attn_splits(const lrqk_layer_t &L) { return (L.s_cap + kAttnRows - 1) / kAttnRows; }
+int score_tma_parts(const lrqk_layer_t &L);
+int attn_scratch_slots(const lrqk_layer_t &L) { return max(attn_splits(L), score_tma_parts(L)); }
 
 template <typename T>
 static int launch_attention_t(const AttnArgs &a, cudaStream_t st) {
@@ -315,8 +318,21 @@ __global__ void seed_kernel(const lrqk_layer_t L, int prompt_len) {
         if (L.policy == LRQK_SLOW_HOST) L.spare_slot[bh] = n;
         if (h == 0) L.ctx_len[b] = prompt_len;
     }
-    for (int i = threadIdx.x; i < 2 * kHistBins; i += blockDim.x) L.hist[(size_t)bh * 2 * kHistBins + i] = 0u;
-    for (int i = threadIdx.x; i < kMetaInts; i += blockDim.x) L.sel_meta[(size_t)bh * kMetaInts + i] = 0;
+    for (int i = threadIdx.x; i < kHistLevels * kHistBins; i += blockDim.x)
+        L.hist[(size_t)bh * kHistLevels * kHistBins + i] = 0u;
+    for (int i = threadIdx.x; i < kMetaInts; i += blockDim.x)
+        L.sel_meta[(size_t)bh * kMetaInts + i] = i == M_BITS_FRESH ? 1 : 0;
+    if (L.res_bits) {  // residency bitmap = the prompt's lite rows
+        uint32_t *bits = L.res_bits + (size_t)bh * ((L.t_max + 31) / 32);
+        for (int w = threadIdx.x; w < (L.t_max + 31) / 32; w += blockDim.x) {
+            uint32_t v = 0u;
+            for (int j = 0; j < 32; ++j) {
+                const int x = w * 32 + j;
+                if (x >= lo && x < prompt_len) v |= 1u << j;
+            }
+            bits[w] = v;
+        }
+    }
     for (int i = threadIdx.x; i < kCounterInts; i += blockDim.x) L.counters[(size_t)bh * kCounterInts + i] = 0;
     if (L.policy == LRQK_SLOW_HOST) {
         const size_t row_bytes = (size_t)L.dim_stride * (L.dtype == LRQK_BF16 ? 2 : 4);

@@ -16,6 +16,10 @@ int launch_select(const lrqk_layer_t &L, cudaStream_t st);
 int launch_gather(const lrqk_layer_t &L, cudaStream_t st);
 int launch_attention(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st);
 int attn_splits(const lrqk_layer_t &L);
+int select_sure_rows(const lrqk_layer_t &L);
+int score_part_rows(const lrqk_layer_t &L);
+int attn_scratch_slots(const lrqk_layer_t &L);
+int launch_select_attend(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st);
 int launch_seed(const lrqk_layer_t &L, int prompt_len, cudaStream_t st);
 int launch_advance(int32_t *ctx_len, int n, cudaStream_t st);
 int launch_proxy_scores(const void *store, int dtype, const float *qh, float *out, int n_heads, int n_rows, int R,
@@ -95,7 +99,7 @@ const char *lrqk_last_error(void) { return g_err; }
 const char *lrqk_buffer_names(void) {
     return "proxy,B_Q,B_K,slow_k,slow_v,slot_k,slot_v,ctx_len,res_idx,res_slot,res_cnt,spare_slot,miss_idx,"
            "miss_slot,miss_cnt,c_miss,c_total,step_miss,step_total,q_hat,k_hat,eta,keys,hist,sel_meta,sure_idx,"
-           "cand,red_scratch,attn_scratch,counters,status,pre";
+           "cand,red_scratch,attn_scratch,counters,status,pre,fcand,fcnt,res_bits";
 }
 
 int lrqk_red_chunks(const lrqk_layer_t *L) { return compress_chunks(*L); }
@@ -132,15 +136,18 @@ int lrqk_layer_buffer_bytes(const lrqk_layer_t *L, size_t *out, int max_out) {
         BH * R * 4,                     // k_hat
         BH * 2 * 4,                     // eta
         BH * T * 4,                     // keys
-        BH * 2 * kHistBins * 4,         // hist (two radix levels)
+        BH * kHistLevels * kHistBins * 4,  // hist (coarse | fine | hint window)
         BH * kMetaInts * 4,             // sel_meta
-        BH * (size_t)L->k_budget * 4,   // sure_idx
+        (size_t)select_sure_rows(*L) * (size_t)L->k_budget * 4,  // sure_idx (per select part in mode 3)
         BH * (size_t)L->cand_cap * 8,   // cand
         BH * compress_scratch_floats_per_head(*L) * 4,       // red_scratch
-        BH * (size_t)attn_splits(*L) * (d + 2) * 4,         // attn_scratch
+        BH * (size_t)attn_scratch_slots(*L) * (d + 2) * 4,  // attn_scratch (attention splits / fused parts)
         BH * kCounterInts * 4,          // counters
         4,                              // status
         BH * compress_pre_floats_per_head(*L) * 4,  // pre
+        (size_t)score_part_rows(*L) * kCandPart * 8,    // fcand
+        (size_t)score_part_rows(*L) * 4,                // fcnt
+        BH * (size_t)((L->t_max + 31) / 32) * 4,        // res_bits
     };
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < n && i < max_out; ++i) out[i] = v[i];
@@ -188,6 +195,13 @@ int lrqk_gather_misses(const lrqk_layer_t *L, void *stream) {
     return check(launch_gather(*L, (cudaStream_t)stream));
 }
 
+int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream) {
+    int rc = validate(L);
+    if (rc) return rc;
+    if (!q || !out) return LRQK_EINVAL;
+    return check(launch_select_attend(*L, q, out, (cudaStream_t)stream));
+}
+
 int lrqk_attention(const lrqk_layer_t *L, const void *q, float *out, void *stream) {
     int rc = validate(L);
     if (rc) return rc;
@@ -202,6 +216,7 @@ int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const 
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = check(launch_compress(*L, q, k, v, 1, st)))) return rc;
     if ((rc = check(launch_score(*L, nullptr, st)))) return rc;
+    if ((rc = check(launch_select_attend(*L, q, out, st)))) return rc;
     if ((rc = check(launch_select(*L, st)))) return rc;
     if ((rc = check(launch_gather(*L, st)))) return rc;
     if ((rc = check(launch_attention(*L, q, out, st)))) return rc;
@@ -262,9 +277,9 @@ static SelWs sel_layout(int32_t n_heads, int32_t t, int32_t k_budget, int32_t li
     L.step_miss = (int32_t *)take(BH * 4);
     L.step_total = (int32_t *)take(BH * 4);
     L.keys = (uint32_t *)take(BH * L.t_max * 4);
-    L.hist = (uint32_t *)take(BH * 2 * kHistBins * 4);
+    L.hist = (uint32_t *)take(BH * kHistLevels * kHistBins * 4);
     L.sel_meta = (int32_t *)take(BH * kMetaInts * 4);
-    L.sure_idx = (int32_t *)take(BH * (size_t)k_budget * 4);
+    L.sure_idx = (int32_t *)take((size_t)select_sure_rows(L) * (size_t)k_budget * 4);
     L.cand = (uint64_t *)take(BH * (size_t)L.cand_cap * 8);
     L.counters = (int32_t *)take(BH * kCounterInts * 4);
     L.status = (uint32_t *)take(4);
@@ -341,22 +356,27 @@ int lrqk_read_status(const uint32_t *status, uint32_t *host_out, void *stream) {
 // ---- development tracing (see common.cuh) --------------------------------
 namespace lrqk {
 __device__ int g_lrqk_trace_on = 0;
-__device__ unsigned int g_lrqk_trace_n = 0;
 __device__ unsigned long long g_lrqk_trace[kTraceCap][2];
 }  // namespace lrqk
 
 extern "C" int lrqk_trace_enable(int on) {
-    unsigned int zero = 0;
     if (cudaMemcpyToSymbol(lrqk::g_lrqk_trace_on, &on, sizeof(int)) != cudaSuccess) return LRQK_ECUDA;
-    if (cudaMemcpyToSymbol(lrqk::g_lrqk_trace_n, &zero, sizeof zero) != cudaSuccess) return LRQK_ECUDA;
-    return LRQK_OK;
+    void *p = nullptr;
+    if (cudaGetSymbolAddress(&p, lrqk::g_lrqk_trace) != cudaSuccess) return LRQK_ECUDA;
+    if (cudaMemset(p, 0, sizeof(unsigned long long) * 2 * lrqk::kTraceCap) != cudaSuccess) return LRQK_ECUDA;
+    return cudaDeviceSynchronize() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
+// Copies the recorded (tag<<48 | block, %globaltimer) pairs, compacted, to out.
 extern "C" int lrqk_trace_read(unsigned long long *out, int cap) {
-    unsigned int n = 0;
-    if (cudaMemcpyFromSymbol(&n, lrqk::g_lrqk_trace_n, sizeof n) != cudaSuccess) return -1;
-    if ((int)n > cap) n = cap;
-    if (n > (unsigned)lrqk::kTraceCap) n = lrqk::kTraceCap;
-    if (n && cudaMemcpyFromSymbol(out, lrqk::g_lrqk_trace, (size_t)n * 16) != cudaSuccess) return -1;
-    return (int)n;
+    static unsigned long long buf[lrqk::kTraceCap][2];
+    if (cudaMemcpyFromSymbol(buf, lrqk::g_lrqk_trace, sizeof buf) != cudaSuccess) return -1;
+    int n = 0;
+    for (int i = 0; i < lrqk::kTraceCap && n < cap; ++i) {
+        if (buf[i][1] == 0) continue;
+        out[2 * n] = buf[i][0];
+        out[2 * n + 1] = buf[i][1];
+        ++n;
+    }
+    return n;
 }

@@ -12,7 +12,10 @@ namespace lrqk {
 
 constexpr int kHistBits = 11;
 constexpr int kHistBins = 1 << kHistBits;  // 2048 bins on the top 11 key bits
-constexpr int kMetaInts = 16;
+constexpr int kMetaInts = 48;
+constexpr int kPartHist = 2048 + 1 + 1;  // per score part: window histogram + count above (+pad)
+constexpr int kCandPart = kPartHist / 2;  // fcand uint64 entries per score part
+constexpr int kHistLevels = 3;   // per head: coarse | band fine (mode 0) or part counts (mode 3) | hint window
 constexpr int kCounterInts = 8;
 constexpr int kRedRows = 384;      // resident rows per compression partial
 constexpr int kAttnRows = 128;     // selected rows per attention split
@@ -26,10 +29,30 @@ enum Meta : int {
     M_LITE = 4,        // lite_start
     M_SURE = 5,        // sure list length (atomic)
     M_CAND = 6,        // candidate list length (atomic)
-    M_MODE = 7,        // 0 radix path, 1 everything fits, 2 overflow fallback
+    M_MODE = 7,        // 0 sampled radix path, 1 everything fits, 3 hint window + scan, 5 hint window, direct writes
+    // 8..11: mode-0 band (select.cu MetaExt)
+    M_HINT = 16,       // persistent: key of the previous step's k-th largest score
+    M_HINT_OK = 17,    // persistent: M_HINT is valid
+    M_KLO = 18,        // this step's hint window start (key)
+    M_FBIN = 19,       // mode 3: window bin holding the k-th largest
+    M_NABOVE = 20,     // mode 3: rows strictly above that bin (all sure)
+    M_ABOVE = 21,      // rows above the hint window (atomic, score kernel)
+    M_SPARTS = 22,     // mode 5: score parts of this head
+    M_HITS = 23,       // mode 5: hits among Omega_{t-1} outside the threshold bin
+    M_PCRIT = 24,      // mode 5: Omega_{t-1} rows inside the threshold bin (atomic count)
+    M_PCRIT_LIST = 25, // mode 5: ... their indices (kPrevCrit)
+    M_STAT = 33,       // persistent: head-steps finalized per mode (33 + mode, modes 0..5; 39: exact fallbacks)
+    M_BITS_FRESH = 40, // res_bits already holds res_idx (set by seed; prepare then skips the hit count)
 };
+constexpr int kPrevCrit = 8;
 
-enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3, C_PREPARE = 4 };
+// attention partial slots per head (attention splits, or select_attend parts)
+LRQK_DEV int attn_slots_dev(const lrqk_layer_t &L, int parts) {
+    const int splits = (L.s_cap + kAttnRows - 1) / kAttnRows;
+    return splits > parts ? splits : parts;
+}
+
+enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3, C_PREPARE = 4, C_FUSED = 5 };
 
 // ---------------------------------------------------------------------------
 // vector loads: 16 bytes of storage -> float lanes
@@ -256,23 +279,23 @@ LRQK_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar
 }  // namespace lrqk
 
 // ---------------------------------------------------------------------------
-// Development tracing: when g_lrqk_trace_on is set (lrqk_trace_enable), thread
-// 0 of a block records (tag, block, %globaltimer) records.  Off by default.
+// Development tracing: when g_lrqk_trace_on is set (lrqk_trace_enable),
+// thread 0 of a block stores (tag, block, %globaltimer) into a fixed slot
+// per (block, tag) -- a plain store, so tracing adds no round trip to the
+// critical path.  Off by default.
 // ---------------------------------------------------------------------------
 namespace lrqk {
 constexpr int kTraceCap = 1 << 16;
 extern __device__ int g_lrqk_trace_on;
-extern __device__ unsigned int g_lrqk_trace_n;
 extern __device__ unsigned long long g_lrqk_trace[kTraceCap][2];
 LRQK_DEV void trace(int tag) {
     if (g_lrqk_trace_on && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        const unsigned i = atomicAdd(&g_lrqk_trace_n, 1u);
-        if (i < kTraceCap) {
-            g_lrqk_trace[i][0] = ((unsigned long long)tag << 48) | ((unsigned long long)blockIdx.y << 24) | blockIdx.x;
-            g_lrqk_trace[i][1] = t;
-        }
+        const unsigned blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        const unsigned i = ((blk & 1023u) << 6) | (unsigned)(tag & 63);
+        g_lrqk_trace[i][0] = ((unsigned long long)tag << 48) | blk;
+        g_lrqk_trace[i][1] = t;
     }
 }
 }  // namespace lrqk

@@ -418,6 +418,49 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
 }
 
 // ---------------------------------------------------------------------------
+// Hit/miss accounting of the HBM policy (cache.py:190-195, 63-74), off the
+// decode critical path: compress_prepare runs after the step's selection on
+// a side stream.  res_bits holds the fast tier before the fetch, Omega_{t-1};
+// the new token t is never in it, so
+//     hits = 1 + #{x in Omega_t : x in Omega_{t-1}},  miss = |Omega_t| - hits,
+// then res_bits becomes Omega_t.  After lrqk_seed_prompt the bitmap already
+// equals Omega (M_BITS_FRESH) and nothing is counted.
+// ---------------------------------------------------------------------------
+__device__ void count_hits_hbm(const lrqk_layer_t &L, int bh, int n, float *scratch) {
+    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+    const int words = (L.t_max + 31) >> 5;
+    uint32_t *bits = L.res_bits + (size_t)bh * words;
+    const int *idx = L.res_idx + (size_t)bh * L.s_cap;
+    __syncthreads();
+    const bool fresh = meta[M_BITS_FRESH] != 0;
+    if (!fresh) {
+        int hit = 0;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int x = __ldcg(idx + i);
+            hit += (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
+        }
+        int *s_red = reinterpret_cast<int *>(scratch);
+        int hits;
+        block_exclusive_scan(hit, s_red, &hits);
+        for (int w = threadIdx.x; w < words; w += blockDim.x) bits[w] = 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int miss = n - (hits + 1);
+            L.c_miss[bh] += miss;
+            L.c_total[bh] += n;
+            L.step_miss[bh] = miss;
+            L.step_total[bh] = n;
+        }
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int x = __ldcg(idx + i);
+            atomicOr(bits + (x >> 5), 1u << (x & 31));
+        }
+    } else if (threadIdx.x == 0) {
+        meta[M_BITS_FRESH] = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // K2p: compress_prepare
 // ---------------------------------------------------------------------------
 template <typename T> constexpr bool kUseMma = false;
@@ -639,6 +682,7 @@ prepare_kernel(const lrqk_layer_t L) {
             }
         }
         if (tid == 0) pre[PL.flags + 1] = ok ? 1.f : 0.f;
+        if (!host) count_hits_hbm(L, bh, n_prev, s_rc);
     }
     trace((int)blockIdx.x < nchunks ? 12 : 13);
     if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_PREPARE, gridDim.x, &s_flag)) return;

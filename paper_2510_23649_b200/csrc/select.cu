@@ -24,14 +24,18 @@
 //                  and does the cache update.  If the verification fails the
 //                  block falls back to an exact radix select over all keys.
 #include "common.cuh"
+#include "select_common.cuh"
 
 namespace lrqk {
 
 constexpr int kScoreThreads = 256;
 constexpr int kSelThreads = 512;
-constexpr int kIdxBits = 21;        // tokens per head < 2^21
-constexpr uint32_t kIdxMax = (1u << kIdxBits) - 1u;
 constexpr int kSampleRows = 16384;  // histogram rows per head before sampling kicks in
+// Direct selection (mode 5, HBM policy): the score kernel also keeps each
+// part's window histogram (fcand, reinterpreted as [parts][kHistBins + 1]
+// uint32: bins, then the count above the window), so its last block knows
+// how many certain winners every part holds -> each select block writes its
+// winners straight to their final positions in res_idx.
 
 // extra sel_meta fields (common.cuh holds the first ones)
 enum MetaExt : int { M_B_HI = 8, M_B_LO = 9, M_STRIDE = 10, M_S2 = 11 };
@@ -42,10 +46,6 @@ LRQK_DEV int fine_bin(uint32_t key, int b_lo, int s2) {
 }
 
 
-LRQK_DEV uint64_t make_comp(uint32_t key, int idx) {
-    return ((uint64_t)key << kIdxBits) | (uint64_t)(kIdxMax - (uint32_t)idx);
-}
-LRQK_DEV int comp_index(uint64_t c) { return (int)(kIdxMax - (uint32_t)(c & kIdxMax)); }
 
 LRQK_DEV int sample_stride(int n_rows) {  // in 32-row tiles
     const int tiles = (n_rows + 31) >> 5;
@@ -176,7 +176,7 @@ score_kernel(const ScoreArgs a) {
             }
         }
         __syncthreads();
-        uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;
+        uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;
         for (int i = tid; i < kHistBins; i += blockDim.x)
             if (s_hist[i]) atomicAdd(ghist + i, (uint32_t)s_hist[i]);
         int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
@@ -234,7 +234,7 @@ constexpr int kCW = 8;  // consumer warps
 template <int NPK> struct ScoreStages {
     static constexpr int kTileBytes = NPK * 512;
     static constexpr int kStageBytes = kCW * kTileBytes;
-    static constexpr int kStages = (96 * 1024 / kStageBytes) < 2 ? 2 : ((96 * 1024 / kStageBytes) > 6 ? 6 : 96 * 1024 / kStageBytes);
+    static constexpr int kStages = (80 * 1024 / kStageBytes) < 2 ? 2 : ((80 * 1024 / kStageBytes) > 6 ? 6 : 80 * 1024 / kStageBytes);
     static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
 
@@ -249,9 +249,11 @@ score_tma_kernel(const ScoreArgs a) {
     uint64_t *full = reinterpret_cast<uint64_t *>(tsm + SS::kStages * SS::kStageBytes);
     uint64_t *empty = full + SS::kStages;
     __shared__ int s_hist[kHistBins];
+    __shared__ int s_win[kHistBins];
     __shared__ int s_scan[32];
     __shared__ int s_flag;
     __shared__ int s_out[2];
+    __shared__ int s_above;
     trace(40);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int P = a.parts;
@@ -266,8 +268,18 @@ score_tma_kernel(const ScoreArgs a) {
     const int tile0 = min(tiles, part * tpp), tile1 = min(tiles, tile0 + tpp);
     const int stride = sample_stride(lite_start);
     const int n_stage_iters = (tile1 - tile0 + kCW - 1) / kCW;
-    for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = 0;
+    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+    // hint window (persistent meta written by the previous step's select)
+    const bool win = meta[M_HINT_OK] != 0;
+    uint32_t klo = 0;
+    if (win) {
+        const uint32_t hk = (uint32_t)meta[M_HINT];
+        klo = hk > kWinKeys / 2 ? hk - kWinKeys / 2 : 0u;
+        if (klo > 0xFFFFFFFFu - (kWinKeys - 1)) klo = 0xFFFFFFFFu - (kWinKeys - 1);
+    }
+    for (int i = tid; i < kHistBins; i += blockDim.x) { s_hist[i] = 0; s_win[i] = 0; }
     if (tid == 0) {
+        s_above = 0;
         for (int s2 = 0; s2 < SS::kStages; ++s2) {
             mbar_init(full + s2, 1);
             mbar_init(empty + s2, kCW);
@@ -299,6 +311,7 @@ score_tma_kernel(const ScoreArgs a) {
         const float *qh = L.q_hat + (size_t)bh * L.rank_stride;
 #pragma unroll
         for (int e = 0; e < R; ++e) qv[e] = qh[e];
+        int above = 0;
         for (int it = 0; it < n_stage_iters; ++it) {
             const int s2 = it % SS::kStages;
             mbar_wait(full + s2, (it / SS::kStages) & 1);
@@ -319,29 +332,104 @@ score_tma_kernel(const ScoreArgs a) {
                 const int row = tile * 32 + lane;
                 const uint32_t key = score_key(s0 + s1);
                 if (row < n) keys[row] = key;
-                if (row < lite_start && (tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
+                if (row < lite_start) {
+                    if ((tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
+                    if (win && key >= klo) {
+                        const uint32_t dk = key - klo;
+                        if (dk < kWinKeys) atomicAdd(&s_win[dk >> kWinShift], 1);
+                        else ++above;
+                    }
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s2);
         }
+        above = __reduce_add_sync(0xffffffffu, above);
+        if (lane == 0 && above) atomicAdd(&s_above, above);
     }
     trace(41);
     __syncthreads();
-    uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;
-    for (int i = tid; i < kHistBins; i += blockDim.x)
+    uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;
+    uint32_t *gwin = ghist + 2 * kHistBins;
+    for (int i = tid; i < kHistBins; i += blockDim.x) {
         if (s_hist[i]) atomicAdd(ghist + i, (uint32_t)s_hist[i]);
+        if (s_win[i]) atomicAdd(gwin + i, (uint32_t)s_win[i]);
+    }
+    if (tid == 0 && s_above) atomicAdd(meta + M_ABOVE, s_above);
+    if (win) {
+        // this part's suffix counts (mode 5): ph[i] = rows of the part with a
+        // key in window bin >= i or above the window; ph[kHistBins] = above
+        uint32_t *ph = reinterpret_cast<uint32_t *>(L.fcand) + ((size_t)bh * P + part) * kPartHist;
+        constexpr int CB = kHistBins / 256;  // bins per thread (threads 0..255)
+        int loc = 0;
+        if (tid < 256)
+#pragma unroll
+            for (int j = 0; j < CB; ++j) loc += s_win[tid * CB + j];
+        int tot;
+        const int ex = block_exclusive_scan(loc, s_scan, &tot);
+        if (tid < 256) {
+            int suf = s_above + tot - ex;  // rows in bins >= tid*CB, plus above
+#pragma unroll
+            for (int j = 0; j < CB; ++j) {
+                ph[tid * CB + j] = (uint32_t)suf;
+                suf -= s_win[tid * CB + j];
+            }
+        }
+        if (tid == 0) ph[kHistBins] = (uint32_t)s_above;
+    }
     int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
     if (!last_arrival(cnt, P, &s_flag)) return;
     trace(42);
     // ---- last block of this head: candidate bins ----------------------------
-    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     const int k_eff = min(L.k_budget, lite_start);
     if (lite_start == 0 || k_eff >= lite_start) {
         if (tid == 0) {
             meta[M_MODE] = 1; meta[M_K_EFF] = k_eff; meta[M_LITE] = lite_start;
-            meta[M_SURE] = 0; meta[M_CAND] = 0;
+            meta[M_SURE] = 0; meta[M_CAND] = 0; meta[M_ABOVE] = 0;
         }
         return;
+    }
+    if (win) {
+        // mode 3 if the k-th largest key falls inside the hint window: the
+        // window histogram is exact, so bin D and the count above it are exact
+        const int above_win = __ldcg(meta + M_ABOVE);
+        for (int i = tid; i < kHistBins; i += blockDim.x) s_win[i] = (int)__ldcg(gwin + i);
+        __syncthreads();
+        int D = -1;
+        if (above_win < k_eff) {
+            find_crossing(s_win, kHistBins, k_eff - above_win, s_scan, s_out);
+            D = s_out[0];
+        }
+        if (D >= 0) {
+            const int nabove = above_win + s_out[1];
+            int mode = 3;
+            if (L.policy == LRQK_SLOW_HBM) {
+                // mode 5: certain winners per part -> exclusive offsets (fcnt)
+                mode = 5;
+                const uint32_t *ph0 = reinterpret_cast<const uint32_t *>(L.fcand) + (size_t)bh * P * kPartHist;
+                const int c = tid < P ? (int)__ldcg(ph0 + (size_t)tid * kPartHist + D + 1) : 0;
+                int tot;
+                const int off = block_exclusive_scan(c, s_scan, &tot);
+                if (tid < P) L.fcnt[(size_t)bh * P + tid] = off;
+                // inconsistent counts, or a threshold bin too large to sort: scan path
+                if (tot != nabove || s_win[D] > kCritCap) mode = 3;
+            }
+            if (tid == 0) {
+                meta[M_KLO] = (int)klo;
+                meta[M_FBIN] = D;
+                meta[M_NABOVE] = nabove;
+                meta[M_SPARTS] = P;
+                meta[M_K_EFF] = k_eff;
+                meta[M_LITE] = lite_start;
+                meta[M_SURE] = 0;
+                meta[M_CAND] = 0;
+                meta[M_ABOVE] = 0;
+                meta[M_MODE] = mode;
+            }
+            trace(43);
+            return;
+        }
+        __syncthreads();
     }
     for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = (int)__ldcg(ghist + i);
     __syncthreads();
@@ -368,6 +456,7 @@ score_tma_kernel(const ScoreArgs a) {
         meta[M_LITE] = lite_start;
         meta[M_SURE] = 0;
         meta[M_CAND] = 0;
+        meta[M_ABOVE] = 0;
         meta[M_MODE] = 0;
     }
     trace(43);
@@ -401,6 +490,34 @@ __device__ uint64_t radix_top_m(Get get, int n, int m, int nbits, int *s_hist, i
     return prefix;
 }
 
+
+// Exclusive block scan of four 16-bit counters packed in a uint64.
+LRQK_DEV uint64_t block_exclusive_scan_u64(uint64_t v, uint64_t *s_warp, uint64_t *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t w = lane < nw ? s_warp[lane] : 0ull;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < nw) s_warp[lane] = w;
+    }
+    __syncthreads();
+    const uint64_t before = warp > 0 ? s_warp[warp - 1] : 0ull;
+    *total = s_warp[nw - 1];
+    __syncthreads();
+    return before + x - v;
+}
+
 // ---------------------------------------------------------------------------
 // K4 + K5: sure/candidate split with an exact fine histogram of the
 // candidate band, then (last block per head) the exact top-k, ascending
@@ -408,7 +525,6 @@ __device__ uint64_t radix_top_m(Get get, int n, int m, int nbits, int *s_hist, i
 // ---------------------------------------------------------------------------
 constexpr int kLocSure = 1024;  // block-local append buffers (spill to global beyond)
 constexpr int kLocCand = 2048;
-constexpr int kCritCap = 4096;  // critical fine bin sorted in shared memory (larger -> exact fallback)
 
 __global__ void __launch_bounds__(kSelThreads, 2)
 select_kernel(const lrqk_layer_t L, int parts) {
@@ -418,6 +534,8 @@ select_kernel(const lrqk_layer_t L, int parts) {
     __shared__ int s_out[2];
     __shared__ int s_flag;
     __shared__ int s_cnt[4];
+    __shared__ uint32_t s_hint_key;
+    __shared__ int s_hint_ok;
     const int tid = threadIdx.x, lane = tid & 31, nt = blockDim.x;
     const int BH = L.batch * L.n_q_heads;
     const bool host = L.policy == LRQK_SLOW_HOST;
@@ -432,11 +550,12 @@ select_kernel(const lrqk_layer_t L, int parts) {
         if (t >= L.t_max) continue;
         int *meta = L.sel_meta + (size_t)bh * kMetaInts;
         const int mode0 = meta[M_MODE];
+        if (mode0 == 5) continue;  // select_attend_kernel handles this head
         const int lite_start = meta[M_LITE];
         const int k_eff = meta[M_K_EFF];
         const uint32_t *keys = L.keys + (size_t)bh * L.t_max;
-        uint32_t *hist2 = L.hist + (size_t)bh * 2 * kHistBins + kHistBins;
-        int *sure = L.sure_idx + (size_t)bh * L.k_budget;
+        uint32_t *hist2 = L.hist + (size_t)bh * kHistLevels * kHistBins + kHistBins;
+        int *sure = L.sure_idx + (size_t)bh * parts * L.k_budget;  // = this head's part-0 region (mode 3)
         uint64_t *cand = L.cand + (size_t)bh * L.cand_cap;
         // ---- scan part: certain winners, candidates, fine histogram ----------
         if (mode0 == 0) {
@@ -524,6 +643,63 @@ select_kernel(const lrqk_layer_t L, int parts) {
             for (int i = tid; i < kHistBins; i += nt)
                 if (s_hist[i]) atomicAdd(hist2 + i, (uint32_t)s_hist[i]);
         }
+        if (mode0 == 3) {
+            // ---- hint-window path: rows above the critical window bin are
+            // certain winners, written per part in ascending order; rows in
+            // the critical bin are collected (few) -------------------------
+            const uint32_t klo = (uint32_t)meta[M_KLO];
+            const int D = meta[M_FBIN];
+            const int per = ((lite_start + parts - 1) / parts + 3) & ~3;  // 16-byte aligned parts
+            const int row0 = min(lite_start, part * per), row1 = min(lite_start, row0 + per);
+            int *psure = L.sure_idx + ((size_t)bh * parts + part) * L.k_budget;
+            int out = 0;  // block-uniform running count
+            constexpr int U = 4;
+            for (int base = row0; base < row1; base += nt * 4 * U) {
+                uint4 kv4[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int i = base + (u * nt + tid) * 4;
+                    kv4[u] = i < row1 ? __ldcg(reinterpret_cast<const uint4 *>(keys + i)) : make_uint4(0, 0, 0, 0);
+                }
+                uint32_t smask = 0;
+                uint64_t packed = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t kk[4] = {kv4[u].x, kv4[u].y, kv4[u].z, kv4[u].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int i = base + (u * nt + tid) * 4 + c;
+                        if (i < row1 && kk[c] >= klo) {
+                            const uint32_t dk = kk[c] - klo;
+                            if (dk >= kWinKeys || (int)(dk >> kWinShift) > D) {
+                                smask |= 1u << (u * 4 + c);
+                            } else if ((int)(dk >> kWinShift) == D) {
+                                const int g = atomicAdd(meta + M_CAND, 1);
+                                if (g < L.cand_cap) cand[g] = make_comp(kk[c], i);
+                            }
+                        }
+                    }
+                    packed |= (uint64_t)__popc((smask >> (u * 4)) & 0xFu) << (16 * u);
+                }
+                uint64_t tot;
+                const uint64_t ex = block_exclusive_scan_u64(packed, reinterpret_cast<uint64_t *>(fsm), &tot);
+                int off_u = out;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    int o = off_u + (int)((ex >> (16 * u)) & 0xFFFFu);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (smask & (1u << (u * 4 + c))) {
+                            if (o < L.k_budget) psure[o] = base + (u * nt + tid) * 4 + c;
+                            ++o;
+                        }
+                    }
+                    off_u += (int)((tot >> (16 * u)) & 0xFFFFu);
+                }
+                out = off_u;
+            }
+            if (tid == 0) hist2[part] = (uint32_t)out;
+        }
         trace(21);
         if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_SELECT, parts, &s_flag)) continue;
         trace(22);
@@ -539,6 +715,8 @@ select_kernel(const lrqk_layer_t L, int parts) {
         uint32_t *slot_used = reinterpret_cast<uint32_t *>(news + L.s_cap);
         const int slot_words = (L.n_slots + 31) >> 5;
         uint64_t *crit = reinterpret_cast<uint64_t *>(slot_used + ((slot_words + 3) & ~3));
+        int *s_sure = reinterpret_cast<int *>(crit + kCritCap);  // [k_budget] mode 3
+        int *s_poff = s_sure + L.k_budget;                        // [parts]   mode 3
         // prefetch in one round trip: Omega_{t-1} (+ slots), the fine
         // histogram, the list lengths; clear the bitmap meanwhile
         const int n_prev = L.res_cnt[bh];
@@ -550,9 +728,76 @@ select_kernel(const lrqk_layer_t L, int parts) {
         }
         if (mode0 == 0)
             for (int i = tid; i < kHistBins; i += nt) s_hist[i] = (int)__ldcg(hist2 + i);
+        if (tid == 0) { s_hint_key = 0u; s_hint_ok = 0; }
+        bool exact_fb = false;  // exact radix fallback over all keys
+        bool use_bitmap = false;  // newl comes from the bitmap compaction
         if (mode0 == 1) {
             for (int i = tid; i < k_eff; i += nt) newl[i] = i;  // everything fits
+        } else if (mode0 == 3) {
+            // ---- hint-window path: sorted per-part sure lists + the critical bin
+            trace(26);
+            const int nabove = meta[M_NABOVE];
+            const int need2 = k_eff - nabove;
+            const int n_crit = __ldcg(meta + M_CAND);
+            const int pc = tid < parts ? (int)__ldcg(hist2 + tid) : 0;
+            int ns_total;
+            const int poff = block_exclusive_scan(pc, s_scan, &ns_total);
+            if (tid < parts) s_poff[tid] = poff;
+            const bool ok = ns_total == nabove && need2 >= 0 && need2 <= n_crit && n_crit <= kCritCap &&
+                            n_crit <= L.cand_cap;
+            int M = 1;
+            while (M < n_crit) M <<= 1;
+            __syncthreads();
+            if (ok) {
+                for (int j = tid; j < ns_total; j += nt) {  // parts are ascending row ranges
+                    int lo = 0, hi = parts - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_poff[mid] <= j) lo = mid; else hi = mid - 1;
+                    }
+                    s_sure[j] = __ldcg(L.sure_idx + ((size_t)bh * parts + lo) * L.k_budget + (j - s_poff[lo]));
+                }
+                for (int i = tid; i < M; i += nt) crit[i] = i < n_crit ? __ldcg(cand + i) : 0ull;
+                __syncthreads();
+                trace(27);
+                block_bitonic(crit, M, true);  // descending composites
+                trace(28);
+                if (tid == 0) {
+                    s_hint_ok = 1;
+                    s_hint_key = need2 > 0 ? (uint32_t)(crit[need2 - 1] >> kIdxBits)
+                                           : (uint32_t)meta[M_KLO] + ((uint32_t)(meta[M_FBIN] + 1) << kWinShift);
+                }
+                __syncthreads();
+                int M2 = 1;
+                while (M2 < need2) M2 <<= 1;
+                for (int i = tid; i < M2; i += nt) crit[i] = i < need2 ? (uint64_t)comp_index(crit[i]) : ~0ull;
+                __syncthreads();
+                block_bitonic(crit, M2, false);  // winners by ascending index
+                trace(29);
+                // merge the ascending sure list and the ascending winners
+                for (int j = tid; j < ns_total; j += nt) {
+                    const int x = s_sure[j];
+                    int lo = 0, hi = need2;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if ((int)crit[mid] < x) lo = mid + 1; else hi = mid;
+                    }
+                    newl[j + lo] = x;
+                }
+                for (int i = tid; i < need2; i += nt) {
+                    const int w = (int)crit[i];
+                    int lo = 0, hi = ns_total;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (s_sure[mid] < w) lo = mid + 1; else hi = mid;
+                    }
+                    newl[i + lo] = w;
+                }
+            } else {
+                exact_fb = true;
+            }
         } else {
+            use_bitmap = true;
             for (int w = tid; w < n_words; w += nt) bitmap[w] = 0u;
             const int n_sure = __ldcg(meta + M_SURE);
             const int n_cand = __ldcg(meta + M_CAND);
@@ -588,38 +833,42 @@ select_kernel(const lrqk_layer_t L, int parts) {
                         __syncthreads();
                         for (int i = n_crit + tid; i < M; i += nt) crit[i] = 0ull;
                         __syncthreads();
-                        for (int kk = 2; kk <= M; kk <<= 1) {  // bitonic sort, descending
-                            for (int j = kk >> 1; j > 0; j >>= 1) {
-                                for (int i = tid; i < M; i += nt) {
-                                    const int ixj = i ^ j;
-                                    if (ixj > i) {
-                                        const uint64_t x = crit[i], y = crit[ixj];
-                                        const bool desc = (i & kk) == 0;
-                                        if (desc ? (x < y) : (x > y)) { crit[i] = y; crit[ixj] = x; }
-                                    }
-                                }
-                                __syncthreads();
-                            }
-                        }
+                        block_bitonic(crit, M, true);  // descending
                         for (int i = tid; i < need2; i += nt) {
                             const int x = comp_index(crit[i]);
                             atomicOr(&bitmap[x >> 5], 1u << (x & 31));
                         }
+                        if (tid == 0 && need2 > 0) {
+                            s_hint_ok = 1;
+                            s_hint_key = (uint32_t)(crit[need2 - 1] >> kIdxBits);
+                        }
                     }
+                } else if (tid == 0) {
+                    const int b_hi = meta[M_B_HI];
+                    s_hint_ok = 1;
+                    s_hint_key = b_hi >= kHistBins - 1 ? 0xFFFFFFFFu : (uint32_t)(b_hi + 1) << (32 - kHistBits);
                 }
             }
-            if (!ok) {
-                // exact fallback over the whole key array
-                __syncthreads();
-                for (int w = tid; w < n_words; w += nt) bitmap[w] = 0u;
-                if (tid == 0) set_status(L.status, LRQK_ST_FALLBACK);
-                auto get = [&](int i) { return make_comp(__ldcg(keys + i), i); };
-                const uint64_t thr = radix_top_m(get, lite_start, k_eff, 32 + kIdxBits, s_hist, s_scan, s_out);
-                for (int i = tid; i < lite_start; i += nt)
-                    if (make_comp(__ldcg(keys + i), i) >= thr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
-            }
-            trace(23);
+            if (!ok) exact_fb = true;
+        }
+        if (exact_fb) {
+            // exact fallback over the whole key array
+            use_bitmap = true;
             __syncthreads();
+            for (int w = tid; w < n_words; w += nt) bitmap[w] = 0u;
+            if (tid == 0) set_status(L.status, LRQK_ST_FALLBACK);
+            auto get = [&](int i) { return make_comp(__ldcg(keys + i), i); };
+            const uint64_t thr = radix_top_m(get, lite_start, k_eff, 32 + kIdxBits, s_hist, s_scan, s_out);
+            for (int i = tid; i < lite_start; i += nt)
+                if (make_comp(__ldcg(keys + i), i) >= thr) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+            if (tid == 0) {
+                s_hint_ok = 1;
+                s_hint_key = (uint32_t)(thr >> kIdxBits);
+            }
+        }
+        trace(23);
+        __syncthreads();
+        if (use_bitmap) {
             // ascending compaction of the bitmap
             const int per = (n_words + nt - 1) / nt;
             const int w0 = tid * per;
@@ -651,7 +900,19 @@ select_kernel(const lrqk_layer_t L, int parts) {
             if (tid == 0) hits_local = 1;
             for (int i = tid; i < n_prev; i += nt) {
                 const int x = prevl[i];
-                const bool in_new = mode0 == 1 || x >= lite_start || ((bitmap[x >> 5] >> (x & 31)) & 1u);
+                bool in_new = mode0 == 1 || x >= lite_start;
+                if (!in_new) {
+                    if (use_bitmap) {
+                        in_new = (bitmap[x >> 5] >> (x & 31)) & 1u;
+                    } else {  // newl[0, k_eff) is ascending
+                        int lo = 0, hi = k_eff;
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (newl[mid] < x) lo = mid + 1; else hi = mid;
+                        }
+                        in_new = lo < k_eff && newl[lo] == x;
+                    }
+                }
                 hits_local += in_new ? 1 : 0;
             }
         } else
@@ -733,16 +994,24 @@ select_kernel(const lrqk_layer_t L, int parts) {
         for (int i = tid; i < S; i += nt) res_idx[i] = newl[i];
         if (tid == 0) {
             L.res_cnt[bh] = S;
-            L.c_miss[bh] += miss;
-            L.c_total[bh] += S;
-            L.step_miss[bh] = miss;
-            L.step_total[bh] = S;
+            if (host) {  // HBM policy: counted by compress_prepare from the residency bitmap
+                L.c_miss[bh] += miss;
+                L.c_total[bh] += S;
+                L.step_miss[bh] = miss;
+                L.step_total[bh] = S;
+            }
             meta[M_SURE] = 0;
             meta[M_CAND] = 0;
+            meta[M_PCRIT] = 0;
+            meta[M_HITS] = 0;
+            meta[M_HINT] = (int)s_hint_key;
+            meta[M_HINT_OK] = s_hint_ok;
+            meta[M_STAT + min(max(mode0, 0), 5)] += 1;
+            if (exact_fb) meta[M_STAT + 6] += 1;
         }
         trace(25);
-        uint32_t *ghist = L.hist + (size_t)bh * 2 * kHistBins;  // both levels, ready for the next step
-        for (int i = tid; i < 2 * kHistBins; i += nt) ghist[i] = 0u;
+        uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;  // both levels, ready for the next step
+        for (int i = tid; i < kHistLevels * kHistBins; i += nt) ghist[i] = 0u;
         __syncthreads();
     }
 }
@@ -793,11 +1062,19 @@ static void launch_score_tma_t(const ScoreArgs &a, int grid, cudaStream_t st) {
     launch_kernel(fn, grid, 32 * (kCW + 1), SS::kSmem, st, true, a);
 }
 
+// parts (blocks) per head of the TMA score kernel; each owns a contiguous
+// tile range and one fcand region
+int score_tma_parts(const lrqk_layer_t &L) {
+    const int BH = L.batch * L.n_q_heads;
+    const int tiles = L.t_max / 32;
+    return max(1, min((2 * num_sms()) / BH, max(1, tiles / 64)));
+}
+int score_part_rows(const lrqk_layer_t &L) { return L.batch * L.n_q_heads * score_tma_parts(L); }
+
 template <typename T>
 static int launch_score_tma(const lrqk_layer_t &L, cudaStream_t st) {
     const int BH = L.batch * L.n_q_heads;
-    const int tiles = L.t_max / 32;
-    const int P = max(1, min((2 * num_sms()) / BH, max(1, tiles / 64)));
+    const int P = score_tma_parts(L);
     ScoreArgs a{L, nullptr, P};
     const int grid = BH * P;
     const int npk = L.rank_stride * (int)sizeof(T) / 16;
@@ -825,13 +1102,20 @@ size_t finalize_smem_bytes(const lrqk_layer_t &L) {
     const size_t cand_pow2 = kCritCap;
     const size_t fin = ((n_words + 3) & ~(size_t)3) * 4 + 4 * (size_t)L.s_cap * 4 +
                        ((slot_words + 3) & ~(size_t)3) * 4 + cand_pow2 * 8;
+    const size_t mode3 = ((size_t)L.k_budget + 512) * 4;
     const size_t scan = (size_t)kLocSure * 4 + (size_t)kLocCand * 8;
-    return fin > scan ? fin : scan;
+    return fin + mode3 > scan ? fin + mode3 : scan;
 }
+
+// select parts per head (one block each); the mode-3 sure lists need one
+// k_budget-row region per (head, part)
+int score_tma_parts(const lrqk_layer_t &L);
+int select_parts(const lrqk_layer_t &L) { return score_tma_parts(L); }  // mode 5 reuses the score partition
+int select_sure_rows(const lrqk_layer_t &L) { return L.batch * L.n_q_heads * select_parts(L); }
 
 int launch_select(const lrqk_layer_t &L, cudaStream_t st) {
     const int BH = L.batch * L.n_q_heads;
-    const int parts = max(1, min((num_sms() * 2) / BH, max(1, L.t_max / 4096)));
+    const int parts = select_parts(L);
     const int grid = max(1, min(BH * parts, num_sms() * 2));
     const size_t smem = finalize_smem_bytes(L);
     cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

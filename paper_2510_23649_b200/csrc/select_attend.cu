@@ -1,0 +1,425 @@
+// K4 + K6 fused (selection mode 5, HBM policy): top-k selection straight
+// from the score keys and exact softmax attention over the winners, in one
+// kernel.  ref: cache.py:149-171 (select_active), linalg.py:96-110
+// (topk_indices), attention.py:23-34 (exact_attention), session.py:99-102.
+//
+// The score kernel (select.cu) has already found, from an exact histogram of
+// the keys around the previous step's threshold, the bin D that holds the
+// k-th largest key, and for every part p of the head the number of certain
+// winners (keys in bins above D) in the parts before it (fcnt).  So each
+// block of this kernel owns one part, and in a single pass over its keys it
+//   - writes its certain winners, ascending, to res_idx[fcnt[p] + rank],
+//   - collects the rows of bin D (a handful) for the last block,
+//   - gathers the winners' K/V rows and accumulates an online-softmax
+//     partial (max, sum, acc) for its rows.
+// The last block of the head ranks bin D (ties -> lower index, as the
+// reference), appends those winners and Omega_l = the lite window, adds
+// their rows to the softmax, merges the parts' partials and writes the
+// output.  Omega_k is stored as [certain winners ascending] ++ [bin-D
+// winners ascending]; attention and compression are sums over the set, and
+// the host views sort it.  Hit/miss counts are done off the critical path by
+// compress_prepare (compress.cu: count_hits_hbm).
+#include "common.cuh"
+#include "select_common.cuh"
+
+namespace lrqk {
+
+int score_tma_parts(const lrqk_layer_t &L);
+
+constexpr int kFThreads = 256;
+constexpr int kFRows = kFThreads * 32;  // keys per scan pass: 32 contiguous keys per thread
+constexpr int kFList = kCritCap + 64;   // last block: bin-D winners + lite rows
+
+struct FArgs {
+    lrqk_layer_t L;
+    const void *q;
+    float *out;
+    int parts;
+};
+
+// Online softmax over the K/V rows listed in rows[0, n) (shared memory),
+// continuing (m, l, acc) of this lane group.  LPR lanes per row, PPL 16-byte
+// packs per lane; all lanes of a warp run the same trip count.
+template <typename T, int LPR, int PPL>
+__device__ void attend_list(const T *kb, const T *vb, const int *rows, int n, const float (&qv)[PPL][Pack<T>::N],
+                            float c, int d, float &m, float &l, float (&acc)[PPL][Pack<T>::N]) {
+    constexpr int N = Pack<T>::N;
+    constexpr int RPW = 32 / LPR;
+    constexpr int U = 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int sub = lane / LPR, sl = lane - sub * LPR;
+    const int step = nw * RPW;
+    for (int b0 = warp * RPW; b0 < n; b0 += step * U) {
+        uint4 kx[U][PPL], vx[U][PPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = b0 + sub + u * step;
+            if (j < n) {
+                const size_t row = (size_t)rows[j] * d;
+#pragma unroll
+                for (int pp = 0; pp < PPL; ++pp) {
+                    kx[u][pp] = *reinterpret_cast<const uint4 *>(kb + row + (sl + pp * LPR) * N);
+                    vx[u][pp] = *reinterpret_cast<const uint4 *>(vb + row + (sl + pp * LPR) * N);
+                }
+            } else {
+#pragma unroll
+                for (int pp = 0; pp < PPL; ++pp) { kx[u][pp] = make_uint4(0, 0, 0, 0); vx[u][pp] = make_uint4(0, 0, 0, 0); }
+            }
+        }
+        float x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float s = 0.f;
+#pragma unroll
+            for (int pp = 0; pp < PPL; ++pp) {
+                float f[N];
+                unpack16<T>(kx[u][pp], f);
+#pragma unroll
+                for (int e = 0; e < N; ++e) s = fmaf(f[e], qv[pp][e], s);
+            }
+            x[u] = s;
+        }
+#pragma unroll
+        for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], o);
+        float mx = m;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            x[u] = (b0 + sub + u * step < n) ? x[u] * c : -INFINITY;
+            mx = fmaxf(mx, x[u]);
+        }
+        if (mx == -INFINITY) continue;
+        const float scale = exp2f(m - mx);
+        l *= scale;
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+            for (int e = 0; e < N; ++e) acc[pp][e] *= scale;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const float p = exp2f(x[u] - mx);
+            l += p;
+#pragma unroll
+            for (int pp = 0; pp < PPL; ++pp) {
+                float f[N];
+                unpack16<T>(vx[u][pp], f);
+#pragma unroll
+                for (int e = 0; e < N; ++e) acc[pp][e] = fmaf(p, f[e], acc[pp][e]);
+            }
+        }
+        m = mx;
+    }
+}
+
+// Merge the lane groups' (m, l, acc) into one block partial: dst[0] = max,
+// dst[1] = sum, dst[2 + i] = acc (log2 domain, as the attention kernel).
+// Groups of a warp merge through shuffles, warps through shared memory with
+// precomputed weights.
+LRQK_DEV void merge_pair(float &m, float &l, float m2, float l2, float &w1, float &w2) {
+    const float M = fmaxf(m, m2);
+    w1 = m == -INFINITY ? 0.f : exp2f(m - M);
+    w2 = m2 == -INFINITY ? 0.f : exp2f(m2 - M);
+    l = l * w1 + l2 * w2;
+    m = M;
+}
+template <typename T, int LPR, int PPL>
+__device__ void block_partial(float m, float l, float (&acc)[PPL][Pack<T>::N], int d, float *s_m, float *s_l,
+                              float *s_acc, float *dst) {
+    constexpr int N = Pack<T>::N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int sl = lane % LPR;
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), l2 = __shfl_xor_sync(0xffffffffu, l, o);
+        float w1, w2;
+        merge_pair(m, l, m2, l2, w1, w2);
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+            for (int e = 0; e < N; ++e) {
+                const float a2 = __shfl_xor_sync(0xffffffffu, acc[pp][e], o);
+                acc[pp][e] = acc[pp][e] * w1 + a2 * w2;
+            }
+    }
+    if (lane < LPR) {
+        if (lane == 0) { s_m[warp] = m; s_l[warp] = l; }
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+            for (int e = 0; e < N; ++e) s_acc[warp * d + (sl + pp * LPR) * N + e] = acc[pp][e];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp weights
+        const float mw = lane < nw ? s_m[lane] : -INFINITY;
+        float M = mw;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float w = (lane < nw && mw != -INFINITY) ? exp2f(mw - M) : 0.f;
+        float lw = lane < nw ? s_l[lane] * w : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lw += __shfl_xor_sync(0xffffffffu, lw, o);
+        if (lane < nw) s_l[lane] = w;  // now the warp weight
+        if (lane == 0) { dst[0] = M; dst[1] = lw; }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float a = 0.f;
+        for (int w = 0; w < nw; ++w) a = fmaf(s_acc[w * d + i], s_l[w], a);
+        dst[2 + i] = a;
+    }
+    __syncthreads();
+}
+
+template <typename T, int LPR, int PPL>
+__global__ void __launch_bounds__(kFThreads, 2)
+select_attend_kernel(const FArgs a) {
+    const lrqk_layer_t &L = a.L;
+    constexpr int N = Pack<T>::N;
+    constexpr int RPW = 32 / LPR;
+    constexpr int NG = (kFThreads / 32) * RPW;
+    extern __shared__ __align__(16) uint8_t f_smem[];
+    int *s_rows = reinterpret_cast<int *>(f_smem);                 // [kFRows] (last block: crit, uint64)
+    int *s_list = s_rows + kFRows;                                 // [kFList]
+    float *s_acc = reinterpret_cast<float *>(s_list + kFList);     // [NG][d]
+    float *s_part = s_acc + NG * L.dim_stride;                     // [d + 2] last block's own partial
+    __shared__ float s_m[kFThreads / 32], s_l[kFThreads / 32];
+    __shared__ float s_pm[64], s_pw[64];
+    __shared__ int s_scan[32];
+    __shared__ int s_flag;
+    const int P = a.parts;
+    const int bh = blockIdx.x / P, part = blockIdx.x - bh * P;
+    const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
+    const int d = L.dim_stride;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int sub = lane / LPR, sl = lane - sub * LPR;
+    trace(50);
+    pdl_wait();
+    pdl_trigger();
+    const int t = L.ctx_len[b];
+    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+    // prefetch this part's first 32 keys per thread (the score kernel's
+    // partition) and the query row together with the meta loads
+    const int lite_start = max(0, t + 1 - L.lite_budget);
+    const int tpp = (((t + 1 + 31) >> 5) + P - 1) / P;
+    const int row0 = min(lite_start, part * tpp * 32), row1 = min(lite_start, (part + 1) * tpp * 32);
+    const uint32_t *keys = L.keys + (size_t)bh * L.t_max;
+    uint4 pf[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int i = row0 + tid * 32 + u * 4;
+        pf[u] = i < row1 ? *reinterpret_cast<const uint4 *>(keys + i) : make_uint4(0, 0, 0, 0);
+    }
+    float qv[PPL][N];
+    {
+        const T *qr = reinterpret_cast<const T *>(a.q) + (size_t)bh * d;
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp) Pack<T>::load(qr + (sl + pp * LPR) * N, qv[pp]);
+    }
+    const int mode = meta[M_MODE];
+    if (t >= L.t_max || mode != 5) return;  // other heads: select_kernel + attention_kernel
+    const uint32_t klo = (uint32_t)meta[M_KLO];
+    const int D = meta[M_FBIN];
+    const int k_eff = meta[M_K_EFF];
+    const int nabove = meta[M_NABOVE];
+    int out = __ldcg(L.fcnt + (size_t)bh * P + part);
+    int *dst = L.res_idx + (size_t)bh * L.s_cap;
+    uint64_t *cand = L.cand + (size_t)bh * L.cand_cap;
+    const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+    const T *kb = reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
+    const T *vb = reinterpret_cast<const T *>(L.slow_v) + kv_rows * d;
+    const float c = 1.4426950408889634f * rsqrtf((float)L.head_dim);  // log2(e) / sqrt(d)
+    float m = -INFINITY, l = 0.f;
+    float acc[PPL][N];
+#pragma unroll
+    for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+        for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
+    trace(51);
+
+    // ---- this part's winners: ordered write, then attention ----------------
+    int nloc = 0;
+    for (int base = row0; base < row1; base += kFRows) {
+        uint4 kv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + tid * 32 + u * 4;
+            kv[u] = base == row0 ? pf[u] : (i < row1 ? *reinterpret_cast<const uint4 *>(keys + i) : make_uint4(0, 0, 0, 0));
+        }
+        uint32_t smask = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t kk[4] = {kv[u].x, kv[u].y, kv[u].z, kv[u].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = base + tid * 32 + u * 4 + e;
+                if (i < row1 && kk[e] >= klo) {
+                    const uint32_t dk = kk[e] - klo;
+                    if (dk >= kWinKeys || (int)(dk >> kWinShift) > D) {
+                        smask |= 1u << (u * 4 + e);
+                    } else if ((int)(dk >> kWinShift) == D) {
+                        const int q = atomicAdd(meta + M_CAND, 1);
+                        if (q < L.cand_cap) cand[q] = make_comp(kk[e], i);
+                    }
+                }
+            }
+        }
+        int tot;
+        int o = nloc + block_exclusive_scan(__popc(smask), s_scan, &tot);
+        while (smask) {  // thread-contiguous keys: ascending order is (thread, bit)
+            const int bpos = __ffs(smask) - 1;
+            smask &= smask - 1u;
+            const int x = base + tid * 32 + bpos;
+            if (o < kFRows) s_rows[o] = x;
+            if (out + o < k_eff) dst[out + o] = x;
+            ++o;
+        }
+        nloc += tot;
+    }
+    const int nl = t + 1 - lite_start;
+    if (part == P - 1) {  // Omega_l = the lite window, attended by the last part
+        for (int i = tid; i < nl; i += blockDim.x) {
+            dst[k_eff + i] = lite_start + i;
+            if (nloc + i < kFRows) s_rows[nloc + i] = lite_start + i;
+        }
+        nloc += nl;
+    }
+    __syncthreads();
+    attend_list<T, LPR, PPL>(kb, vb, s_rows, min(nloc, kFRows), qv, c, d, m, l, acc);
+    trace(52);
+    float *part_dst = L.attn_scratch + ((size_t)bh * attn_slots_dev(L, P) + part) * (size_t)(d + 2);
+    block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, part_dst);
+    if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_FUSED, P, &s_flag)) return;
+    trace(53);
+
+    // ---- last block: rank bin D, Omega_l, merge ------------------------------
+    const int need2 = k_eff - nabove;
+    const int n_crit = __ldcg(meta + M_CAND);
+    int M = 1;
+    while (M < n_crit) M <<= 1;
+    const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && M <= kCritCap;
+    uint64_t *crit = reinterpret_cast<uint64_t *>(s_rows);
+    int nwin = 0;
+    uint32_t hint = klo + ((uint32_t)(D + 1) << kWinShift);
+    if (ok) {
+        for (int i = tid; i < M; i += blockDim.x) crit[i] = i < n_crit ? __ldcg(cand + i) : 0ull;
+        __syncthreads();
+        block_bitonic(crit, M, true);  // descending composites: ties -> lower index first
+        if (need2 > 0) hint = (uint32_t)(crit[need2 - 1] >> kIdxBits);
+        int M2 = 1;
+        while (M2 < need2) M2 <<= 1;
+        for (int i = tid; i < M2; i += blockDim.x) crit[i] = i < need2 ? (uint64_t)comp_index(crit[i]) : ~0ull;
+        __syncthreads();
+        block_bitonic(crit, M2, false);  // winners by ascending index
+        nwin = need2;
+        trace(55);
+    } else if (tid == 0) {
+        set_status(L.status, LRQK_ST_INDEX_RANGE);  // inconsistent selection state (never expected)
+    }
+    for (int i = tid; i < nwin; i += blockDim.x) {
+        const int x = (int)crit[i];
+        dst[nabove + i] = x;
+        s_list[i] = x;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+        for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
+    m = -INFINITY;
+    l = 0.f;
+    trace(56);
+    attend_list<T, LPR, PPL>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);
+    trace(57);
+    block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, s_part);
+    trace(58);
+    // merge the P part partials with this block's (the lite rows are never
+    // empty, so the running max is finite)
+    const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, P) * (size_t)(d + 2);
+    float MM = s_part[0];
+    for (int p0 = 0; p0 < P; p0 += 64) {
+        const int np = min(64, P - p0);
+        for (int p = tid; p < np; p += blockDim.x) s_pm[p] = __ldcg(parts + (size_t)(p0 + p) * (d + 2));
+        __syncthreads();
+        for (int p = 0; p < np; ++p) MM = fmaxf(MM, s_pm[p]);
+        __syncthreads();
+    }
+    trace(59);
+    const float w0 = s_part[0] == -INFINITY ? 0.f : exp2f(s_part[0] - MM);
+    float den = s_part[1] * w0;
+    for (int i = tid; i < d; i += blockDim.x) s_part[2 + i] *= w0;
+    __syncthreads();
+    for (int p0 = 0; p0 < P; p0 += 64) {
+        const int np = min(64, P - p0);
+        for (int p = tid; p < np; p += blockDim.x) {
+            const float pm = __ldcg(parts + (size_t)(p0 + p) * (d + 2));
+            s_pw[p] = pm == -INFINITY ? 0.f : exp2f(pm - MM);
+            s_pm[p] = __ldcg(parts + (size_t)(p0 + p) * (d + 2) + 1);
+        }
+        __syncthreads();
+        for (int p = 0; p < np; ++p) den = fmaf(s_pm[p], s_pw[p], den);
+        for (int i = tid; i < d; i += blockDim.x) {
+            float o0 = s_part[2 + i];
+            for (int p = 0; p < np; ++p) o0 = fmaf(__ldcg(parts + (size_t)(p0 + p) * (d + 2) + 2 + i), s_pw[p], o0);
+            s_part[2 + i] = o0;
+        }
+        __syncthreads();
+    }
+    trace(60);
+    const float inv = 1.f / den;
+    for (int i = tid; i < d; i += blockDim.x) a.out[(size_t)bh * d + i] = s_part[2 + i] * inv;
+    if (tid == 0) {
+        L.res_cnt[bh] = k_eff + (t + 1 - lite_start);
+        meta[M_CAND] = 0;
+        meta[M_HINT] = (int)hint;
+        meta[M_HINT_OK] = 1;
+        meta[M_STAT + 5] += 1;
+    }
+    uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;  // ready for the next step
+    for (int i = tid; i < kHistLevels * kHistBins; i += blockDim.x) ghist[i] = 0u;
+    trace(54);
+}
+
+template <typename T>
+static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
+    const lrqk_layer_t &L = a.L;
+    constexpr int N = Pack<T>::N;
+    const int packs = L.dim_stride / N;
+    const int lpr = packs < 32 ? packs : 32;
+    const int ppl = packs / lpr;
+    const int ng = (kFThreads / 32) * (32 / lpr);
+    const size_t smem = (size_t)kFRows * 4 + (size_t)kFList * 4 + ((size_t)ng * L.dim_stride + L.dim_stride + 2) * 4;
+    const int grid = L.batch * L.n_q_heads * a.parts;
+#define LRQK_F(LP, PP)                                                                            \
+    do {                                                                                          \
+        auto fn = select_attend_kernel<T, LP, PP>;                                                \
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+        launch_kernel(fn, grid, kFThreads, smem, st, true, a);                                    \
+    } while (0)
+    if (ppl == 1) {
+        switch (lpr) {
+            case 1: LRQK_F(1, 1); break;
+            case 2: LRQK_F(2, 1); break;
+            case 4: LRQK_F(4, 1); break;
+            case 8: LRQK_F(8, 1); break;
+            case 16: LRQK_F(16, 1); break;
+            case 32: LRQK_F(32, 1); break;
+            default: return LRQK_EUNSUPPORTED;
+        }
+    } else if (ppl == 2 && lpr == 32) {
+        LRQK_F(32, 2);
+    } else {
+        return LRQK_EUNSUPPORTED;
+    }
+#undef LRQK_F
+    return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+}
+
+int launch_select_attend(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st) {
+    if (L.policy != LRQK_SLOW_HBM) return LRQK_OK;  // mode 5 is HBM-only
+    FArgs a{L, q, out, score_tma_parts(L)};
+    return L.dtype == LRQK_BF16 ? launch_select_attend_t<__nv_bfloat16>(a, st) : launch_select_attend_t<float>(a, st);
+}
+
+}  // namespace lrqk

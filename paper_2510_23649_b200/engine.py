@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import functools
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -29,7 +30,7 @@ from . import _lib
 from .errors import NonFiniteError, SolveFailedError
 
 SHARED_SCRATCH = ("q_hat", "k_hat", "eta", "keys", "hist", "sel_meta", "sure_idx", "cand", "red_scratch",
-                  "attn_scratch", "counters", "miss_idx", "miss_slot", "miss_cnt", "status")
+                  "attn_scratch", "counters", "miss_idx", "miss_slot", "miss_cnt", "status", "fcand", "fcnt")
 
 
 def pow2_at_least(x: int, lo: int = 8) -> int:
@@ -381,16 +382,18 @@ class Engine:
 
     def launches_per_step(self):
         """Kernels one decode step launches: per layer compress, score,
-        select, [gather], attention and the next step's compress_prepare,
-        plus the ctx advance."""
-        per = 5 + (1 if self.shape.policy == "host" else 0)
+        [select_attend], select, [gather], attention and the next step's
+        compress_prepare, plus the ctx advance."""
+        per = 5 + (1 if self.shape.policy == "host" else 1)
         return self.n_layers * per + 1
 
-    def decode_step(self, q=None, k=None, v=None, out=None, stream=None, overlap=True):
+    def decode_step(self, q=None, k=None, v=None, out=None, stream=None, overlap=None):
         """One token for every sequence through all layers.  With overlap,
         each layer's compress_prepare (the q/k-independent half of the next
         step's compression) runs on a side stream concurrently with the rest
         of the step and is joined before the step ends."""
+        if overlap is None:
+            overlap = os.environ.get("LRQK_OVERLAP", "1") != "0"
         q = self.q_buf if q is None else q
         k = self.k_buf if k is None else k
         v = self.v_buf if v is None else v
@@ -409,6 +412,7 @@ class Engine:
             _lib.check(lib.lrqk_decode_compress(lp, q[i].data_ptr(), k[i].data_ptr(), v[i].data_ptr(), 1, sp),
                        "lrqk_decode_compress")
             _lib.check(lib.lrqk_score(lp, sp), "lrqk_score")
+            _lib.check(lib.lrqk_select_attend(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_select_attend")
             _lib.check(lib.lrqk_select(lp, sp), "lrqk_select")
             _lib.check(lib.lrqk_gather_misses(lp, sp), "lrqk_gather_misses")
             if overlap:

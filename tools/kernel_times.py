@@ -48,9 +48,11 @@ q = torch.randn(B, Hq, d, device=dev, generator=g).to(sdt)
 k = torch.randn(B, Hkv, d, device=dev, generator=g).to(sdt)
 v = torch.randn(B, Hkv, d, device=dev, generator=g).to(sdt)
 out = torch.zeros(B, Hq, d, device=dev)
-names = ["compress", "score", "select", "gather", "attention", "prepare", "advance"]
+names = ["compress", "score", "select_attend", "select", "gather", "attention", "prepare", "advance"]
 calls = [lambda: lib.lrqk_decode_compress(L.ptr, q.data_ptr(), k.data_ptr(), v.data_ptr(), 1, sp),
-         lambda: lib.lrqk_score(L.ptr, sp), lambda: lib.lrqk_select(L.ptr, sp),
+         lambda: lib.lrqk_score(L.ptr, sp),
+         lambda: lib.lrqk_select_attend(L.ptr, q.data_ptr(), out.data_ptr(), sp),
+         lambda: lib.lrqk_select(L.ptr, sp),
          lambda: lib.lrqk_gather_misses(L.ptr, sp),
          lambda: lib.lrqk_attention(L.ptr, q.data_ptr(), out.data_ptr(), sp),
          lambda: lib.lrqk_compress_prepare(L.ptr, sp),
@@ -67,6 +69,9 @@ for s in range(a.steps):
     for i, n in enumerate(names):
         times[n].append(evs[i].elapsed_time(evs[i + 1]) * 1e3)
 st = int(L.view("status").item())
+meta = L.buf["sel_meta"].view(torch.int32)[: B * Hq * 48].view(B * Hq, 48).cpu()
+print("select modes", sorted(set(meta[:, 7].tolist())), "hint_ok", int(meta[:, 17].sum()), "fbin", meta[:4, 19].tolist(),
+      "stats", meta[:, 33:40].sum(0).tolist())
 import numpy as np
 lib.lrqk_trace_enable(1)
 ti = names.index(a.trace)
