@@ -333,7 +333,7 @@ def run_ours(args, world, rank, local):
             _lib.check(lib.lrqk_select(layer.ptr, sp), "select")
             _lib.check(lib.lrqk_gather_misses(layer.ptr, sp), "gather")
             _lib.check(lib.lrqk_attention(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "attention")
-            _lib.check(lib.lrqk_compress_prepare(layer.ptr, sp), "prepare")
+        _lib.check(lib.lrqk_compress_prepare_layers(eng._dev_layers.data_ptr(), eng._host_layers, L, sp), "prepare")
         _lib.check(lib.lrqk_advance(eng.ctx.data_ptr(), B, sp), "advance")
     torch.cuda.synchronize()
     eng.raise_status()

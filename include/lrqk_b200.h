@@ -136,6 +136,13 @@ int lrqk_seed_prompt(const lrqk_layer_t *L, int32_t prompt_len, void *stream);
  * ref: decode.py:84-119 (the q/k-independent parts of update_qhat/khat). */
 int lrqk_compress_prepare(const lrqk_layer_t *L, void *stream);
 
+/* lrqk_compress_prepare for n_layers identically shaped layers in one
+ * launch: dev_layers is a device copy of host_layers[0..n_layers).  A
+ * layer's precompute is only consumed by its next decode step, so an engine
+ * runs this once per step after the last layer. */
+int lrqk_compress_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int32_t n_layers,
+                                 void *stream);
+
 /* Per-token compression + B line-search update + append of k_hat/k/v.
  * ref: decode.py:122-184 (decode_compress, update_projections),
  *      cache.py:199-214 (append_token), session.py:95-98.

@@ -78,6 +78,7 @@ SIGNATURES = {
     "lrqk_select": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_gather_misses": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_attention": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
+    "lrqk_compress_prepare_layers": (C.c_int, [_P, C.POINTER(LayerStruct), C.c_int32, _P]),
     "lrqk_select_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_decode_step": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P, _P, C.c_int, _P]),
     "lrqk_advance": (C.c_int, [_P, C.c_int32, _P]),

@@ -11,6 +11,7 @@ int compress_chunks(const lrqk_layer_t &L);
 size_t compress_scratch_floats_per_head(const lrqk_layer_t &L);
 size_t compress_pre_floats_per_head(const lrqk_layer_t &L);
 int launch_prepare(const lrqk_layer_t &L, cudaStream_t st);
+int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int n_layers, cudaStream_t st);
 int launch_score(const lrqk_layer_t &L, const float *ext_scores, cudaStream_t st);
 int launch_select(const lrqk_layer_t &L, cudaStream_t st);
 int launch_gather(const lrqk_layer_t &L, cudaStream_t st);
@@ -167,6 +168,20 @@ int lrqk_compress_prepare(const lrqk_layer_t *L, void *stream) {
     int rc = validate(L);
     if (rc) return rc;
     return check(launch_prepare(*L, (cudaStream_t)stream));
+}
+
+int lrqk_compress_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int32_t n_layers,
+                                 void *stream) {
+    if (!dev_layers || !host_layers || n_layers < 1) return LRQK_EINVAL;
+    for (int i = 0; i < n_layers; ++i) {
+        const int rc = validate(&host_layers[i]);
+        if (rc) return rc;
+        const lrqk_layer_t &a = host_layers[i], &b = host_layers[0];
+        if (a.batch != b.batch || a.n_q_heads != b.n_q_heads || a.dim_stride != b.dim_stride ||
+            a.rank_stride != b.rank_stride || a.s_cap != b.s_cap || a.dtype != b.dtype || a.policy != b.policy)
+            return LRQK_EINVAL;  // one launch covers identically shaped layers
+    }
+    return check(launch_prepare_layers(dev_layers, host_layers, n_layers, (cudaStream_t)stream));
 }
 
 int lrqk_decode_compress(const lrqk_layer_t *L, const void *q, const void *k, const void *v, int update_b,

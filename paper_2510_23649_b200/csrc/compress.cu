@@ -29,6 +29,9 @@
 // when the reference's Cholesky does.  If P or R is not SPD, K2c solves each
 // full system directly with the reference's jitter retry (linalg.py:80-91).
 #include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -66,6 +69,7 @@ struct PreLayoutOrder {  // compress_kernel bulk-copies Pinv|Rinv and ZQ|ZK as p
 };
 // Per-head reduction scratch of K2p: chunk partials [Y (R*d) | G (R*R)] + the
 // prep block's B_Q B_Q^T.
+__host__ __device__ inline int compress_chunks_dev(const lrqk_layer_t &L) { return (L.s_cap + kRedRows - 1) / kRedRows; }
 __host__ __device__ inline size_t red_head_floats(int R, int d, int nchunks) {
     return (size_t)nchunks * (R * d + R * R) + R * R;
 }
@@ -303,7 +307,8 @@ constexpr int kMmaRows = 64;  // rows per sub-chunk
 __host__ __device__ inline int mma_stage_bytes(int R, int d) { return kMmaRows * ((d * 2 + 16) + (R * 2 + 16)); }
 
 __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int nrow, const __nv_bfloat16 *kbase,
-                                   const __nv_bfloat16 *proxy, bool host, float *part, uint8_t *smem) {
+                                   const __nv_bfloat16 *proxy, bool host, float *part, uint8_t *smem,
+                                   int *s_ridx = nullptr, int *s_rproxy = nullptr, int nbuf = 2) {
     const int d = L.dim_stride, R = L.rank_stride;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ldk = d * 2 + 16, lda = R * 2 + 16;  // bytes
@@ -322,8 +327,14 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
 #pragma unroll
             for (int c = 0; c < 4; ++c) { yacc[a][b2][c] = 0.f; gacc[a][c] = 0.f; }
     const int nsub = (nrow + kMmaRows - 1) / kMmaRows;
+    if (s_ridx != nullptr) {  // this slice's row indices, one round trip
+        for (int j = tid; j < nrow; j += blockDim.x) s_ridx[j] = host ? rslot[j] : ridx[j];
+        if (host) for (int j = tid; j < nrow; j += blockDim.x) s_rproxy[j] = ridx[j];
+        __syncthreads();
+        trace(17);
+    }
     auto issue = [&](int sub) {
-        uint8_t *buf = smem + (sub & 1) * stage;
+        uint8_t *buf = smem + (sub % nbuf) * stage;
         uint8_t *kb_s = buf, *ab_s = buf + kMmaRows * ldk;
         const int s0 = sub * kMmaRows;
         const int ns = min(kMmaRows, nrow - s0);
@@ -332,7 +343,7 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
             if (e < kMmaRows * kp) {
                 const int j = e / kp, pk = e - j * kp;
                 if (j < ns) {
-                    const int src = host ? rslot[s0 + j] : ridx[s0 + j];
+                    const int src = s_ridx ? s_ridx[s0 + j] : (host ? rslot[s0 + j] : ridx[s0 + j]);
                     cp_async16(kb_s + j * ldk + pk * 16, kbase + (size_t)src * d + pk * 8);
                 } else {
                     *reinterpret_cast<uint4 *>(kb_s + j * ldk + pk * 16) = make_uint4(0, 0, 0, 0);
@@ -340,18 +351,27 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
             } else {
                 const int e2 = e - kMmaRows * kp;
                 const int j = e2 / ap, pk = e2 - j * ap;
-                if (j < ns) cp_async16(ab_s + j * lda + pk * 16, proxy + proxy_pack_offset(ridx[s0 + j], pk, ap) * 8);
+                if (j < ns) {
+                    const int x = s_ridx ? (host ? s_rproxy[s0 + j] : s_ridx[s0 + j]) : ridx[s0 + j];
+                    cp_async16(ab_s + j * lda + pk * 16, proxy + proxy_pack_offset(x, pk, ap) * 8);
+                }
                 else *reinterpret_cast<uint4 *>(ab_s + j * lda + pk * 16) = make_uint4(0, 0, 0, 0);
             }
         }
         cp_async_commit();
     };
-    if (nsub > 0) issue(0);
+    // nbuf - 1 sub-chunk gathers stay in flight: the gather of sub + nbuf - 1
+    // goes out as soon as sub's data has landed, into the buffer freed by sub - 1
+    for (int sub = 0; sub < min(nbuf - 1, nsub); ++sub) issue(sub);
     for (int sub = 0; sub < nsub; ++sub) {
-        if (sub + 1 < nsub) { issue(sub + 1); cp_async_wait<1>(); }
+        const int ahead = min(nsub - sub - 1, nbuf - 2);  // groups allowed to stay pending
+        if (ahead >= 2) cp_async_wait<2>();
+        else if (ahead == 1) cp_async_wait<1>();
         else cp_async_wait<0>();
         __syncthreads();
-        const uint8_t *buf = smem + (sub & 1) * stage;
+        if (sub + nbuf - 1 < nsub) issue(sub + nbuf - 1);
+        if (sub == 0) trace(18);
+        const uint8_t *buf = smem + (sub % nbuf) * stage;
         const uint8_t *kb_s = buf, *ab_s = buf + kMmaRows * ldk;
         const int q = lane >> 3, i8 = lane & 7;
 #pragma unroll
@@ -392,6 +412,7 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
         }
         __syncthreads();
     }
+    trace(19);
     // accumulator fragments -> partial (Y row-major R x d, then G R x R)
     const int fr = lane >> 2, fc = (lane & 3) * 2;
 #pragma unroll
@@ -434,10 +455,21 @@ __device__ void count_hits_hbm(const lrqk_layer_t &L, int bh, int n, float *scra
     __syncthreads();
     const bool fresh = meta[M_BITS_FRESH] != 0;
     if (!fresh) {
+        // all index loads of a thread in flight together, then the bit loads
+        constexpr int UH = 8;
         int hit = 0;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int x = __ldcg(idx + i);
-            hit += (__ldcg(bits + (x >> 5)) >> (x & 31)) & 1u;
+        for (int i0 = 0; i0 < n; i0 += blockDim.x * UH) {
+            int xs[UH];
+            uint32_t ws[UH];
+#pragma unroll
+            for (int u = 0; u < UH; ++u) {
+                const int i = i0 + u * blockDim.x + threadIdx.x;
+                xs[u] = i < n ? __ldcg(idx + i) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < UH; ++u) ws[u] = xs[u] >= 0 ? __ldcg(bits + (xs[u] >> 5)) : 0u;
+#pragma unroll
+            for (int u = 0; u < UH; ++u) hit += xs[u] >= 0 ? (int)((ws[u] >> (xs[u] & 31)) & 1u) : 0;
         }
         int *s_red = reinterpret_cast<int *>(scratch);
         int hits;
@@ -451,9 +483,16 @@ __device__ void count_hits_hbm(const lrqk_layer_t &L, int bh, int n, float *scra
             L.step_miss[bh] = miss;
             L.step_total[bh] = n;
         }
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int x = __ldcg(idx + i);
-            atomicOr(bits + (x >> 5), 1u << (x & 31));
+        for (int i0 = 0; i0 < n; i0 += blockDim.x * UH) {
+            int xs[UH];
+#pragma unroll
+            for (int u = 0; u < UH; ++u) {
+                const int i = i0 + u * blockDim.x + threadIdx.x;
+                xs[u] = i < n ? __ldcg(idx + i) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < UH; ++u)
+                if (xs[u] >= 0) atomicOr(bits + (xs[u] >> 5), 1u << (xs[u] & 31));
         }
     } else if (threadIdx.x == 0) {
         meta[M_BITS_FRESH] = 0;
@@ -752,6 +791,168 @@ prepare_kernel(const lrqk_layer_t L) {
 }
 
 // ---------------------------------------------------------------------------
+// K2p in two short kernels (bf16 storage):
+//  prepare_reduce_cluster_kernel -- one cluster of kPcCtas CTAs per head;
+//    every CTA gathers its slice of Omega_t and reduces it on the tensor
+//    cores into shared memory (Y_c = A^T K, G_c = A^T A); CTA 0 sums the
+//    slices over distributed shared memory in rank order (deterministic)
+//    and writes Y | G for the head.
+//  prepare_finish_kernel -- one block per head: R = B_K B_K^T,
+//    P = B_Q B_Q^T + l2 G, W = B_Q + l2 Y, P^-1, R^-1 (what compress needs
+//    besides q and k), and the HBM-policy hit/miss count.
+// Both are brief, so the precompute barely competes with the decode chain
+// it overlaps on the side stream.
+// ---------------------------------------------------------------------------
+constexpr int kPcCtas = 8;
+constexpr int kPcBufs = 4;  // gather buffers per CTA (kPcBufs - 1 sub-chunks in flight)
+
+__host__ __device__ inline size_t pc_part_floats(int R, int d) { return (size_t)R * d + (size_t)R * R; }
+
+__device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ __align__(16) float smem[];
+    const int crank = (int)cluster.block_rank();
+    const int bh = blockIdx.y;
+    const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
+    const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
+    const int d = L.dim_stride, R = L.rank_stride;
+    const int n = L.res_cnt[bh];
+    const bool host = L.policy == LRQK_SLOW_HOST;
+    const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+    const __nv_bfloat16 *proxy = reinterpret_cast<const __nv_bfloat16 *>(L.proxy) + (size_t)bh * L.t_max * R;
+    const __nv_bfloat16 *kbase = host ? reinterpret_cast<const __nv_bfloat16 *>(L.slot_k) + (size_t)bh * L.n_slots * d
+                                      : reinterpret_cast<const __nv_bfloat16 *>(L.slow_k) + kv_rows * d;
+    const size_t PF = pc_part_floats(R, d);
+    float *part = smem;  // [R*d | R*R]  Y_c | G_c
+    trace(10);
+    const int chunk = (n + kPcCtas - 1) / kPcCtas;
+    const int row0 = crank * chunk, nrow = max(0, min(chunk, n - row0));
+    int *s_ridx = reinterpret_cast<int *>(reinterpret_cast<uint8_t *>(part + PF) + kPcBufs * mma_stage_bytes(R, d));
+    prepare_reduce_mma(L, bh, row0, nrow, kbase, proxy, host, part, reinterpret_cast<uint8_t *>(part + PF),
+                       s_ridx, s_ridx + chunk, kPcBufs);
+    trace(11);
+    cluster.sync();
+    {   // every CTA sums one slice of Y | G over the cluster, in rank order
+        float *dst = L.red_scratch + (size_t)bh * red_head_floats(R, d, compress_chunks_dev(L));
+        const size_t per = (PF + kPcCtas - 1) / kPcCtas;
+        const size_t e0 = crank * per, e1 = min(PF, e0 + per);
+        const float *src[kPcCtas];
+#pragma unroll
+        for (int c = 0; c < kPcCtas; ++c) src[c] = cluster.map_shared_rank(part, c);
+        for (size_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+            float v[kPcCtas];
+#pragma unroll
+            for (int c = 0; c < kPcCtas; ++c) v[c] = src[c][e];
+            float acc = 0.f;
+#pragma unroll
+            for (int c = 0; c < kPcCtas; ++c) acc += v[c];
+            dst[e] = acc;
+        }
+    }
+    cluster.sync();  // the other CTAs' shared memory stays alive until here
+    trace(12);
+}
+
+__device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L) {
+    extern __shared__ __align__(16) float smem[];
+    __shared__ float s_rc[256];
+    const int bh = blockIdx.x;
+    const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
+    const int tid = threadIdx.x;
+    const int n = L.res_cnt[bh];
+    const bool host = L.policy == LRQK_SLOW_HOST;
+    const PreLayout PL = pre_layout(R, d);
+    float *pre = L.pre + (size_t)bh * PL.total;
+    const float *YG = L.red_scratch + (size_t)bh * red_head_floats(R, d, compress_chunks_dev(L));
+    const int ldB = d + 4, ldM = R + 4;
+    const int RB = R / 4, NP = RB * (RB + 1) / 2;
+    float *sBQ = smem;                   // [R][ldB]
+    float *sBK = sBQ + R * ldB;          // [R][ldB]
+    float *b0 = sBK + R * ldB;           // [R][ldM]  R, then R^-1
+    float *b1 = b0 + R * ldM;            // [R][ldM]  P, then P^-1
+    float *tmp = b1 + R * ldM;           // [2 * NP * 16] gram scratch
+    trace(13);
+    if (!host) count_hits_hbm(L, bh, n, s_rc);
+    stage_rows_f32(sBQ, ldB, L.B_Q + (size_t)bh * R * d, R, d);
+    stage_rows_f32(sBK, ldB, L.B_K + (size_t)bh * R * d, R, d);
+    for (int e = tid; e < R * R; e += blockDim.x) {  // identity padding
+        const int i = e / R, j = e - i * R;
+        if (i >= r || j >= r) { b0[i * ldM + j] = (i == j) ? 1.f : 0.f; b1[i * ldM + j] = (i == j) ? 1.f : 0.f; }
+    }
+    __syncthreads();
+    gram_rows(sBK, r, d, ldB, b0, ldM, tmp);  // R (exactly symmetric)
+    gram_rows(sBQ, r, d, ldB, b1, ldM, tmp);  // B_Q B_Q^T
+    const float l2 = L.lambda_2;
+    const bool have_res = n > 0;
+    const float *Gs = YG + (size_t)R * d;
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int i = e / R, j = e - i * R;
+        const bool in = i < r && j < r;
+        float pv = 0.f;
+        if (in) {
+            pv = b1[i * ldM + j] + (have_res ? l2 * __ldcg(Gs + min(i, j) * R + max(i, j)) : 0.f);
+            b1[i * ldM + j] = pv;
+        }
+        pre[PL.P + e] = pv;
+        pre[PL.R + e] = in ? b0[i * ldM + j] : 0.f;
+    }
+    for (int e4 = tid; e4 < R * d / 4; e4 += blockDim.x) {  // W = B_Q + l2 Y
+        const int p2 = (e4 * 4) / d, i = e4 * 4 - p2 * d;
+        float4 acc = *reinterpret_cast<const float4 *>(sBQ + p2 * ldB + i);
+        if (have_res) {
+            const float4 y = __ldcg(reinterpret_cast<const float4 *>(YG) + e4);
+            acc.x = fmaf(l2, y.x, acc.x); acc.y = fmaf(l2, y.y, acc.y);
+            acc.z = fmaf(l2, y.z, acc.z); acc.w = fmaf(l2, y.w, acc.w);
+        }
+        *reinterpret_cast<float4 *>(pre + PL.W + e4 * 4) = acc;
+    }
+    __syncthreads();
+    trace(14);
+    const bool okR = block_gj(b0, R, ldM, s_rc);
+    const bool okP = block_gj(b1, R, ldM, s_rc);
+    for (int e = tid; e < R * R; e += blockDim.x) {
+        const int i = e / R, j = e - i * R;
+        const bool in = i < r && j < r;
+        if (okR) pre[PL.Rinv + e] = in ? b0[i * ldM + j] : 0.f;
+        if (okP) pre[PL.Pinv + e] = in ? b1[i * ldM + j] : 0.f;
+    }
+    if (tid == 0) {
+        pre[PL.flags + 0] = okP ? 1.f : 0.f;
+        pre[PL.flags + 1] = okR ? 1.f : 0.f;
+    }
+    trace(16);
+}
+
+// one layer (struct by value) or a batch of layers (device array, layer =
+// blockIdx.z): every layer's precompute is only needed by its next step, so
+// the engine runs all layers' compress_prepare together at the end of a step
+__global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
+prepare_reduce_cluster_kernel(const lrqk_layer_t L) { prepare_reduce_body(L); }
+__global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
+prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls) { prepare_reduce_body(Ls[blockIdx.z]); }
+__global__ void __launch_bounds__(kCompressThreads)
+prepare_finish_kernel(const lrqk_layer_t L) { prepare_finish_body(L); }
+__global__ void __launch_bounds__(kCompressThreads)
+prepare_finish_layers_kernel(const lrqk_layer_t *Ls) { prepare_finish_body(Ls[blockIdx.z]); }
+
+static bool pc_enabled() {
+    static const bool on = [] { const char *e = getenv("LRQK_PREPARE_CLUSTER"); return !(e && e[0] == '0'); }();
+    return on;
+}
+
+static size_t prepare_reduce_smem_bytes(const lrqk_layer_t &L) {
+    const int d = L.dim_stride, R = L.rank_stride;
+    const size_t chunk = ((size_t)L.s_cap + kPcCtas - 1) / kPcCtas;
+    return pc_part_floats(R, d) * sizeof(float) + kPcBufs * (size_t)mma_stage_bytes(R, d) + 2 * chunk * sizeof(int);
+}
+static size_t prepare_finish_smem_bytes(const lrqk_layer_t &L) {
+    const size_t d = L.dim_stride, R = L.rank_stride;
+    const size_t ldB = d + 4, ldM = R + 4, RB = R / 4, NP = RB * (RB + 1) / 2;
+    return (2 * R * ldB + 2 * R * ldM + 2 * NP * 16) * sizeof(float);
+}
+
+// ---------------------------------------------------------------------------
 // K2c: compress (one block per head)
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -785,9 +986,8 @@ compress_kernel(const CompressArgs args) {
     float *sBK = sBQ + R * d;            // [R][d]
     float *sPi = sBK + R * d;            // [R][R]  P^-1 (P in the fallback)
     float *sRi = sPi + R * R;            // [R][R]  R^-1 (R in the fallback)
-    float *sZQ = sRi + R * R;            // [R][d]  Z_Q (or W in the fallback)
-    float *sZK = sZQ + R * d;            // [R][d]  Z_K
-    float *b0 = sZK + R * d;             // [R][R]  fallback scratch
+    float *sW = sRi + R * R;             // [R][d]  W = B_Q + l2 A_res^T K_res
+    float *b0 = sW + R * d;              // [R][R]  fallback scratch
     float *sM = b0 + R * R;              // [R][R]  fallback system
     float *vq = sM + R * R;              // [d]
     float *vk = vq + d;                  // [d]
@@ -798,16 +998,16 @@ compress_kernel(const CompressArgs args) {
     float *u = kh + R;                   // [R]
     float *prevc = u + R;                // [2R]
     float *resid = prevc + 2 * R;        // [2][d]
-    static_assert(PreLayoutOrder::kPairs, "pre layout keeps Pinv|Rinv and ZQ|ZK adjacent");
+    static_assert(PreLayoutOrder::kPairs, "pre layout keeps Pinv|Rinv adjacent");
     if (tid == 0) {
         mbar_init(&s_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         const uint32_t mat = (uint32_t)(R * d * 4), sq = (uint32_t)(R * R * 4);
-        mbar_expect_tx(&s_bar, 4 * mat + 2 * sq);
+        mbar_expect_tx(&s_bar, 3 * mat + 2 * sq);
         bulk_g2s(sBQ, L.B_Q + (size_t)bh * R * d, mat, &s_bar);
         bulk_g2s(sBK, L.B_K + (size_t)bh * R * d, mat, &s_bar);
         bulk_g2s(sPi, pre + PL.Pinv, 2 * sq, &s_bar);
-        bulk_g2s(sZQ, pre + PL.ZQ, 2 * mat, &s_bar);
+        bulk_g2s(sW, pre + PL.W, mat, &s_bar);
         s_bad = 0;
     }
     // B_Q/B_K and pre were written by the previous step (older than this
@@ -830,8 +1030,7 @@ compress_kernel(const CompressArgs args) {
         if (!isfinite(vq[i]) || !isfinite(vk[i]) || !isfinite(to_float<T>(vrow[i]))) s_bad = 1;
     }
     mbar_wait(&s_bar, 0);
-    if (!fast) {  // rare: the direct solves need W, P, R instead of Z_Q, P^-1, R^-1
-        for (int e = tid; e < R * d; e += blockDim.x) sZQ[e] = __ldcg(pre + PL.W + e);
+    if (!fast) {  // rare: the direct solves need P, R instead of P^-1, R^-1
         for (int e = tid; e < R * R; e += blockDim.x) {
             sPi[e] = __ldcg(pre + PL.P + e);
             sRi[e] = __ldcg(pre + PL.R + e);
@@ -843,7 +1042,7 @@ compress_kernel(const CompressArgs args) {
         return;
     }
     trace(1);
-    // ---- y_q = Z_Q q (or m = W q), y_k = Z_K k (or k B_K^T), qk -------------
+    // ---- m_q = q W^T, m_k = k B_K^T, qk; then y_q = m_q P^-1, y_k = m_k R^-1 ---
     // one 8-lane group per output row; 32 groups per block
     {
         const int grp = tid >> 3, gl = tid & 7;
@@ -853,7 +1052,7 @@ compress_kernel(const CompressArgs args) {
             const bool valid = o < 2 * r + 1;
             float acc = 0.f;
             if (valid) {
-                const float *x = o < r ? sZQ + o * ldB : (o < 2 * r ? (fast ? sZK : sBK) + (o - r) * ldB : vq);
+                const float *x = o < r ? sW + o * ldB : (o < 2 * r ? sBK + (o - r) * ldB : vq);
                 const float *y = o < r ? vq : vk;
                 for (int i = gl * 4; i < d; i += 32) {
                     const float4 xv = *reinterpret_cast<const float4 *>(x + i);
@@ -872,6 +1071,16 @@ compress_kernel(const CompressArgs args) {
         }
     }
     __syncthreads();
+    if (fast) {  // y_q = m_q P^-1 (warp 0), y_k = m_k R^-1 = k_hat0 (warp 1), decode.py:79-108
+        if (warp < 2) {
+            const float *mv = warp == 0 ? yq : yk;
+            const float *S = warp == 0 ? sPi : sRi;
+            float *dstv = warp == 0 ? u : prevc;
+            warp_vecmat(mv, S, r, ldM, dstv);
+            for (int i = lane; i < r; i += 32) (warp == 0 ? yq : yk)[i] = dstv[i];
+        }
+        __syncthreads();
+    }
     trace(2);
     const float qk = s_scalar[0];
     const float l1 = L.lambda_1;
@@ -1104,10 +1313,38 @@ static size_t prepare_smem_bytes(const lrqk_layer_t &L) {
 }
 static size_t compress_smem_bytes(const lrqk_layer_t &L) {
     const size_t d = L.dim_stride, R = L.rank_stride;
-    return (4 * R * d + 4 * R * R + 4 * d + 7 * R) * sizeof(float);
+    return (3 * R * d + 4 * R * R + 4 * d + 7 * R) * sizeof(float);
+}
+
+int launch_prepare(const lrqk_layer_t &L, cudaStream_t st);
+int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int n_layers,
+                          cudaStream_t st) {
+    const lrqk_layer_t &L = host_layers[0];
+    if (L.dtype == LRQK_BF16 && L.rank_stride >= 16 && L.dim_stride >= 64 && pc_enabled()) {
+        const size_t s1 = prepare_reduce_smem_bytes(L), s2 = prepare_finish_smem_bytes(L);
+        cudaFuncSetAttribute(prepare_reduce_cluster_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+        cudaFuncSetAttribute(prepare_finish_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+        prepare_reduce_cluster_layers_kernel<<<dim3(kPcCtas, L.batch * L.n_q_heads, n_layers), kCompressThreads, s1,
+                                               st>>>(dev_layers);
+        prepare_finish_layers_kernel<<<dim3(L.batch * L.n_q_heads, 1, n_layers), kCompressThreads, s2, st>>>(dev_layers);
+        return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+    }
+    for (int i = 0; i < n_layers; ++i) {
+        const int rc = launch_prepare(host_layers[i], st);
+        if (rc) return rc;
+    }
+    return LRQK_OK;
 }
 
 int launch_prepare(const lrqk_layer_t &L, cudaStream_t st) {
+    if (L.dtype == LRQK_BF16 && L.rank_stride >= 16 && L.dim_stride >= 64 && pc_enabled()) {
+        const size_t s1 = prepare_reduce_smem_bytes(L), s2 = prepare_finish_smem_bytes(L);
+        cudaFuncSetAttribute(prepare_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+        cudaFuncSetAttribute(prepare_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+        prepare_reduce_cluster_kernel<<<dim3(kPcCtas, L.batch * L.n_q_heads), kCompressThreads, s1, st>>>(L);
+        prepare_finish_kernel<<<L.batch * L.n_q_heads, kCompressThreads, s2, st>>>(L);
+        return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
+    }
     dim3 grid(compress_chunks(L) + 1, L.batch * L.n_q_heads);
     const size_t smem = prepare_smem_bytes(L);
     if (L.dtype == LRQK_BF16) {

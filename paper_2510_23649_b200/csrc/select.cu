@@ -292,6 +292,7 @@ score_tma_kernel(const ScoreArgs a) {
     const uint8_t *src = reinterpret_cast<const uint8_t *>(reinterpret_cast<const T *>(L.proxy) +
                                                            (size_t)bh * L.t_max * R);
     uint32_t *keys = L.keys + (size_t)bh * L.t_max;
+    const uint64_t pol_stream = l2_policy_evict_first(), pol_keys = l2_policy_evict_last();
     if (warp == kCW) {
         // ---------------- producer ----------------
         if (lane == 0) {
@@ -301,8 +302,10 @@ score_tma_kernel(const ScoreArgs a) {
                 const int nt = min(kCW, tile1 - tile0 - it * kCW);
                 const uint32_t bytes = (uint32_t)nt * SS::kTileBytes;
                 mbar_expect_tx(full + s2, bytes);
-                bulk_g2s(tsm + s2 * SS::kStageBytes, src + (size_t)(tile0 + it * kCW) * SS::kTileBytes, bytes,
-                         full + s2);
+                // the proxy store is streamed once per step: evict it first, so the
+                // keys (read again by the selection) stay in L2
+                bulk_g2s_hint(tsm + s2 * SS::kStageBytes, src + (size_t)(tile0 + it * kCW) * SS::kTileBytes, bytes,
+                              full + s2, pol_stream);
             }
         }
     } else {
@@ -331,7 +334,7 @@ score_tma_kernel(const ScoreArgs a) {
                 }
                 const int row = tile * 32 + lane;
                 const uint32_t key = score_key(s0 + s1);
-                if (row < n) keys[row] = key;
+                if (row < n) st_hint_u32(keys + row, key, pol_keys);
                 if (row < lite_start) {
                     if ((tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
                     if (win && key >= klo) {

@@ -184,7 +184,6 @@ select_attend_kernel(const FArgs a) {
     float *s_acc = reinterpret_cast<float *>(s_list + kFList);     // [NG][d]
     float *s_part = s_acc + NG * L.dim_stride;                     // [d + 2] last block's own partial
     __shared__ float s_m[kFThreads / 32], s_l[kFThreads / 32];
-    __shared__ float s_pm[64], s_pw[64];
     __shared__ int s_scan[32];
     __shared__ int s_flag;
     const int P = a.parts;
@@ -293,16 +292,56 @@ select_attend_kernel(const FArgs a) {
     if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_FUSED, P, &s_flag)) return;
     trace(53);
 
-    // ---- last block: rank bin D, Omega_l, merge ------------------------------
+    // ---- last block: rank bin D, merge -------------------------------------
     const int need2 = k_eff - nabove;
     const int n_crit = __ldcg(meta + M_CAND);
-    int M = 1;
-    while (M < n_crit) M <<= 1;
-    const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && M <= kCritCap;
-    uint64_t *crit = reinterpret_cast<uint64_t *>(s_rows);
-    int nwin = 0;
+    const int lane_ = tid & 31, warp_ = tid >> 5;
+    const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && n_crit <= kCritCap;
+    const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, P) * (size_t)(d + 2);
+    // the parts' (max, sum), fetched while bin D is ranked
+    float *s_pml = s_part + d + 2;  // [2 * P]
+    for (int p = tid; p < P; p += blockDim.x) {
+        s_pml[2 * p] = __ldcg(parts + (size_t)p * (d + 2));
+        s_pml[2 * p + 1] = __ldcg(parts + (size_t)p * (d + 2) + 1);
+    }
     uint32_t hint = klo + ((uint32_t)(D + 1) << kWinShift);
-    if (ok) {
+    int nwin = 0;
+    if (!ok) {
+        if (tid == 0) set_status(L.status, LRQK_ST_INDEX_RANGE);  // inconsistent selection state (never expected)
+    } else if (n_crit <= 32) {
+        // one warp: bitonic sort of the composites (descending), then of the
+        // winners' indices (ascending), through shuffles
+        if (warp_ == 0) {
+            uint64_t v = lane_ < n_crit ? __ldcg(cand + lane_) : 0ull;
+#pragma unroll
+            for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+                for (int j = kk >> 1; j > 0; j >>= 1) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, j);
+                    const bool hi = ((lane_ & kk) == 0) == ((lane_ & j) == 0);  // keep the larger one
+                    v = hi ? (v > o ? v : o) : (v < o ? v : o);
+                }
+            const uint64_t last = __shfl_sync(0xffffffffu, v, max(need2 - 1, 0));
+            if (need2 > 0) hint = (uint32_t)(last >> kIdxBits);
+            uint32_t ix = lane_ < need2 ? (uint32_t)comp_index(v) : 0xFFFFFFFFu;
+#pragma unroll
+            for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+                for (int j = kk >> 1; j > 0; j >>= 1) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, ix, j);
+                    const bool lo = ((lane_ & kk) == 0) == ((lane_ & j) == 0);  // keep the smaller one
+                    ix = lo ? min(ix, o) : max(ix, o);
+                }
+            if (lane_ < need2) {
+                dst[nabove + lane_] = (int)ix;
+                s_list[lane_] = (int)ix;
+            }
+        }
+        nwin = need2;
+    } else {
+        int M = 1;
+        while (M < n_crit) M <<= 1;
+        uint64_t *crit = reinterpret_cast<uint64_t *>(s_rows);
         for (int i = tid; i < M; i += blockDim.x) crit[i] = i < n_crit ? __ldcg(cand + i) : 0ull;
         __syncthreads();
         block_bitonic(crit, M, true);  // descending composites: ties -> lower index first
@@ -312,63 +351,49 @@ select_attend_kernel(const FArgs a) {
         for (int i = tid; i < M2; i += blockDim.x) crit[i] = i < need2 ? (uint64_t)comp_index(crit[i]) : ~0ull;
         __syncthreads();
         block_bitonic(crit, M2, false);  // winners by ascending index
+        for (int i = tid; i < need2; i += blockDim.x) {
+            dst[nabove + i] = (int)crit[i];
+            s_list[i] = (int)crit[i];
+        }
         nwin = need2;
-        trace(55);
-    } else if (tid == 0) {
-        set_status(L.status, LRQK_ST_INDEX_RANGE);  // inconsistent selection state (never expected)
-    }
-    for (int i = tid; i < nwin; i += blockDim.x) {
-        const int x = (int)crit[i];
-        dst[nabove + i] = x;
-        s_list[i] = x;
     }
     __syncthreads();
+    trace(55);
 #pragma unroll
     for (int pp = 0; pp < PPL; ++pp)
 #pragma unroll
         for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
     m = -INFINITY;
     l = 0.f;
-    trace(56);
     attend_list<T, LPR, PPL>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);
-    trace(57);
     block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, s_part);
     trace(58);
-    // merge the P part partials with this block's (the lite rows are never
-    // empty, so the running max is finite)
-    const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, P) * (size_t)(d + 2);
+    // merge the P part partials with this block's (the lite rows, in the last
+    // part, are never empty, so the maximum is finite)
     float MM = s_part[0];
-    for (int p0 = 0; p0 < P; p0 += 64) {
-        const int np = min(64, P - p0);
-        for (int p = tid; p < np; p += blockDim.x) s_pm[p] = __ldcg(parts + (size_t)(p0 + p) * (d + 2));
-        __syncthreads();
-        for (int p = 0; p < np; ++p) MM = fmaxf(MM, s_pm[p]);
-        __syncthreads();
-    }
-    trace(59);
+    for (int p = 0; p < P; ++p) MM = fmaxf(MM, s_pml[2 * p]);
     const float w0 = s_part[0] == -INFINITY ? 0.f : exp2f(s_part[0] - MM);
     float den = s_part[1] * w0;
-    for (int i = tid; i < d; i += blockDim.x) s_part[2 + i] *= w0;
-    __syncthreads();
-    for (int p0 = 0; p0 < P; p0 += 64) {
-        const int np = min(64, P - p0);
-        for (int p = tid; p < np; p += blockDim.x) {
-            const float pm = __ldcg(parts + (size_t)(p0 + p) * (d + 2));
-            s_pw[p] = pm == -INFINITY ? 0.f : exp2f(pm - MM);
-            s_pm[p] = __ldcg(parts + (size_t)(p0 + p) * (d + 2) + 1);
+    for (int p = 0; p < P; ++p)
+        if (s_pml[2 * p] != -INFINITY) den = fmaf(s_pml[2 * p + 1], exp2f(s_pml[2 * p] - MM), den);
+    const float inv = 1.f / den;
+    for (int i = tid; i < d; i += blockDim.x) {
+        float o0 = s_part[2 + i] * w0, o1 = 0.f;
+        int p = 0;
+        for (; p + 1 < P; p += 2) {
+            const float a0 = __ldcg(parts + (size_t)p * (d + 2) + 2 + i);
+            const float a1 = __ldcg(parts + (size_t)(p + 1) * (d + 2) + 2 + i);
+            const float m0 = s_pml[2 * p], m1 = s_pml[2 * p + 2];
+            o0 = fmaf(a0, m0 == -INFINITY ? 0.f : exp2f(m0 - MM), o0);
+            o1 = fmaf(a1, m1 == -INFINITY ? 0.f : exp2f(m1 - MM), o1);
         }
-        __syncthreads();
-        for (int p = 0; p < np; ++p) den = fmaf(s_pm[p], s_pw[p], den);
-        for (int i = tid; i < d; i += blockDim.x) {
-            float o0 = s_part[2 + i];
-            for (int p = 0; p < np; ++p) o0 = fmaf(__ldcg(parts + (size_t)(p0 + p) * (d + 2) + 2 + i), s_pw[p], o0);
-            s_part[2 + i] = o0;
+        if (p < P) {
+            const float m0 = s_pml[2 * p];
+            o0 = fmaf(__ldcg(parts + (size_t)p * (d + 2) + 2 + i), m0 == -INFINITY ? 0.f : exp2f(m0 - MM), o0);
         }
-        __syncthreads();
+        a.out[(size_t)bh * d + i] = (o0 + o1) * inv;
     }
     trace(60);
-    const float inv = 1.f / den;
-    for (int i = tid; i < d; i += blockDim.x) a.out[(size_t)bh * d + i] = s_part[2 + i] * inv;
     if (tid == 0) {
         L.res_cnt[bh] = k_eff + (t + 1 - lite_start);
         meta[M_CAND] = 0;
@@ -389,7 +414,8 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
     const int lpr = packs < 32 ? packs : 32;
     const int ppl = packs / lpr;
     const int ng = (kFThreads / 32) * (32 / lpr);
-    const size_t smem = (size_t)kFRows * 4 + (size_t)kFList * 4 + ((size_t)ng * L.dim_stride + L.dim_stride + 2) * 4;
+    const size_t smem = (size_t)kFRows * 4 + (size_t)kFList * 4 +
+                        ((size_t)ng * L.dim_stride + L.dim_stride + 2 + 2 * (size_t)a.parts) * 4;
     const int grid = L.batch * L.n_q_heads * a.parts;
 #define LRQK_F(LP, PP)                                                                            \
     do {                                                                                          \

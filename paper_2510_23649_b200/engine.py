@@ -29,8 +29,12 @@ import torch
 from . import _lib
 from .errors import NonFiniteError, SolveFailedError
 
-SHARED_SCRATCH = ("q_hat", "k_hat", "eta", "keys", "hist", "sel_meta", "sure_idx", "cand", "red_scratch",
-                  "attn_scratch", "counters", "miss_idx", "miss_slot", "miss_cnt", "status", "fcand", "fcnt")
+# per-step scratch that layers decoded one after another may share; the
+# selection meta (it carries the threshold hint to the next step) and the
+# compress_prepare reduction (all layers' precompute runs in one launch) are
+# per layer
+SHARED_SCRATCH = ("q_hat", "k_hat", "eta", "keys", "hist", "sure_idx", "cand", "attn_scratch", "counters",
+                  "miss_idx", "miss_slot", "miss_cnt", "status", "fcand", "fcnt")
 
 
 def pow2_at_least(x: int, lo: int = 8) -> int:
@@ -375,6 +379,11 @@ class Engine:
                                    device=self.device)
         self.graph = None
         self.kernels_per_step = None
+        # the layers' descriptors, on the host and on the device, for the
+        # batched compress_prepare launch
+        self._host_layers = (_lib.LayerStruct * n_layers)(*[l.struct for l in self.layers])
+        raw = bytes(self._host_layers)
+        self._dev_layers = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(self.device)
 
     @property
     def ctx(self):
@@ -382,18 +391,18 @@ class Engine:
 
     def launches_per_step(self):
         """Kernels one decode step launches: per layer compress, score,
-        [select_attend], select, [gather], attention and the next step's
-        compress_prepare, plus the ctx advance."""
-        per = 5 + (1 if self.shape.policy == "host" else 1)
-        return self.n_layers * per + 1
+        [select_attend], select, [gather], attention; then the batched
+        compress_prepare (two kernels for bf16) and the ctx advance."""
+        per = 5
+        prep = 2 if self.shape.dtype == "bf16" else self.n_layers
+        return self.n_layers * per + prep + 1
 
-    def decode_step(self, q=None, k=None, v=None, out=None, stream=None, overlap=None):
-        """One token for every sequence through all layers.  With overlap,
-        each layer's compress_prepare (the q/k-independent half of the next
-        step's compression) runs on a side stream concurrently with the rest
-        of the step and is joined before the step ends."""
-        if overlap is None:
-            overlap = os.environ.get("LRQK_OVERLAP", "1") != "0"
+    def decode_step(self, q=None, k=None, v=None, out=None, stream=None):
+        """One token for every sequence through all layers (session.py:88-117
+        per (sequence, head, layer)), then every layer's compress_prepare --
+        the q/k-independent half of the next step's compression -- in one
+        batched launch: a layer's precompute is only read by its next step,
+        so batching it keeps it off the per-layer critical path."""
         q = self.q_buf if q is None else q
         k = self.k_buf if k is None else k
         v = self.v_buf if v is None else v
@@ -401,12 +410,6 @@ class Engine:
         lib = _lib.lib()
         main = stream if stream is not None else torch.cuda.current_stream()
         sp = _lib.stream_ptr(main)
-        if overlap:
-            if getattr(self, "_side", None) is None:
-                self._side = torch.cuda.Stream(device=self.device)
-            side = self._side
-            side.wait_stream(main)
-            ssp = _lib.stream_ptr(side)
         for i, layer in enumerate(self.layers):
             lp = layer.ptr
             _lib.check(lib.lrqk_decode_compress(lp, q[i].data_ptr(), k[i].data_ptr(), v[i].data_ptr(), 1, sp),
@@ -415,17 +418,10 @@ class Engine:
             _lib.check(lib.lrqk_select_attend(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_select_attend")
             _lib.check(lib.lrqk_select(lp, sp), "lrqk_select")
             _lib.check(lib.lrqk_gather_misses(lp, sp), "lrqk_gather_misses")
-            if overlap:
-                ev = torch.cuda.Event()
-                ev.record(main)
-                side.wait_event(ev)
-                _lib.check(lib.lrqk_compress_prepare(lp, ssp), "lrqk_compress_prepare")
             _lib.check(lib.lrqk_attention(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_attention")
-            if not overlap:
-                _lib.check(lib.lrqk_compress_prepare(lp, sp), "lrqk_compress_prepare")
+        _lib.check(lib.lrqk_compress_prepare_layers(self._dev_layers.data_ptr(), self._host_layers, self.n_layers, sp),
+                   "lrqk_compress_prepare_layers")
         _lib.check(lib.lrqk_advance(self.ctx.data_ptr(), self.shape.batch, sp), "lrqk_advance")
-        if overlap:
-            main.wait_stream(side)
         return out
 
     def capture(self, warmup_steps=0):

@@ -290,3 +290,47 @@ def test_selection_exact_with_prefill_factors(ctx):
         assert idx.min() >= 0 and idx.max() <= t
         layer.raise_status()
         _select_exact_check(layer, t, kb, lb)
+
+
+def test_engine_matches_per_layer_steps():
+    """The multi-layer Engine (shared per-step scratch, all layers'
+    compress_prepare in one batched launch, CUDA graph replay) must give
+    exactly the results of stepping each layer on its own through
+    lrqk_decode_step."""
+    from paper_2510_23649_b200.engine import Engine, LayerShape, LayerState
+
+    torch.manual_seed(0)
+    nL, B, Hq, Hkv, d, r, kb, lb, l = 3, 1, 4, 2, 128, 32, 64, 16, 3000
+    sh = LayerShape(batch=B, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, rank=r, k_budget=kb, lite_budget=lb,
+                    t_max=l + 32, dtype="bf16")
+    eng = Engine(nL, sh, device="cuda")
+    ref = [LayerState(sh) for _ in range(nL)]
+    for i in range(nL):
+        AK = torch.randn(B, Hq, l, r, device="cuda")
+        BQ = torch.randn(B, Hq, r, d, device="cuda") / d ** 0.5
+        BK = torch.randn(B, Hq, r, d, device="cuda") / d ** 0.5
+        K = torch.randn(B, Hkv, l, d, device="cuda").bfloat16()
+        V = torch.randn(B, Hkv, l, d, device="cuda").bfloat16()
+        eng.layers[i].load_prompt(AK, BQ, BK, K, V)
+        ref[i].load_prompt(AK, BQ, BK, K, V)
+    outs = torch.zeros(nL, B, Hq, d, device="cuda")
+    for step in range(6):
+        q = torch.randn(nL, B, Hq, d, device="cuda").bfloat16()
+        k = torch.randn(nL, B, Hkv, d, device="cuda").bfloat16()
+        v = torch.randn(nL, B, Hkv, d, device="cuda").bfloat16()
+        eng.q_buf[..., :d].copy_(q)
+        eng.k_buf[..., :d].copy_(k)
+        eng.v_buf[..., :d].copy_(v)
+        if step < 3:
+            eng.decode_step()
+        else:
+            eng.replay()
+        for i in range(nL):
+            ref[i].step(q[i].contiguous(), k[i].contiguous(), v[i].contiguous(), outs[i])
+        torch.cuda.synchronize()
+        eng.raise_status()
+        for i in range(nL):
+            ref[i].raise_status()
+            assert torch.equal(eng.out_buf[i][..., :d], outs[i]), f"layer {i} step {step}"
+            for name in ("res_cnt", "step_miss", "c_miss", "B_Q", "B_K"):
+                assert torch.equal(eng.layers[i].view(name), ref[i].view(name)), (name, i, step)
