@@ -9,7 +9,7 @@ LIB := $(PKG)/liblrqk_b200.so
 
 all: $(LIB)
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/select_common.cuh include/lrqk_b200.h
+build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/select_common.cuh $(PKG)/csrc/mma_common.cuh include/lrqk_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblrqk_b200.so")
+LIB_PATH = os.environ.get("LRQK_LIB_PATH") or os.path.join(_HERE, "liblrqk_b200.so")
 
 F32, BF16 = 0, 1
 SLOW_HBM, SLOW_HOST = 0, 1

@@ -43,6 +43,7 @@ enum Meta : int {
     M_PCRIT_LIST = 25, // mode 5: ... their indices (kPrevCrit)
     M_STAT = 33,       // persistent: head-steps finalized per mode (33 + mode, modes 0..5; 39: exact fallbacks)
     M_BITS_FRESH = 40, // res_bits already holds res_idx (set by seed; prepare then skips the hit count)
+    M_YG = 41,         // Y|G partial slots written by select_attend this step (0: cluster reduce does it)
 };
 constexpr int kPrevCrit = 8;
 
@@ -51,6 +52,13 @@ LRQK_DEV int attn_slots_dev(const lrqk_layer_t &L, int parts) {
     const int splits = (L.s_cap + kAttnRows - 1) / kAttnRows;
     return splits > parts ? splits : parts;
 }
+
+// compress_prepare reductions, per head: `yg_slots` partials of
+// [Y = A_res^T K_res (R x d) | G = A_res^T A_res (R x R)], summed by the
+// finish kernel.  select_attend writes one per score part plus one for the
+// threshold-bin winners (meta M_YG = slots used); otherwise the cluster
+// reduce writes slot 0.  yg_slots is computed on the host (capi.cu).
+__host__ __device__ inline size_t yg_part_floats(int R, int d) { return (size_t)R * d + (size_t)R * R; }
 
 enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3, C_PREPARE = 4, C_FUSED = 5 };
 
@@ -307,7 +315,11 @@ constexpr int kTraceCap = 1 << 16;
 extern __device__ int g_lrqk_trace_on;
 extern __device__ unsigned long long g_lrqk_trace[kTraceCap][2];
 LRQK_DEV void trace(int tag) {
-    if (g_lrqk_trace_on && threadIdx.x == 0) {
+#ifdef LRQK_NO_TRACE
+    (void)tag;
+    return;
+#endif
+    if (threadIdx.x == 0 && g_lrqk_trace_on) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         const unsigned blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);

@@ -34,6 +34,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "mma_common.cuh"
 
 namespace lrqk {
 
@@ -279,32 +280,6 @@ __device__ void gram_rows(const float *X, int r, int d, int ldx, float *out, int
 // (16-byte LDGSTS) into two buffers, so the next sub-chunk's gather overlaps
 // the current sub-chunk's MMAs; fragments come from ldmatrix.trans.
 // ---------------------------------------------------------------------------
-LRQK_DEV void cp_async16(void *dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-                 "l"(src) : "memory");
-}
-LRQK_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> LRQK_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-LRQK_DEV void ldsm_x4_trans(uint32_t (&r)[4], const void *p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
-}
-LRQK_DEV void ldsm_x2_trans(uint32_t (&r)[2], const void *p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
-                 : "=r"(r[0]), "=r"(r[1]) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
-}
-LRQK_DEV void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
-    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-                 "{%0,%1,%2,%3};"
-                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-
-constexpr int kMmaRows = 64;  // rows per sub-chunk
-
-// smem bytes of the two gather buffers (row strides padded by 16 bytes)
-__host__ __device__ inline int mma_stage_bytes(int R, int d) { return kMmaRows * ((d * 2 + 16) + (R * 2 + 16)); }
 
 __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int nrow, const __nv_bfloat16 *kbase,
                                    const __nv_bfloat16 *proxy, bool host, float *part, uint8_t *smem,
@@ -808,7 +783,7 @@ constexpr int kPcBufs = 4;  // gather buffers per CTA (kPcBufs - 1 sub-chunks in
 
 __host__ __device__ inline size_t pc_part_floats(int R, int d) { return (size_t)R * d + (size_t)R * R; }
 
-__device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L) {
+__device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L, int yg_slots) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) float smem[];
@@ -818,6 +793,7 @@ __device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L) {
     const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
     const int d = L.dim_stride, R = L.rank_stride;
     const int n = L.res_cnt[bh];
+    if (L.sel_meta[(size_t)bh * kMetaInts + M_YG] > 0) return;  // select_attend reduced this head already
     const bool host = L.policy == LRQK_SLOW_HOST;
     const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
     const __nv_bfloat16 *proxy = reinterpret_cast<const __nv_bfloat16 *>(L.proxy) + (size_t)bh * L.t_max * R;
@@ -834,7 +810,7 @@ __device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L) {
     trace(11);
     cluster.sync();
     {   // every CTA sums one slice of Y | G over the cluster, in rank order
-        float *dst = L.red_scratch + (size_t)bh * red_head_floats(R, d, compress_chunks_dev(L));
+        float *dst = L.red_scratch + (size_t)bh * yg_slots * PF;
         const size_t per = (PF + kPcCtas - 1) / kPcCtas;
         const size_t e0 = crank * per, e1 = min(PF, e0 + per);
         const float *src[kPcCtas];
@@ -854,7 +830,7 @@ __device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L) {
     trace(12);
 }
 
-__device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L) {
+__device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int yg_slots) {
     extern __shared__ __align__(16) float smem[];
     __shared__ float s_rc[256];
     const int bh = blockIdx.x;
@@ -864,7 +840,21 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L) {
     const bool host = L.policy == LRQK_SLOW_HOST;
     const PreLayout PL = pre_layout(R, d);
     float *pre = L.pre + (size_t)bh * PL.total;
-    const float *YG = L.red_scratch + (size_t)bh * red_head_floats(R, d, compress_chunks_dev(L));
+    // Y | G: the sum of the partial slots select_attend wrote (M_YG), or the
+    // cluster reduce's slot 0
+    const size_t PF = yg_part_floats(R, d);
+    float *YG = L.red_scratch + (size_t)bh * yg_slots * PF;
+    int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+    const int nyg = meta[M_YG];
+    if (nyg > 1) {
+        for (size_t e = tid; e < PF; e += blockDim.x) {
+            float acc = 0.f;
+            for (int c2 = 0; c2 < nyg; ++c2) acc += __ldcg(YG + (size_t)c2 * PF + e);
+            YG[e] = acc;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) meta[M_YG] = 0;
     const int ldB = d + 4, ldM = R + 4;
     const int RB = R / 4, NP = RB * (RB + 1) / 2;
     float *sBQ = smem;                   // [R][ldB]
@@ -928,13 +918,13 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L) {
 // blockIdx.z): every layer's precompute is only needed by its next step, so
 // the engine runs all layers' compress_prepare together at the end of a step
 __global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
-prepare_reduce_cluster_kernel(const lrqk_layer_t L) { prepare_reduce_body(L); }
+prepare_reduce_cluster_kernel(const lrqk_layer_t L, int yg_slots) { prepare_reduce_body(L, yg_slots); }
 __global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
-prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls) { prepare_reduce_body(Ls[blockIdx.z]); }
+prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) { prepare_reduce_body(Ls[blockIdx.z], yg_slots); }
 __global__ void __launch_bounds__(kCompressThreads)
-prepare_finish_kernel(const lrqk_layer_t L) { prepare_finish_body(L); }
+prepare_finish_kernel(const lrqk_layer_t L, int yg_slots) { prepare_finish_body(L, yg_slots); }
 __global__ void __launch_bounds__(kCompressThreads)
-prepare_finish_layers_kernel(const lrqk_layer_t *Ls) { prepare_finish_body(Ls[blockIdx.z]); }
+prepare_finish_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) { prepare_finish_body(Ls[blockIdx.z], yg_slots); }
 
 static bool pc_enabled() {
     static const bool on = [] { const char *e = getenv("LRQK_PREPARE_CLUSTER"); return !(e && e[0] == '0'); }();
@@ -1220,25 +1210,21 @@ compress_kernel(const CompressArgs args) {
         resid[w] = a0 + a1 - (side ? vk[i] : vq[i]);
     }
     __syncthreads();
+    trace(5);
     if (warp < 2) {
         const int side = warp;
         const float *xh = side ? kh : qh;
         const float nx = warp_dot(xh, xh, r);
-        double num = 0.0, den = 0.0;
-        for (int i = lane; i < d; i += 32) {
-            const double rr = (double)resid[side * d + i];
-            const double s = (double)nx * rr;
-            num += rr * s;
-            den += s * s;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            num += __shfl_xor_sync(0xffffffffu, num, o);
-            den += __shfl_xor_sync(0xffffffffu, den, o);
-        }
-        if (lane == 0) s_scalar[2 + side] = (den <= 1e-14 * (1.0 + fabs(num))) ? 0.f : (float)(num / den);
+        // s = x_hat grad = |x_hat|^2 resid, so num = |x|^2 |resid|^2 and
+        // den = |x|^4 |resid|^2 (decode.py:150-166, with its underflow floor)
+        float ss = 0.f;
+        for (int i = lane; i < d; i += 32) ss = fmaf(resid[side * d + i], resid[side * d + i], ss);
+        ss = warp_sum(ss);
+        const float num = nx * ss, den = nx * num;
+        if (lane == 0) s_scalar[2 + side] = (den <= 1e-14f * (1.f + fabsf(num))) ? 0.f : num / den;
     }
     __syncthreads();
+    trace(6);
     if (args.update_b) {
         const int n4 = r * d / 4;
         for (int w = tid; w < 2 * n4; w += blockDim.x) {
@@ -1292,8 +1278,12 @@ compress_kernel(const CompressArgs args) {
 
 int compress_chunks(const lrqk_layer_t &L) { return (L.s_cap + kRedRows - 1) / kRedRows; }
 
+int score_tma_parts(const lrqk_layer_t &L);
+// Y|G partial slots per head: the legacy reduce's chunks, or one per score
+// part plus one (select_attend)
+int yg_slots(const lrqk_layer_t &L) { return std::max(compress_chunks(L) + 1, score_tma_parts(L) + 1); }
 size_t compress_scratch_floats_per_head(const lrqk_layer_t &L) {
-    return red_head_floats(L.rank_stride, L.dim_stride, compress_chunks(L));
+    return (size_t)yg_slots(L) * yg_part_floats(L.rank_stride, L.dim_stride);
 }
 size_t compress_pre_floats_per_head(const lrqk_layer_t &L) {
     return pre_layout(L.rank_stride, L.dim_stride).total;
@@ -1317,6 +1307,7 @@ static size_t compress_smem_bytes(const lrqk_layer_t &L) {
 }
 
 int launch_prepare(const lrqk_layer_t &L, cudaStream_t st);
+int yg_slots(const lrqk_layer_t &L);
 int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int n_layers,
                           cudaStream_t st) {
     const lrqk_layer_t &L = host_layers[0];
@@ -1325,8 +1316,9 @@ int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *ho
         cudaFuncSetAttribute(prepare_reduce_cluster_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
         cudaFuncSetAttribute(prepare_finish_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
         prepare_reduce_cluster_layers_kernel<<<dim3(kPcCtas, L.batch * L.n_q_heads, n_layers), kCompressThreads, s1,
-                                               st>>>(dev_layers);
-        prepare_finish_layers_kernel<<<dim3(L.batch * L.n_q_heads, 1, n_layers), kCompressThreads, s2, st>>>(dev_layers);
+                                               st>>>(dev_layers, yg_slots(L));
+        prepare_finish_layers_kernel<<<dim3(L.batch * L.n_q_heads, 1, n_layers), kCompressThreads, s2, st>>>(
+            dev_layers, yg_slots(L));
         return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
     }
     for (int i = 0; i < n_layers; ++i) {
@@ -1341,8 +1333,8 @@ int launch_prepare(const lrqk_layer_t &L, cudaStream_t st) {
         const size_t s1 = prepare_reduce_smem_bytes(L), s2 = prepare_finish_smem_bytes(L);
         cudaFuncSetAttribute(prepare_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
         cudaFuncSetAttribute(prepare_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-        prepare_reduce_cluster_kernel<<<dim3(kPcCtas, L.batch * L.n_q_heads), kCompressThreads, s1, st>>>(L);
-        prepare_finish_kernel<<<L.batch * L.n_q_heads, kCompressThreads, s2, st>>>(L);
+        prepare_reduce_cluster_kernel<<<dim3(kPcCtas, L.batch * L.n_q_heads), kCompressThreads, s1, st>>>(L, yg_slots(L));
+        prepare_finish_kernel<<<L.batch * L.n_q_heads, kCompressThreads, s2, st>>>(L, yg_slots(L));
         return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
     }
     dim3 grid(compress_chunks(L) + 1, L.batch * L.n_q_heads);

@@ -21,10 +21,12 @@
 // compress_prepare (compress.cu: count_hits_hbm).
 #include "common.cuh"
 #include "select_common.cuh"
+#include "mma_common.cuh"
 
 namespace lrqk {
 
 int score_tma_parts(const lrqk_layer_t &L);
+int yg_slots(const lrqk_layer_t &L);
 
 constexpr int kFThreads = 256;
 constexpr int kFRows = kFThreads * 32;  // keys per scan pass: 32 contiguous keys per thread
@@ -35,6 +37,7 @@ struct FArgs {
     const void *q;
     float *out;
     int parts;
+    int yg_slots;
 };
 
 // Online softmax over the K/V rows listed in rows[0, n) (shared memory),
@@ -112,6 +115,114 @@ __device__ void attend_list(const T *kb, const T *vb, const int *rows, int n, co
     }
 }
 
+// Staged variant: the listed rows' K and V (and, with YG, their proxy rows
+// A) are gathered 64 at a time into shared memory with cp.async (double
+// buffered); each chunk feeds the online softmax of this block and, with YG,
+// the tensor-core reduction Y += A^T K, G += A^T A that the next step's
+// compression needs over Omega_t (compress.cu K2p), so compress_prepare
+// does not gather these rows again.
+template <typename T, int LPR, int PPL, bool YG>
+__device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *vb, const T *proxy, const int *rows,
+                                   int n, const float (&qv)[PPL][Pack<T>::N], float c, float &m, float &l,
+                                   float (&acc)[PPL][Pack<T>::N], uint8_t *stage, float (&yacc)[2][2][4],
+                                   float (&gacc)[4][4]) {
+    constexpr int N = Pack<T>::N;
+    constexpr int RPW = 32 / LPR;
+    const int d = L.dim_stride, R = L.rank_stride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int sub = lane / LPR, sl = lane - sub * LPR;
+    const int ng = nw * RPW, gidx = warp * RPW + sub;
+    const int ldk = d * (int)sizeof(T) + 16, lda = R * 2 + 16;  // bytes (padded rows)
+    const int kp = d * (int)sizeof(T) / 16, ap = YG ? R * 2 / 16 : 0;
+    const int tile_kv = kMmaRows * ldk, buf = 2 * tile_kv + (YG ? kMmaRows * lda : 0);
+    const int nch = (n + kMmaRows - 1) / kMmaRows;
+    auto issue = [&](int ch) {
+        uint8_t *kS = stage + (ch & 1) * buf, *vS = kS + tile_kv, *aS = vS + tile_kv;
+        const int r0 = ch * kMmaRows, nr = min(kMmaRows, n - r0);
+        const int tot = kMmaRows * (2 * kp + ap);
+        for (int e = tid; e < tot; e += blockDim.x) {
+            if (e < 2 * kMmaRows * kp) {
+                const int isv = e >= kMmaRows * kp;
+                const int e2 = e - isv * kMmaRows * kp;
+                const int j = e2 / kp, pk = e2 - j * kp;
+                uint8_t *dst = (isv ? vS : kS) + j * ldk + pk * 16;
+                if (j < nr) cp_async16(dst, (isv ? vb : kb) + (size_t)rows[r0 + j] * d + pk * (16 / sizeof(T)));
+                else *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
+            } else if (YG) {
+                const int e2 = e - 2 * kMmaRows * kp;
+                const int j = e2 / ap, pk = e2 - j * ap;
+                uint8_t *dst = aS + j * lda + pk * 16;
+                if (j < nr) cp_async16(dst, proxy + proxy_pack_offset(rows[r0 + j], pk, ap) * 8);
+                else *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        cp_async_commit();
+    };
+    if (nch > 0) issue(0);
+    for (int ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) { issue(ch + 1); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        __syncthreads();
+        const uint8_t *kS = stage + (ch & 1) * buf, *vS = kS + tile_kv, *aS = vS + tile_kv;
+        const int nr = min(kMmaRows, n - ch * kMmaRows);
+        // online softmax over this chunk: group gidx takes rows gidx, gidx + ng, ...
+        for (int j0 = 0; j0 < kMmaRows; j0 += ng * 4) {
+            float x[4];
+            uint4 vx[4][PPL];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + gidx + u * ng;
+                float sdot = 0.f;
+#pragma unroll
+                for (int pp = 0; pp < PPL; ++pp) {
+                    const uint4 kx = j < kMmaRows ? *reinterpret_cast<const uint4 *>(kS + j * ldk + (sl + pp * LPR) * 16)
+                                                  : make_uint4(0, 0, 0, 0);
+                    vx[u][pp] = j < kMmaRows ? *reinterpret_cast<const uint4 *>(vS + j * ldk + (sl + pp * LPR) * 16)
+                                             : make_uint4(0, 0, 0, 0);
+                    float f[N];
+                    unpack16<T>(kx, f);
+#pragma unroll
+                    for (int e = 0; e < N; ++e) sdot = fmaf(f[e], qv[pp][e], sdot);
+                }
+                x[u] = sdot;
+            }
+#pragma unroll
+            for (int o = LPR / 2; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] += __shfl_xor_sync(0xffffffffu, x[u], o);
+            float mx = m;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                x[u] = (j0 + gidx + u * ng < nr) ? x[u] * c : -INFINITY;
+                mx = fmaxf(mx, x[u]);
+            }
+            if (mx != -INFINITY) {
+                const float scale = exp2f(m - mx);
+                l *= scale;
+#pragma unroll
+                for (int pp = 0; pp < PPL; ++pp)
+#pragma unroll
+                    for (int e = 0; e < N; ++e) acc[pp][e] *= scale;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float pr = exp2f(x[u] - mx);
+                    l += pr;
+#pragma unroll
+                    for (int pp = 0; pp < PPL; ++pp) {
+                        float f[N];
+                        unpack16<T>(vx[u][pp], f);
+#pragma unroll
+                        for (int e = 0; e < N; ++e) acc[pp][e] = fmaf(pr, f[e], acc[pp][e]);
+                    }
+                }
+                m = mx;
+            }
+        }
+        if constexpr (YG) mma_reduce_tile<2, 2>(kS, ldk, aS, lda, R, yacc, gacc);
+        __syncthreads();
+    }
+}
+
 // Merge the lane groups' (m, l, acc) into one block partial: dst[0] = max,
 // dst[1] = sum, dst[2 + i] = acc (log2 domain, as the attention kernel).
 // Groups of a warp merge through shuffles, warps through shared memory with
@@ -171,18 +282,14 @@ __device__ void block_partial(float m, float l, float (&acc)[PPL][Pack<T>::N], i
     __syncthreads();
 }
 
-template <typename T, int LPR, int PPL>
+template <typename T, int LPR, int PPL, bool YG>
 __global__ void __launch_bounds__(kFThreads, 2)
 select_attend_kernel(const FArgs a) {
     const lrqk_layer_t &L = a.L;
     constexpr int N = Pack<T>::N;
-    constexpr int RPW = 32 / LPR;
-    constexpr int NG = (kFThreads / 32) * RPW;
-    extern __shared__ __align__(16) uint8_t f_smem[];
-    int *s_rows = reinterpret_cast<int *>(f_smem);                 // [kFRows] (last block: crit, uint64)
-    int *s_list = s_rows + kFRows;                                 // [kFList]
-    float *s_acc = reinterpret_cast<float *>(s_list + kFList);     // [NG][d]
-    float *s_part = s_acc + NG * L.dim_stride;                     // [d + 2] last block's own partial
+    extern __shared__ __align__(128) uint8_t f_smem[];
+    int *s_rows = reinterpret_cast<int *>(f_smem);                     // [s_cap] this part's rows / winners
+    uint8_t *stage = f_smem + (((size_t)L.s_cap * 4 + 127) & ~(size_t)127);  // K/V/A chunks; later scratch
     __shared__ float s_m[kFThreads / 32], s_l[kFThreads / 32];
     __shared__ int s_scan[32];
     __shared__ int s_flag;
@@ -190,7 +297,7 @@ select_attend_kernel(const FArgs a) {
     const int bh = blockIdx.x / P, part = blockIdx.x - bh * P;
     const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
     const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
-    const int d = L.dim_stride;
+    const int d = L.dim_stride, R = L.rank_stride;
     const int tid = threadIdx.x, lane = tid & 31;
     const int sub = lane / LPR, sl = lane - sub * LPR;
     trace(50);
@@ -228,16 +335,22 @@ select_attend_kernel(const FArgs a) {
     const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
     const T *kb = reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
     const T *vb = reinterpret_cast<const T *>(L.slow_v) + kv_rows * d;
+    const T *proxy = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
     const float c = 1.4426950408889634f * rsqrtf((float)L.head_dim);  // log2(e) / sqrt(d)
+    const size_t PF = yg_part_floats(R, d);
+    float *yg = L.red_scratch + (size_t)bh * a.yg_slots * PF;
     float m = -INFINITY, l = 0.f;
     float acc[PPL][N];
 #pragma unroll
     for (int pp = 0; pp < PPL; ++pp)
 #pragma unroll
         for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
+    float yacc[2][2][4], gacc[4][4];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { yacc[i / 8][(i / 4) & 1][i & 3] = 0.f; gacc[i / 4][i & 3] = 0.f; }
     trace(51);
 
-    // ---- this part's winners: ordered write, then attention ----------------
+    // ---- this part's winners: ordered write, then attention (+ Y, G) -------
     int nloc = 0;
     for (int base = row0; base < row1; base += kFRows) {
         uint4 kv[8];
@@ -270,7 +383,7 @@ select_attend_kernel(const FArgs a) {
             const int bpos = __ffs(smask) - 1;
             smask &= smask - 1u;
             const int x = base + tid * 32 + bpos;
-            if (o < kFRows) s_rows[o] = x;
+            if (o < L.s_cap) s_rows[o] = x;
             if (out + o < k_eff) dst[out + o] = x;
             ++o;
         }
@@ -280,13 +393,16 @@ select_attend_kernel(const FArgs a) {
     if (part == P - 1) {  // Omega_l = the lite window, attended by the last part
         for (int i = tid; i < nl; i += blockDim.x) {
             dst[k_eff + i] = lite_start + i;
-            if (nloc + i < kFRows) s_rows[nloc + i] = lite_start + i;
+            if (nloc + i < L.s_cap) s_rows[nloc + i] = lite_start + i;
         }
         nloc += nl;
     }
     __syncthreads();
-    attend_list<T, LPR, PPL>(kb, vb, s_rows, min(nloc, kFRows), qv, c, d, m, l, acc);
+    attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc, stage, yacc,
+                                        gacc);
     trace(52);
+    if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)part * PF);
+    float *s_acc = reinterpret_cast<float *>(stage);  // [nwarps][d]
     float *part_dst = L.attn_scratch + ((size_t)bh * attn_slots_dev(L, P) + part) * (size_t)(d + 2);
     block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, part_dst);
     if (!last_arrival(L.counters + (size_t)bh * kCounterInts + C_FUSED, P, &s_flag)) return;
@@ -298,12 +414,7 @@ select_attend_kernel(const FArgs a) {
     const int lane_ = tid & 31, warp_ = tid >> 5;
     const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && n_crit <= kCritCap;
     const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, P) * (size_t)(d + 2);
-    // the parts' (max, sum), fetched while bin D is ranked
-    float *s_pml = s_part + d + 2;  // [2 * P]
-    for (int p = tid; p < P; p += blockDim.x) {
-        s_pml[2 * p] = __ldcg(parts + (size_t)p * (d + 2));
-        s_pml[2 * p + 1] = __ldcg(parts + (size_t)p * (d + 2) + 1);
-    }
+    int *s_list = s_rows;  // the winners of bin D
     uint32_t hint = klo + ((uint32_t)(D + 1) << kWinShift);
     int nwin = 0;
     if (!ok) {
@@ -341,7 +452,7 @@ select_attend_kernel(const FArgs a) {
     } else {
         int M = 1;
         while (M < n_crit) M <<= 1;
-        uint64_t *crit = reinterpret_cast<uint64_t *>(s_rows);
+        uint64_t *crit = reinterpret_cast<uint64_t *>(stage);
         for (int i = tid; i < M; i += blockDim.x) crit[i] = i < n_crit ? __ldcg(cand + i) : 0ull;
         __syncthreads();
         block_bitonic(crit, M, true);  // descending composites: ties -> lower index first
@@ -365,9 +476,19 @@ select_attend_kernel(const FArgs a) {
         for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
     m = -INFINITY;
     l = 0.f;
-    attend_list<T, LPR, PPL>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { yacc[i / 8][(i / 4) & 1][i & 3] = 0.f; gacc[i / 4][i & 3] = 0.f; }
+    attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
+    if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
+    float *s_part = reinterpret_cast<float *>(stage) + (kFThreads / 32) * d;  // [d + 2]
+    float *s_pml = s_part + d + 2;                                             // [2 * P]
     block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, s_part);
     trace(58);
+    for (int p = tid; p < P; p += blockDim.x) {
+        s_pml[2 * p] = __ldcg(parts + (size_t)p * (d + 2));
+        s_pml[2 * p + 1] = __ldcg(parts + (size_t)p * (d + 2) + 1);
+    }
+    __syncthreads();
     // merge the P part partials with this block's (the lite rows, in the last
     // part, are never empty, so the maximum is finite)
     float MM = s_part[0];
@@ -399,6 +520,7 @@ select_attend_kernel(const FArgs a) {
         meta[M_CAND] = 0;
         meta[M_HINT] = (int)hint;
         meta[M_HINT_OK] = 1;
+        meta[M_YG] = YG ? P + 1 : 0;
         meta[M_STAT + 5] += 1;
     }
     uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;  // ready for the next step
@@ -413,28 +535,34 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
     const int packs = L.dim_stride / N;
     const int lpr = packs < 32 ? packs : 32;
     const int ppl = packs / lpr;
-    const int ng = (kFThreads / 32) * (32 / lpr);
-    const size_t smem = (size_t)kFRows * 4 + (size_t)kFList * 4 +
-                        ((size_t)ng * L.dim_stride + L.dim_stride + 2 + 2 * (size_t)a.parts) * 4;
+    // the Y|G reduction rides along for the bf16 rank-32, d-128 layout
+    const bool yg = sizeof(T) == 2 && L.rank_stride == 32 && L.dim_stride == 128;
+    const size_t ldk = (size_t)L.dim_stride * sizeof(T) + 16, lda = (size_t)L.rank_stride * 2 + 16;
+    const size_t stage = 2 * (2 * kMmaRows * ldk + (yg ? kMmaRows * lda : 0));
+    const size_t last = (size_t)kCritCap * 8 > stage ? (size_t)kCritCap * 8 : stage;  // crit sort reuses it
+    const size_t tail = ((size_t)(kFThreads / 32) * L.dim_stride + L.dim_stride + 2 + 2 * (size_t)a.parts) * 4;
+    const size_t smem = (((size_t)L.s_cap * 4 + 127) & ~(size_t)127) + (last > tail ? last : tail);
     const int grid = L.batch * L.n_q_heads * a.parts;
-#define LRQK_F(LP, PP)                                                                            \
+#define LRQK_F(LP, PP, YG)                                                                        \
     do {                                                                                          \
-        auto fn = select_attend_kernel<T, LP, PP>;                                                \
+        auto fn = select_attend_kernel<T, LP, PP, YG>;                                            \
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
         launch_kernel(fn, grid, kFThreads, smem, st, true, a);                                    \
     } while (0)
-    if (ppl == 1) {
+    if (yg && ppl == 1 && lpr == 16) {
+        if constexpr (sizeof(T) == 2) LRQK_F(16, 1, true);
+    } else if (ppl == 1) {
         switch (lpr) {
-            case 1: LRQK_F(1, 1); break;
-            case 2: LRQK_F(2, 1); break;
-            case 4: LRQK_F(4, 1); break;
-            case 8: LRQK_F(8, 1); break;
-            case 16: LRQK_F(16, 1); break;
-            case 32: LRQK_F(32, 1); break;
+            case 1: LRQK_F(1, 1, false); break;
+            case 2: LRQK_F(2, 1, false); break;
+            case 4: LRQK_F(4, 1, false); break;
+            case 8: LRQK_F(8, 1, false); break;
+            case 16: LRQK_F(16, 1, false); break;
+            case 32: LRQK_F(32, 1, false); break;
             default: return LRQK_EUNSUPPORTED;
         }
     } else if (ppl == 2 && lpr == 32) {
-        LRQK_F(32, 2);
+        LRQK_F(32, 2, false);
     } else {
         return LRQK_EUNSUPPORTED;
     }
@@ -444,7 +572,7 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
 
 int launch_select_attend(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st) {
     if (L.policy != LRQK_SLOW_HBM) return LRQK_OK;  // mode 5 is HBM-only
-    FArgs a{L, q, out, score_tma_parts(L)};
+    FArgs a{L, q, out, score_tma_parts(L), yg_slots(L)};
     return L.dtype == LRQK_BF16 ? launch_select_attend_t<__nv_bfloat16>(a, st) : launch_select_attend_t<float>(a, st);
 }
 

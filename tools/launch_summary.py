@@ -15,6 +15,10 @@ print(f"{'kernel':60s} {'n':>5s} {'mean_us':>10s} {'total_us':>12s}")
 for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
     print(f"{k[:60]:60s} {len(v):5d} {sum(v)/len(v):10.2f} {sum(v):12.1f}")
 last_pf = max((i for i, (k, _) in enumerate(launches) if "pf_" in k or "seed" in k), default=-1)
+if len(sys.argv) > 2:  # steady state: skip the first N decode steps (ends of steps = advance_kernel)
+    adv = [i for i, (k, _) in enumerate(launches) if "advance_kernel" in k and i > last_pf]
+    if len(adv) > int(sys.argv[2]):
+        last_pf = adv[int(sys.argv[2]) - 1]
 dec = [(k, v) for k, v in launches[last_pf + 1:] if k.startswith("lrqk::")]
 tot = sum(v for _, v in dec) or 1.0
 dagg = collections.defaultdict(float)
