@@ -144,6 +144,9 @@ int lrqk_compress_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_laye
                                  void *stream);
 
 /* Per-token compression + B line-search update + append of k_hat/k/v.
+ * With bf16 storage (rank >= 16, d >= 64) the B update only feeds the next
+ * step, so it is deferred: the next lrqk_compress_prepare(_layers) applies
+ * it before forming the next step's systems (eta is written then). 
  * ref: decode.py:122-184 (decode_compress, update_projections),
  *      cache.py:199-214 (append_token), session.py:95-98.
  * q [B,Hq,dim_stride], k/v [B,Hkv,dim_stride] dtype. */

@@ -45,11 +45,12 @@ struct CompressArgs {
     lrqk_layer_t L;
     const void *q, *k, *v;
     int update_b;
+    int defer_b;  // leave the B update to the next compress_prepare (cluster path)
 };
 
 // Per-head precompute ("pre" buffer) written by K2p, read by K2c.
 struct PreLayout {
-    int Pinv, Rinv, P, R, ZQ, ZK, W, flags, total;
+    int Pinv, Rinv, P, R, ZQ, ZK, W, flags, X, total;
 };
 __host__ __device__ inline PreLayout pre_layout(int R, int d) {
     PreLayout p;
@@ -61,7 +62,8 @@ __host__ __device__ inline PreLayout pre_layout(int R, int d) {
     p.ZQ = o; o += R * d;
     p.ZK = o; o += R * d;
     p.W = o; o += R * d;
-    p.flags = o; o += 4;   // okP, okR
+    p.flags = o; o += 4;   // okP, okR, B update pending
+    p.X = o; o += 2 * d + 2 * R;  // deferred B update: q, k, q_hat, k_hat of the step
     p.total = (o + 3) & ~3;
     return p;
 }
@@ -778,6 +780,56 @@ prepare_kernel(const lrqk_layer_t L) {
 // Both are brief, so the precompute barely competes with the decode chain
 // it overlaps on the side stream.
 // ---------------------------------------------------------------------------
+// The line-search B update of decode.py:150-184 for both sides, on B rows
+// staged in shared memory (row stride ldB): resid = x_hat B - x,
+// eta = (resid . s) / (s . s) with s = |x_hat|^2 resid (0 under the
+// reference's floor), B -= eta x_hat^T resid.  X = [q | k | q_hat | k_hat].
+// Writes the updated rows back to B_Q / B_K and eta.  scratch: 2 * d floats.
+__device__ void apply_deferred_b_update(const lrqk_layer_t &L, int bh, const float *X, float *sBQ, float *sBK,
+                                        int ldB, float *scratch, float *s_red) {
+    const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float *resid = scratch;  // [2][d]
+    for (int w = tid; w < 2 * d; w += blockDim.x) {
+        const int side = w / d, i = w - side * d;
+        const float *xh = X + 2 * d + side * R;
+        const float *Bm = side ? sBK : sBQ;
+        float a0 = 0.f, a1 = 0.f;
+        int p = 0;
+        for (; p + 1 < r; p += 2) {
+            a0 = fmaf(__ldcg(xh + p), Bm[p * ldB + i], a0);
+            a1 = fmaf(__ldcg(xh + p + 1), Bm[(p + 1) * ldB + i], a1);
+        }
+        if (p < r) a0 = fmaf(__ldcg(xh + p), Bm[p * ldB + i], a0);
+        resid[w] = a0 + a1 - __ldcg(X + side * d + i);
+    }
+    __syncthreads();
+    if (warp < 2) {
+        const int side = warp;
+        const float *xh = X + 2 * d + side * R;
+        float nx = 0.f;
+        for (int p = lane; p < r; p += 32) nx = fmaf(__ldcg(xh + p), __ldcg(xh + p), nx);
+        nx = warp_sum(nx);
+        float ss = 0.f;
+        for (int i = lane; i < d; i += 32) ss = fmaf(resid[side * d + i], resid[side * d + i], ss);
+        ss = warp_sum(ss);
+        const float num = nx * ss, den = nx * num;
+        if (lane == 0) s_red[side] = (den <= 1e-14f * (1.f + fabsf(num))) ? 0.f : num / den;
+    }
+    __syncthreads();
+    for (int w = tid; w < 2 * r * d; w += blockDim.x) {
+        const int side = w / (r * d), e = w - side * r * d;
+        const int p = e / d, i = e - p * d;
+        const float eta = s_red[side];
+        float *Bm = side ? sBK : sBQ;
+        const float v = Bm[p * ldB + i] - eta * __ldcg(X + 2 * d + side * R + p) * resid[side * d + i];
+        Bm[p * ldB + i] = v;
+        (side ? L.B_K : L.B_Q)[(size_t)bh * R * d + p * d + i] = v;
+    }
+    if (tid < 2) L.eta[(size_t)bh * 2 + tid] = s_red[tid];
+    __syncthreads();
+}
+
 constexpr int kPcCtas = 8;
 constexpr int kPcBufs = 4;  // gather buffers per CTA (kPcBufs - 1 sub-chunks in flight)
 
@@ -866,6 +918,11 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
     if (!host) count_hits_hbm(L, bh, n, s_rc);
     stage_rows_f32(sBQ, ldB, L.B_Q + (size_t)bh * R * d, R, d);
     stage_rows_f32(sBK, ldB, L.B_K + (size_t)bh * R * d, R, d);
+    if (pre[PL.flags + 2] != 0.f) {  // the step's deferred line-search B update
+        __syncthreads();
+        apply_deferred_b_update(L, bh, pre + PL.X, sBQ, sBK, ldB, tmp, s_rc);
+        if (tid == 0) pre[PL.flags + 2] = 0.f;
+    }
     for (int e = tid; e < R * R; e += blockDim.x) {  // identity padding
         const int i = e / R, j = e - i * R;
         if (i >= r || j >= r) { b0[i * ldM + j] = (i == j) ? 1.f : 0.f; b1[i * ldM + j] = (i == j) ? 1.f : 0.f; }
@@ -929,6 +986,12 @@ prepare_finish_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) { prepare_fin
 static bool pc_enabled() {
     static const bool on = [] { const char *e = getenv("LRQK_PREPARE_CLUSTER"); return !(e && e[0] == '0'); }();
     return on;
+}
+
+// compress_prepare runs as cluster reduce + finish kernels (which also apply
+// the deferred B update) for bf16 storage with rank >= 16, d >= 64
+static bool cluster_prepare_path(const lrqk_layer_t &L) {
+    return L.dtype == LRQK_BF16 && L.rank_stride >= 16 && L.dim_stride >= 64 && pc_enabled();
 }
 
 static size_t prepare_reduce_smem_bytes(const lrqk_layer_t &L) {
@@ -1193,6 +1256,16 @@ compress_kernel(const CompressArgs args) {
         __syncthreads();
     }
     trace(3);
+    if (args.update_b && args.defer_b) {
+        // The line-search B update (decode.py:150-184) only feeds the next
+        // step: hand q, k, q_hat, k_hat to compress_prepare, which applies it
+        // off the decode critical path.
+        float *X = L.pre + (size_t)bh * PL.total + PL.X;
+        for (int i = tid; i < d; i += blockDim.x) { X[i] = vq[i]; X[d + i] = vk[i]; }
+        for (int i = tid; i < R; i += blockDim.x) { X[2 * d + i] = qh[i]; X[2 * d + R + i] = kh[i]; }
+        if (tid == 0) L.pre[(size_t)bh * PL.total + PL.flags + 2] = 1.f;
+        s_scalar[2] = s_scalar[3] = 0.f;
+    } else {
 
     // ---------------- line-search B update (decode.py:150-184), both sides --
     // resid = x_hat B - x ; s = x_hat grad = |x_hat|^2 resid ; eta = (resid.s)/(s.s)
@@ -1244,6 +1317,7 @@ compress_kernel(const CompressArgs args) {
             *reinterpret_cast<float4 *>((side ? L.B_K : L.B_Q) + (size_t)bh * R * d + p * d + i) = o;
         }
     }
+    }  // immediate B update
     trace(4);
 
     // ---------------- outputs and appends ---------------------------------
@@ -1251,7 +1325,7 @@ compress_kernel(const CompressArgs args) {
         L.q_hat[(size_t)bh * R + i] = qh[i];
         L.k_hat[(size_t)bh * R + i] = kh[i];
     }
-    if (tid == 0) {
+    if (tid == 0 && !(args.update_b && args.defer_b)) {
         L.eta[(size_t)bh * 2 + 0] = s_scalar[2];
         L.eta[(size_t)bh * 2 + 1] = s_scalar[3];
     }
@@ -1311,7 +1385,7 @@ int yg_slots(const lrqk_layer_t &L);
 int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int n_layers,
                           cudaStream_t st) {
     const lrqk_layer_t &L = host_layers[0];
-    if (L.dtype == LRQK_BF16 && L.rank_stride >= 16 && L.dim_stride >= 64 && pc_enabled()) {
+    if (cluster_prepare_path(L)) {
         const size_t s1 = prepare_reduce_smem_bytes(L), s2 = prepare_finish_smem_bytes(L);
         cudaFuncSetAttribute(prepare_reduce_cluster_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
         cudaFuncSetAttribute(prepare_finish_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
@@ -1329,7 +1403,7 @@ int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *ho
 }
 
 int launch_prepare(const lrqk_layer_t &L, cudaStream_t st) {
-    if (L.dtype == LRQK_BF16 && L.rank_stride >= 16 && L.dim_stride >= 64 && pc_enabled()) {
+    if (cluster_prepare_path(L)) {
         const size_t s1 = prepare_reduce_smem_bytes(L), s2 = prepare_finish_smem_bytes(L);
         cudaFuncSetAttribute(prepare_reduce_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
         cudaFuncSetAttribute(prepare_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
@@ -1351,7 +1425,7 @@ int launch_prepare(const lrqk_layer_t &L, cudaStream_t st) {
 
 int launch_compress(const lrqk_layer_t &L, const void *q, const void *k, const void *v, int update_b,
                     cudaStream_t st) {
-    CompressArgs a{L, q, k, v, update_b};
+    CompressArgs a{L, q, k, v, update_b, cluster_prepare_path(L) ? 1 : 0};
     const size_t smem = compress_smem_bytes(L);
     if (L.dtype == LRQK_BF16) {
         cudaFuncSetAttribute(compress_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
