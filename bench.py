@@ -420,7 +420,7 @@ def cpu_baseline(w, total_seq, budget_s=15.0, steps_override=None):
     ctx = w["ctx"]
     # probe one step to size the sample
     probe = _cpu_worker((ctx, w["d"], w["r"], w["k"], w["lite"], 1, 0))
-    n_steps = steps_override or max(2, min(20, int(budget_s / max(probe, 1e-3) / 2)))
+    n_steps = steps_override or max(2, min(500, int(budget_s / max(probe, 1e-3) / 2)))
     with mp.get_context("spawn").Pool(cores) as pool:
         t0 = time.perf_counter()
         per = pool.map(_cpu_worker, [(ctx, w["d"], w["r"], w["k"], w["lite"], n_steps, 1 + i) for i in range(cores)])

@@ -336,7 +336,8 @@ score_tma_kernel(const ScoreArgs a) {
                 const uint32_t key = score_key(s0 + s1);
                 if (row < n) st_hint_u32(keys + row, key, pol_keys);
                 if (row < lite_start) {
-                    if ((tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
+                    // the sampled coarse histogram only serves the no-hint path
+                    if (!win && (tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
                     if (win && key >= klo) {
                         const uint32_t dk = key - klo;
                         if (dk < kWinKeys) atomicAdd(&s_win[dk >> kWinShift], 1);
@@ -433,6 +434,21 @@ score_tma_kernel(const ScoreArgs a) {
             return;
         }
         __syncthreads();
+    }
+    if (win) {  // the hint window missed and no coarse histogram was taken: exact path
+        if (tid == 0) {
+            meta[M_B_HI] = kHistBins - 1;
+            meta[M_B_LO] = 0;
+            meta[M_STRIDE] = 1;
+            meta[M_S2] = 0;
+            meta[M_K_EFF] = k_eff;
+            meta[M_LITE] = lite_start;
+            meta[M_SURE] = 0;
+            meta[M_CAND] = 0;
+            meta[M_ABOVE] = 0;
+            meta[M_MODE] = 0;
+        }
+        return;
     }
     for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = (int)__ldcg(ghist + i);
     __syncthreads();

@@ -223,6 +223,45 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
     }
 }
 
+// Y = A^T K and G = A^T A over n <= kMmaRows listed rows (bf16 storage), on
+// the CUDA cores: the rows are staged as fp32 in shared memory (stage >=
+// n * (d + R) floats), then each thread owns (R*d + R*R) / blockDim.x
+// outputs.  Writes the full partial (zeros for n == 0).
+template <typename T>
+__device__ void yg_rows_small(const lrqk_layer_t &L, const T *kb, const T *proxy, const int *rows, int n,
+                              float *stage, float *dst) {
+    const int d = L.dim_stride, R = L.rank_stride, ap = R * (int)sizeof(T) / 16;
+    constexpr int N = Pack<T>::N;
+    float *sK = stage, *sA = stage + (size_t)kMmaRows * d;
+    for (int e = threadIdx.x; e < n * (d / N + ap); e += blockDim.x) {
+        float f[N];
+        if (e < n * (d / N)) {
+            const int j = e / (d / N), pk = e - j * (d / N);
+            unpack16<T>(*reinterpret_cast<const uint4 *>(kb + (size_t)rows[j] * d + pk * N), f);
+#pragma unroll
+            for (int u = 0; u < N; ++u) sK[j * d + pk * N + u] = f[u];
+        } else {
+            const int e2 = e - n * (d / N), j = e2 / ap, pk = e2 - j * ap;
+            unpack16<T>(*reinterpret_cast<const uint4 *>(proxy + proxy_pack_offset(rows[j], pk, ap) * N), f);
+#pragma unroll
+            for (int u = 0; u < N; ++u) sA[j * R + pk * N + u] = f[u];
+        }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < R * d + R * R; o += blockDim.x) {
+        float acc = 0.f;
+        if (o < R * d) {
+            const int p = o / d, i = o - p * d;
+            for (int j = 0; j < n; ++j) acc = fmaf(sA[j * R + p], sK[j * d + i], acc);
+        } else {
+            const int o2 = o - R * d, p = o2 / R, q = o2 - p * R;
+            for (int j = 0; j < n; ++j) acc = fmaf(sA[j * R + p], sA[j * R + q], acc);
+        }
+        dst[o] = acc;
+    }
+    __syncthreads();
+}
+
 // Merge the lane groups' (m, l, acc) into one block partial: dst[0] = max,
 // dst[1] = sum, dst[2 + i] = acc (log2 domain, as the attention kernel).
 // Groups of a warp merge through shuffles, warps through shared memory with
@@ -478,8 +517,15 @@ select_attend_kernel(const FArgs a) {
     l = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) { yacc[i / 8][(i / 4) & 1][i & 3] = 0.f; gacc[i / 4][i & 3] = 0.f; }
-    attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
-    if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
+    if (nwin > kMmaRows) {
+        attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
+        if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
+    } else {
+        // a handful of rows: attention from registers; Y, G on the CUDA cores
+        attend_list<T, LPR, PPL>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);
+        if constexpr (YG) yg_rows_small(L, kb, proxy, s_list, nwin, reinterpret_cast<float *>(stage),
+                                        yg + (size_t)P * PF);
+    }
     float *s_part = reinterpret_cast<float *>(stage) + (kFThreads / 32) * d;  // [d + 2]
     float *s_pml = s_part + d + 2;                                             // [2 * P]
     block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, s_part);
