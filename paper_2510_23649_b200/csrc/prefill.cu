@@ -1,3 +1,4 @@
+#include <cstdlib>
 // K1: prefill joint rank-r factorisation, batched over heads.
 //
 // ref: prefill.py:142-230 (lagrangian_value, update_B, update_AK, update_AQ,
@@ -23,6 +24,7 @@
 // does the r x r algebra (Gauss-Jordan inverse with the reference jitter
 // retry, linalg.py:80-91).
 #include "common.cuh"
+#include "mma_common.cuh"
 
 namespace lrqk {
 
@@ -238,6 +240,253 @@ pf_pass_kernel(const PfDims D, const T *X, int is_k, const float *A_in, float *A
         part[ds * rs + rs * rs] = sd;
         part[ds * rs + rs * rs + 1] = want_x2 ? sx : 0.f;
     }
+}
+
+// ---------------------------------------------------------------------------
+// Tensor-core pass (bf16 X, d = 128, rank_stride RS in {16, 32, 64}): the
+// same three products as pf_pass_kernel on mma.sync m16n8k16 with fp32
+// accumulation.  X is exact in bf16; the fp32 operands W and A are split
+// into bf16 hi + lo parts (3xBF16: hi*hi + hi*lo + lo*hi), which keeps the
+// products to ~2^-16 relative, the accuracy class of the fp32 CUDA-core
+// pass.  Per 128-row tile, 8 warps:
+//   A_new = X W      warp w: rows [16w, 16w+16) x all RS columns
+//   C    += X^T A    warp w: d rows [16w, 16w+16) x all RS columns
+//   G    += A^T A    RS/16 x RS/8 tiles spread over the warps
+// The pass is memory-bound (X streamed once, A read/written once), so
+// mma.sync already reaches the HBM roofline.
+// ---------------------------------------------------------------------------
+constexpr int kPfD = 128;
+
+LRQK_DEV void ldsm_x4(uint32_t (&r)[4], const void *p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+LRQK_DEV void ldsm_x2(uint32_t (&r)[2], const void *p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1]) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+}
+LRQK_DEV void split_bf16(float v, __nv_bfloat16 &hi, __nv_bfloat16 &lo) {
+    hi = __float2bfloat16_rn(v);
+    lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+}
+
+template <int RS>
+__global__ void __launch_bounds__(kPfThreads)
+pf_pass_mma_kernel(const PfDims D, const __nv_bfloat16 *X, int is_k, const float *A_in, float *A_out, int update,
+                   int want_x2, float *scratch) {
+    constexpr int NT = RS / 8;                        // n tiles over the rank
+    constexpr int GT = (RS / 16) * (RS / 8);          // G tiles
+    constexpr int GPW = (GT + 7) / 8;                 // G tiles per warp
+    constexpr int LDX = kPfD * 2 + 16, LDA = RS * 2 + 16, LDW = kPfD * 2 + 16;  // bytes
+    extern __shared__ __align__(16) uint8_t pm[];
+    uint8_t *sXb = pm;                                // 2 x [128][LDX]  X tiles (bf16), double buffered
+    uint8_t *sAh = sXb + 2 * kPfRows * LDX;           // [128][LDA]  A tile hi
+    uint8_t *sAl = sAh + kPfRows * LDA;               // [128][LDA]  A tile lo
+    uint8_t *sWh = sAl + kPfRows * LDA;               // [RS][LDW]   W^T hi
+    uint8_t *sWl = sWh + RS * LDW;                    // [RS][LDW]   W^T lo
+    float *sRed = reinterpret_cast<float *>(sWl + RS * LDW);
+    const int h = blockIdx.y, nb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const PfState st = pf_state(D);
+    float *hs = scratch + (size_t)h * D.head_sz;
+    if (hs[st.misc + PF_ACTIVE] == 0.f) return;
+    const int xh = is_k ? h / D.group : h;
+    const __nv_bfloat16 *Xh = X + (size_t)xh * D.l * kPfD;
+    const float *Ain = A_in + (size_t)h * D.l * RS;
+    float *Aout = A_out + (size_t)h * D.l * RS;
+    if (update) {  // W^T (RS x d), split
+        const float *W = hs + st.W;  // [d][RS]
+        for (int e = tid; e < kPfD * RS; e += blockDim.x) {
+            const int k = e / RS, p = e - k * RS;
+            __nv_bfloat16 hi, lo;
+            split_bf16(W[e], hi, lo);
+            reinterpret_cast<__nv_bfloat16 *>(sWh + p * LDW)[k] = hi;
+            reinterpret_cast<__nv_bfloat16 *>(sWl + p * LDW)[k] = lo;
+        }
+    }
+    const int nchunks = (D.l + kPfRows - 1) / kPfRows;
+    const int c0 = (int)((long long)nchunks * nb / D.NB), c1 = (int)((long long)nchunks * (nb + 1) / D.NB);
+    const int q = lane >> 3, i8 = lane & 7, fr = lane >> 2, fc = (lane & 3) * 2;
+    float cacc[NT][4], gacc[GPW][4];
+    static_assert(kPfD / 8 == 16, "X rows are 16 packs");
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cacc[n][e] = 0.f;
+#pragma unroll
+    for (int g = 0; g < GPW; ++g)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) gacc[g][e] = 0.f;
+    float diff = 0.f, x2 = 0.f;
+    // X tiles stream through shared memory with cp.async, one tile ahead
+    auto issue_x = [&](int c) {
+        uint8_t *dst = sXb + (c & 1) * kPfRows * LDX;
+        const int row0 = c * kPfRows, nrow = min(kPfRows, D.l - row0);
+        for (int e = tid; e < kPfRows * (kPfD / 8); e += blockDim.x) {
+            const int i = e >> 4, pk = e & 15;
+            if (i < nrow) cp_async16(dst + i * LDX + pk * 16, Xh + (size_t)(row0 + i) * kPfD + pk * 8);
+            else *reinterpret_cast<uint4 *>(dst + i * LDX + pk * 16) = make_uint4(0, 0, 0, 0);
+        }
+        cp_async_commit();
+    };
+    if (c0 < c1) issue_x(c0);
+    for (int c = c0; c < c1; ++c) {
+        const int row0 = c * kPfRows;
+        const int nrow = min(kPfRows, D.l - row0);
+        uint8_t *sX = sXb + (c & 1) * kPfRows * LDX;
+        __syncthreads();  // the other buffer is free again
+        if (c + 1 < c1) { issue_x(c + 1); cp_async_wait<1>(); }
+        else cp_async_wait<0>();
+        // old A of this warp's rows (update: the convergence measure), early
+        float2 aold[NT][2];
+        if (update) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int i = warp * 16 + fr + hf * 8;
+                    aold[n][hf] = i < nrow ? __ldcs(reinterpret_cast<const float2 *>(Ain + (size_t)(row0 + i) * RS + n * 8 + fc))
+                                           : make_float2(0.f, 0.f);
+                }
+        }
+        __syncthreads();
+        if (want_x2) {
+            for (int e = tid; e < kPfRows * (kPfD / 8); e += blockDim.x) {
+                float f[8];
+                unpack16<__nv_bfloat16>(*reinterpret_cast<const uint4 *>(sX + (e >> 4) * LDX + (e & 15) * 16), f);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x2 = fmaf(f[u], f[u], x2);
+            }
+        }
+        if (!update) {  // A tile from A_in, split
+            for (int e = tid; e < kPfRows * RS; e += blockDim.x) {
+                const int i = e / RS, p2 = e - i * RS;
+                const float v = i < nrow ? Ain[(size_t)(row0 + i) * RS + p2] : 0.f;
+                __nv_bfloat16 hi, lo;
+                split_bf16(v, hi, lo);
+                reinterpret_cast<__nv_bfloat16 *>(sAh + i * LDA)[p2] = hi;
+                reinterpret_cast<__nv_bfloat16 *>(sAl + i * LDA)[p2] = lo;
+            }
+        }
+        __syncthreads();
+        if (update) {
+            // ---- A_new = X W: warp rows [16w, 16w+16) -------------------------
+            float aacc[NT][4];
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) aacc[n][e] = 0.f;
+#pragma unroll
+            for (int ks = 0; ks < kPfD; ks += 16) {
+                uint32_t af[4];
+                ldsm_x4(af, sX + (warp * 16 + (lane & 15)) * LDX + (ks + (lane >> 4) * 8) * 2);
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    uint32_t bh[2], bl[2];
+                    const uint8_t *wrow = (lane & 7) * LDW + (ks + ((lane >> 3) & 1) * 8) * 2 + (size_t)n * 8 * LDW + sWh;
+                    ldsm_x2(bh, wrow);
+                    ldsm_x2(bl, wrow + (sWl - sWh));
+                    mma_bf16_16816(aacc[n], af, bh);
+                    mma_bf16_16816(aacc[n], af, bl);
+                }
+            }
+            // fragment rows fr, fr + 8 of this warp's 16, columns n*8 + fc, +1
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int i = warp * 16 + fr + hf * 8, p2 = n * 8 + fc;
+                    float v0 = p2 < D.r ? aacc[n][hf * 2] : 0.f, v1 = p2 + 1 < D.r ? aacc[n][hf * 2 + 1] : 0.f;
+                    if (i >= nrow) { v0 = 0.f; v1 = 0.f; }
+                    if (i < nrow) {
+                        const float2 old = aold[n][hf];
+                        diff = fmaf(v0 - old.x, v0 - old.x, diff);
+                        diff = fmaf(v1 - old.y, v1 - old.y, diff);
+                        *reinterpret_cast<float2 *>(Aout + (size_t)(row0 + i) * RS + p2) = make_float2(v0, v1);
+                    }
+                    __nv_bfloat16 h0, l0, h1, l1;
+                    split_bf16(v0, h0, l0);
+                    split_bf16(v1, h1, l1);
+                    __nv_bfloat162 hh, ll;
+                    hh.x = h0; hh.y = h1; ll.x = l0; ll.y = l1;
+                    *reinterpret_cast<__nv_bfloat162 *>(sAh + i * LDA + p2 * 2) = hh;
+                    *reinterpret_cast<__nv_bfloat162 *>(sAl + i * LDA + p2 * 2) = ll;
+                }
+            }
+            __syncthreads();
+        }
+        // ---- C += X^T A: warp d rows [16w, 16w+16) ---------------------------
+#pragma unroll
+        for (int ks = 0; ks < kPfRows; ks += 16) {
+            uint32_t af[4];
+            ldsm_x4_trans(af, sX + (ks + ((q & 2) ? 8 : 0) + i8) * LDX + (warp * 16 + ((q & 1) ? 8 : 0)) * 2);
+            const int k0 = ks + ((lane >> 3) & 1) * 8;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                uint32_t bh[2], bl[2];
+                ldsm_x2_trans(bh, sAh + (k0 + i8) * LDA + n * 16);
+                ldsm_x2_trans(bl, sAl + (k0 + i8) * LDA + n * 16);
+                mma_bf16_16816(cacc[n], af, bh);
+                mma_bf16_16816(cacc[n], af, bl);
+            }
+        }
+        // ---- G += A^T A (hi hi + hi lo + lo hi) -------------------------------
+#pragma unroll
+        for (int g = 0; g < GPW; ++g) {
+            const int gt = warp + 8 * g;
+            if (gt >= GT) break;
+            const int mt = gt / NT, n0 = (gt % NT) * 8;
+#pragma unroll
+            for (int ks = 0; ks < kPfRows; ks += 16) {
+                uint32_t ah[4], al[4];
+                const int m0 = mt * 16 + ((q & 1) ? 8 : 0), kk = ks + ((q & 2) ? 8 : 0);
+                ldsm_x4_trans(ah, sAh + (kk + i8) * LDA + m0 * 2);
+                ldsm_x4_trans(al, sAl + (kk + i8) * LDA + m0 * 2);
+                uint32_t bh[2], bl[2];
+                const int k0 = ks + ((lane >> 3) & 1) * 8;
+                ldsm_x2_trans(bh, sAh + (k0 + i8) * LDA + n0 * 2);
+                ldsm_x2_trans(bl, sAl + (k0 + i8) * LDA + n0 * 2);
+                mma_bf16_16816(gacc[g], ah, bh);
+                mma_bf16_16816(gacc[g], ah, bl);
+                mma_bf16_16816(gacc[g], al, bh);
+            }
+        }
+    }
+    // ---- this block's partial: C (d x RS) | G (RS x RS) | diff | x2 ---------
+    float *part = scratch + pf_part_off(D, h, nb);
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        const int k = warp * 16 + fr, p2 = n * 8 + fc;
+        *reinterpret_cast<float2 *>(part + k * RS + p2) = make_float2(cacc[n][0], cacc[n][1]);
+        *reinterpret_cast<float2 *>(part + (k + 8) * RS + p2) = make_float2(cacc[n][2], cacc[n][3]);
+    }
+#pragma unroll
+    for (int g = 0; g < GPW; ++g) {
+        const int gt = warp + 8 * g;
+        if (gt >= GT) break;
+        const int mt = gt / NT, n0 = (gt % NT) * 8;
+        float *gp = part + kPfD * RS + (mt * 16 + fr) * RS + n0 + fc;
+        *reinterpret_cast<float2 *>(gp) = make_float2(gacc[g][0], gacc[g][1]);
+        *reinterpret_cast<float2 *>(gp + 8 * RS) = make_float2(gacc[g][2], gacc[g][3]);
+    }
+    float v2[2] = {diff, x2};
+    for (int j = 0; j < 2; ++j) {
+        const float sj = warp_sum(v2[j]);
+        if (lane == 0) sRed[j * 32 + warp] = sj;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float sd = 0.f, sx = 0.f;
+        for (int w = 0; w < (int)blockDim.x / 32; ++w) { sd += sRed[w]; sx += sRed[32 + w]; }
+        part[kPfD * RS + RS * RS] = sd;
+        part[kPfD * RS + RS * RS + 1] = want_x2 ? sx : 0.f;
+    }
+}
+
+template <int RS>
+static size_t pf_mma_smem() {
+    return 2 * (size_t)kPfRows * (kPfD * 2 + 16) + 2 * (size_t)kPfRows * (RS * 2 + 16) +
+           2 * (size_t)RS * (kPfD * 2 + 16) + 64 * sizeof(float);
 }
 
 // d x d Gram of X (objective only): GX[i][j] = sum_l X[l][i] X[l][j]
@@ -569,6 +818,11 @@ static PfDims pf_dims(const lrqk_prefill_t &P, int nsm) {
 
 extern int num_sms();
 
+static bool pf_mma_enabled() {
+    static const bool on = [] { const char *e = getenv("LRQK_PREFILL_MMA"); return !(e && e[0] == '0'); }();
+    return on;
+}
+
 size_t prefill_scratch_floats(const lrqk_prefill_t &P) {
     PfDims D = pf_dims(P, num_sms());
     return (size_t)D.H * D.head_sz + (P.want_objective ? (size_t)(D.H + D.H / D.group) * D.ds * D.ds : 0);
@@ -584,8 +838,21 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
     const size_t solve_smem = (2 * (size_t)D.rs * (D.rs + 1) + (size_t)D.rs * D.ds + 64) * sizeof(float);
     dim3 pgrid(D.NB, D.H);
     const bool bf = P.dtype == LRQK_BF16;
+    const bool mma = bf && D.ds == kPfD && (D.rs == 16 || D.rs == 32 || D.rs == 64) && pf_mma_enabled();
     auto pass = [&](const void *X, int is_k, float *A, int update, int want_x2) {
-        if (bf) {
+        if (mma) {
+            const __nv_bfloat16 *Xb = reinterpret_cast<const __nv_bfloat16 *>(X);
+#define LRQK_PF_MMA(RSV)                                                                             \
+    do {                                                                                             \
+        auto fn = pf_pass_mma_kernel<RSV>;                                                           \
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pf_mma_smem<RSV>()); \
+        fn<<<pgrid, kPfThreads, pf_mma_smem<RSV>(), st>>>(D, Xb, is_k, A, A, update, want_x2, P.scratch); \
+    } while (0)
+            if (D.rs == 16) LRQK_PF_MMA(16);
+            else if (D.rs == 32) LRQK_PF_MMA(32);
+            else LRQK_PF_MMA(64);
+#undef LRQK_PF_MMA
+        } else if (bf) {
             auto fn = pf_pass_kernel<__nv_bfloat16>;
             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem);
             fn<<<pgrid, kPfThreads, pass_smem, st>>>(D, reinterpret_cast<const __nv_bfloat16 *>(X), is_k, A, A,

@@ -85,3 +85,25 @@ def test_prefill_monotone_objective_batched():
         aq, ak = np.random.default_rng(0).standard_normal((l, r)), None
         run = O.factorize(Q[h], K[h // G], rank=r, max_iter=10, tol=1e-30)
         np.testing.assert_allclose(obj[h], run.objective, rtol=2e-3)
+
+
+@pytest.mark.parametrize("r", [16, 32, 64])
+def test_prefill_tensor_core_pass_matches_fp32_path(r):
+    """bf16 storage takes the tensor-core pass (mma.sync, 3xBF16 split of the
+    fp32 factors); on bf16-exact inputs it must agree with the fp32 CUDA-core
+    pass to the split's accuracy."""
+    from paper_2510_23649_b200.engine import prefill_factorize_device
+
+    rng = np.random.default_rng(7)
+    H, G, l, d = 4, 2, 2000, 128
+    Q = torch.as_tensor(rng.standard_normal((H, l, d)), dtype=torch.float32).bfloat16().float().cuda()
+    K = torch.as_tensor(rng.standard_normal((H // G, l, d)), dtype=torch.float32).bfloat16().float().cuda()
+    a = prefill_factorize_device(Q, K, r, max_iter=2, tol=1e-30, want_objective=True, dtype="f32", group=G)
+    b = prefill_factorize_device(Q, K, r, max_iter=2, tol=1e-30, want_objective=True, dtype="bf16", group=G)
+    torch.cuda.synchronize()
+    for name in ("A_Q", "A_K", "B_Q", "B_K"):
+        x, y = a[name].float(), b[name].float()
+        err = (x - y).norm() / x.norm()
+        assert err < 2e-3, (name, float(err))
+    np.testing.assert_allclose(b["objective"].cpu().numpy(), a["objective"].cpu().numpy(), rtol=2e-3)
+    assert torch.equal(a["sweeps"], b["sweeps"])
