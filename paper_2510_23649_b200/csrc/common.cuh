@@ -44,6 +44,7 @@ enum Meta : int {
     M_STAT = 33,       // persistent: head-steps finalized per mode (33 + mode, modes 0..5; 39: exact fallbacks)
     M_BITS_FRESH = 40, // res_bits already holds res_idx (set by seed; prepare then skips the hit count)
     M_YG = 41,         // Y|G partial slots written by select_attend this step (0: cluster reduce does it)
+    M_YG_ADD = 42,     // bin-D winners (res_idx[M_NABOVE, +n)) whose Y|G the finish kernel adds
 };
 constexpr int kPrevCrit = 8;
 

@@ -906,7 +906,17 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
         }
         __syncthreads();
     }
-    if (tid == 0) meta[M_YG] = 0;
+    const int nadd = meta[M_YG_ADD];
+    if (nadd > 0) {  // the threshold-bin winners select_attend left to this kernel
+        __syncthreads();
+        yg_rows_small(L, reinterpret_cast<const __nv_bfloat16 *>(L.slow_k) +
+                             ((size_t)(bh / L.n_q_heads) * L.n_kv_heads + (bh % L.n_q_heads) / (L.n_q_heads / L.n_kv_heads)) *
+                                 L.t_max * d,
+                      reinterpret_cast<const __nv_bfloat16 *>(L.proxy) + (size_t)bh * L.t_max * R,
+                      L.res_idx + (size_t)bh * L.s_cap + meta[M_NABOVE], nadd, smem, YG);
+    }
+    __syncthreads();
+    if (tid == 0) { meta[M_YG] = 0; meta[M_YG_ADD] = 0; }
     const int ldB = d + 4, ldM = R + 4;
     const int RB = R / 4, NP = RB * (RB + 1) / 2;
     float *sBQ = smem;                   // [R][ldB]

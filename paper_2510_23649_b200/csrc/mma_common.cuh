@@ -42,7 +42,9 @@ LRQK_DEV void mma_reduce_tile(const uint8_t *kb_s, int ldk, const uint8_t *ab_s,
                               float (&yacc)[MT][NTW][4], float (&gacc)[4][4]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane >> 3, i8 = lane & 7;
-    const int GT = (R / 16) * (R / 8);
+    constexpr int RR = MT * 16;  // rank_stride (== R)
+    constexpr int GT = (RR / 16) * (RR / 8);
+    (void)R;
 #pragma unroll
     for (int ks = 0; ks < kMmaRows; ks += 16) {
         uint32_t af[MT][4];
@@ -64,7 +66,7 @@ LRQK_DEV void mma_reduce_tile(const uint8_t *kb_s, int ldk, const uint8_t *ab_s,
         for (int w2 = 0; w2 < 4; ++w2) {
             const int gtile = warp + 8 * w2;
             if (gtile >= GT) break;
-            const int mt = gtile / (R / 8), n0 = (gtile % (R / 8)) * 8;
+            const int mt = gtile / (RR / 8), n0 = (gtile % (RR / 8)) * 8;
             uint32_t bfr[2];
             const int k0 = ks + ((lane >> 3) & 1) * 8;
             ldsm_x2_trans(bfr, ab_s + (k0 + i8) * lda + n0 * 2);
@@ -100,6 +102,45 @@ LRQK_DEV void mma_write_partial(const float (&yacc)[MT][NTW][4], const float (&g
         *reinterpret_cast<float2 *>(gp) = make_float2(gacc[w2][0], gacc[w2][1]);
         *reinterpret_cast<float2 *>(gp + 8 * R) = make_float2(gacc[w2][2], gacc[w2][3]);
     }
+}
+
+// Y = A^T K and G = A^T A over n <= kMmaRows listed rows (bf16 storage), on
+// the CUDA cores, ADDED to dst[R*d | R*R]: the rows are staged as fp32 in
+// shared memory (stage >= kMmaRows * (d + R) floats), then each thread owns
+// (R*d + R*R) / blockDim.x outputs.
+template <typename T>
+__device__ void yg_rows_small(const lrqk_layer_t &L, const T *kb, const T *proxy, const int *rows, int n,
+                              float *stage, float *dst) {
+    const int d = L.dim_stride, R = L.rank_stride, ap = R * (int)sizeof(T) / 16;
+    constexpr int N = Pack<T>::N;
+    float *sK = stage, *sA = stage + (size_t)kMmaRows * d;
+    for (int e = threadIdx.x; e < n * (d / N + ap); e += blockDim.x) {
+        float f[N];
+        if (e < n * (d / N)) {
+            const int j = e / (d / N), pk = e - j * (d / N);
+            unpack16<T>(*reinterpret_cast<const uint4 *>(kb + (size_t)rows[j] * d + pk * N), f);
+#pragma unroll
+            for (int u = 0; u < N; ++u) sK[j * d + pk * N + u] = f[u];
+        } else {
+            const int e2 = e - n * (d / N), j = e2 / ap, pk = e2 - j * ap;
+            unpack16<T>(*reinterpret_cast<const uint4 *>(proxy + proxy_pack_offset(rows[j], pk, ap) * N), f);
+#pragma unroll
+            for (int u = 0; u < N; ++u) sA[j * R + pk * N + u] = f[u];
+        }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < R * d + R * R; o += blockDim.x) {
+        float acc = 0.f;
+        if (o < R * d) {
+            const int p = o / d, i = o - p * d;
+            for (int j = 0; j < n; ++j) acc = fmaf(sA[j * R + p], sK[j * d + i], acc);
+        } else {
+            const int o2 = o - R * d, p = o2 / R, q = o2 - p * R;
+            for (int j = 0; j < n; ++j) acc = fmaf(sA[j * R + p], sA[j * R + q], acc);
+        }
+        dst[o] += acc;
+    }
+    __syncthreads();
 }
 
 }  // namespace lrqk

@@ -43,12 +43,11 @@ struct FArgs {
 // Online softmax over the K/V rows listed in rows[0, n) (shared memory),
 // continuing (m, l, acc) of this lane group.  LPR lanes per row, PPL 16-byte
 // packs per lane; all lanes of a warp run the same trip count.
-template <typename T, int LPR, int PPL>
+template <typename T, int LPR, int PPL, int U = 8>
 __device__ void attend_list(const T *kb, const T *vb, const int *rows, int n, const float (&qv)[PPL][Pack<T>::N],
                             float c, int d, float &m, float &l, float (&acc)[PPL][Pack<T>::N]) {
     constexpr int N = Pack<T>::N;
     constexpr int RPW = 32 / LPR;
-    constexpr int U = 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int sub = lane / LPR, sl = lane - sub * LPR;
     const int step = nw * RPW;
@@ -133,27 +132,44 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
     const int sub = lane / LPR, sl = lane - sub * LPR;
     const int ng = nw * RPW, gidx = warp * RPW + sub;
     const int ldk = d * (int)sizeof(T) + 16, lda = R * 2 + 16;  // bytes (padded rows)
-    const int kp = d * (int)sizeof(T) / 16, ap = YG ? R * 2 / 16 : 0;
+    const int kp = d * (int)sizeof(T) / 16;
     const int tile_kv = kMmaRows * ldk, buf = 2 * tile_kv + (YG ? kMmaRows * lda : 0);
     const int nch = (n + kMmaRows - 1) / kMmaRows;
     auto issue = [&](int ch) {
         uint8_t *kS = stage + (ch & 1) * buf, *vS = kS + tile_kv, *aS = vS + tile_kv;
         const int r0 = ch * kMmaRows, nr = min(kMmaRows, n - r0);
-        const int tot = kMmaRows * (2 * kp + ap);
-        for (int e = tid; e < tot; e += blockDim.x) {
-            if (e < 2 * kMmaRows * kp) {
-                const int isv = e >= kMmaRows * kp;
-                const int e2 = e - isv * kMmaRows * kp;
-                const int j = e2 / kp, pk = e2 - j * kp;
-                uint8_t *dst = (isv ? vS : kS) + j * ldk + pk * 16;
-                if (j < nr) cp_async16(dst, (isv ? vb : kb) + (size_t)rows[r0 + j] * d + pk * (16 / sizeof(T)));
-                else *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
-            } else if (YG) {
-                const int e2 = e - 2 * kMmaRows * kp;
-                const int j = e2 / ap, pk = e2 - j * ap;
-                uint8_t *dst = aS + j * lda + pk * 16;
-                if (j < nr) cp_async16(dst, proxy + proxy_pack_offset(rows[r0 + j], pk, ap) * 8);
-                else *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
+        if constexpr (YG) {
+            // bf16, d = 128, R = 32: 16 packs per K/V row, 4 per proxy row (shifts only)
+            for (int e = tid; e < kMmaRows * 16; e += blockDim.x) {
+                const int j = e >> 4, pk = e & 15;
+                uint8_t *dk = kS + j * ldk + pk * 16, *dv = vS + j * ldk + pk * 16;
+                if (j < nr) {
+                    const size_t row = (size_t)rows[r0 + j] * 128 + pk * 8;
+                    cp_async16(dk, kb + row);
+                    cp_async16(dv, vb + row);
+                } else {
+                    *reinterpret_cast<uint4 *>(dk) = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(dv) = make_uint4(0, 0, 0, 0);
+                }
+            }
+            for (int e = tid; e < kMmaRows * 4; e += blockDim.x) {
+                const int j = e >> 2, pk = e & 3;
+                uint8_t *da = aS + j * lda + pk * 16;
+                if (j < nr) cp_async16(da, proxy + proxy_pack_offset(rows[r0 + j], pk, 4) * 8);
+                else *reinterpret_cast<uint4 *>(da) = make_uint4(0, 0, 0, 0);
+            }
+        } else {
+            for (int e = tid; e < kMmaRows * kp; e += blockDim.x) {
+                const int j = e / kp, pk = e - j * kp;
+                uint8_t *dk = kS + j * ldk + pk * 16, *dv = vS + j * ldk + pk * 16;
+                if (j < nr) {
+                    const size_t row = (size_t)rows[r0 + j] * d + pk * (16 / sizeof(T));
+                    cp_async16(dk, kb + row);
+                    cp_async16(dv, vb + row);
+                } else {
+                    *reinterpret_cast<uint4 *>(dk) = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(dv) = make_uint4(0, 0, 0, 0);
+                }
             }
         }
         cp_async_commit();
@@ -221,45 +237,6 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
         if constexpr (YG) mma_reduce_tile<2, 2>(kS, ldk, aS, lda, R, yacc, gacc);
         __syncthreads();
     }
-}
-
-// Y = A^T K and G = A^T A over n <= kMmaRows listed rows (bf16 storage), on
-// the CUDA cores: the rows are staged as fp32 in shared memory (stage >=
-// n * (d + R) floats), then each thread owns (R*d + R*R) / blockDim.x
-// outputs.  Writes the full partial (zeros for n == 0).
-template <typename T>
-__device__ void yg_rows_small(const lrqk_layer_t &L, const T *kb, const T *proxy, const int *rows, int n,
-                              float *stage, float *dst) {
-    const int d = L.dim_stride, R = L.rank_stride, ap = R * (int)sizeof(T) / 16;
-    constexpr int N = Pack<T>::N;
-    float *sK = stage, *sA = stage + (size_t)kMmaRows * d;
-    for (int e = threadIdx.x; e < n * (d / N + ap); e += blockDim.x) {
-        float f[N];
-        if (e < n * (d / N)) {
-            const int j = e / (d / N), pk = e - j * (d / N);
-            unpack16<T>(*reinterpret_cast<const uint4 *>(kb + (size_t)rows[j] * d + pk * N), f);
-#pragma unroll
-            for (int u = 0; u < N; ++u) sK[j * d + pk * N + u] = f[u];
-        } else {
-            const int e2 = e - n * (d / N), j = e2 / ap, pk = e2 - j * ap;
-            unpack16<T>(*reinterpret_cast<const uint4 *>(proxy + proxy_pack_offset(rows[j], pk, ap) * N), f);
-#pragma unroll
-            for (int u = 0; u < N; ++u) sA[j * R + pk * N + u] = f[u];
-        }
-    }
-    __syncthreads();
-    for (int o = threadIdx.x; o < R * d + R * R; o += blockDim.x) {
-        float acc = 0.f;
-        if (o < R * d) {
-            const int p = o / d, i = o - p * d;
-            for (int j = 0; j < n; ++j) acc = fmaf(sA[j * R + p], sK[j * d + i], acc);
-        } else {
-            const int o2 = o - R * d, p = o2 / R, q = o2 - p * R;
-            for (int j = 0; j < n; ++j) acc = fmaf(sA[j * R + p], sA[j * R + q], acc);
-        }
-        dst[o] = acc;
-    }
-    __syncthreads();
 }
 
 // Merge the lane groups' (m, l, acc) into one block partial: dst[0] = max,
@@ -522,9 +499,8 @@ select_attend_kernel(const FArgs a) {
         if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
     } else {
         // a handful of rows: attention from registers; Y, G on the CUDA cores
-        attend_list<T, LPR, PPL>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);
-        if constexpr (YG) yg_rows_small(L, kb, proxy, s_list, nwin, reinterpret_cast<float *>(stage),
-                                        yg + (size_t)P * PF);
+        attend_list<T, LPR, PPL, 1>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);  // compact code: few rows
+        // their Y, G contributions are added by the finish kernel (M_YG_ADD)
     }
     float *s_part = reinterpret_cast<float *>(stage) + (kFThreads / 32) * d;  // [d + 2]
     float *s_pml = s_part + d + 2;                                             // [2 * P]
@@ -566,7 +542,10 @@ select_attend_kernel(const FArgs a) {
         meta[M_CAND] = 0;
         meta[M_HINT] = (int)hint;
         meta[M_HINT_OK] = 1;
-        meta[M_YG] = YG ? P + 1 : 0;
+        // Y|G slots: the P parts (+ the large-bin path's slot P); the few
+        // bin-D winners of the common path are added by the finish kernel
+        meta[M_YG] = YG ? (nwin > kMmaRows ? P + 1 : P) : 0;
+        meta[M_YG_ADD] = YG && nwin <= kMmaRows ? nwin : 0;
         meta[M_STAT + 5] += 1;
     }
     uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;  // ready for the next step
