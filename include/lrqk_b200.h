@@ -163,9 +163,10 @@ int lrqk_select(const lrqk_layer_t *L, void *stream);
 
 /* Fused selection + attention for the heads whose score pass located the
  * k-th largest key in its threshold window (the common case, HBM policy):
- * writes Omega_t to res_idx and the attention row to out for those heads;
- * lrqk_select / lrqk_attention then skip them.  Launch it right after
- * lrqk_score.  ref: cache.py:149-171, attention.py:23-34. */
+ * writes Omega_t to res_idx and the attention's softmax partials for those
+ * heads; lrqk_select skips them and lrqk_attention only merges their
+ * partials into out.  Launch it right after lrqk_score, and lrqk_attention
+ * after it.  ref: cache.py:149-171, attention.py:23-34. */
 int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
 /* Host policy: copy this step's missed K/V rows from the pinned host slow

@@ -19,6 +19,45 @@ struct AttnArgs {
 // softmax over its rows; groups, warps and finally splits are merged with the
 // usual (max, sum, acc) rescaling.  The last split block of a head merges the
 // split partials and writes the output.
+// Output of a head whose selection ran in select_attend_kernel: its
+// parts + 1 partials (max, sum, acc[d]; log2 domain) merged by one block.
+__device__ void merge_select_attend_partials(const lrqk_layer_t &L, int bh, float *out) {
+    __shared__ float s_w[64], s_den, s_mx;
+    const int d = L.dim_stride;
+    const int np = L.sel_meta[(size_t)bh * kMetaInts + M_ATT_PARTS];
+    const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, np - 1) * (size_t)(d + 2);
+    if (threadIdx.x < 32) {
+        float mx = -INFINITY;
+        for (int p = threadIdx.x; p < np; p += 32) mx = fmaxf(mx, __ldcg(parts + (size_t)p * (d + 2)));
+        mx = warp_max(mx);
+        float den = 0.f;
+        for (int p = threadIdx.x; p < np; p += 32) {
+            const float pm = __ldcg(parts + (size_t)p * (d + 2));
+            const float w = pm == -INFINITY ? 0.f : exp2f(pm - mx);
+            if (p < 64) s_w[p] = w;
+            den = fmaf(__ldcg(parts + (size_t)p * (d + 2) + 1), w, den);
+        }
+        den = warp_sum(den);
+        if (threadIdx.x == 0) { s_den = den; s_mx = mx; }
+    }
+    __syncthreads();
+    const float inv = 1.f / s_den;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        float o = 0.f;
+        for (int p = 0; p < np; ++p) {
+            float w;
+            if (p < 64) {
+                w = s_w[p];
+            } else {
+                const float pm = __ldcg(parts + (size_t)p * (d + 2));
+                w = pm == -INFINITY ? 0.f : exp2f(pm - s_mx);
+            }
+            o = fmaf(__ldcg(parts + (size_t)p * (d + 2) + 2 + i), w, o);
+        }
+        out[(size_t)bh * d + i] = o * inv;
+    }
+}
+
 template <typename T, int LPR, int PPL>
 __global__ void __launch_bounds__(kAttnThreads)
 attention_kernel(const AttnArgs a) {
@@ -39,7 +78,11 @@ attention_kernel(const AttnArgs a) {
     trace(30);
     pdl_wait();
     pdl_trigger();
-    if (L.sel_meta[(size_t)bh * kMetaInts + M_MODE] == 5) return;  // done by select_attend_kernel
+    if (L.sel_meta[(size_t)bh * kMetaInts + M_MODE] == 5) {
+        // select_attend_kernel left parts + 1 softmax partials: merge them
+        if (split == 0) merge_select_attend_partials(L, bh, a.out);
+        return;
+    }
     const int S = L.res_cnt[bh];
     const bool host = L.policy == LRQK_SLOW_HOST;
     const T *kb, *vb;
@@ -200,7 +243,7 @@ attention_kernel(const AttnArgs a) {
 
 int attn_splits(const lrqk_layer_t &L) { return (L.s_cap + kAttnRows - 1) / kAttnRows; }
 int score_tma_parts(const lrqk_layer_t &L);
-int attn_scratch_slots(const lrqk_layer_t &L) { return max(attn_splits(L), score_tma_parts(L)); }
+int attn_scratch_slots(const lrqk_layer_t &L) { return max(attn_splits(L), score_tma_parts(L) + 1); }
 
 template <typename T>
 static int launch_attention_t(const AttnArgs &a, cudaStream_t st) {

@@ -45,13 +45,16 @@ enum Meta : int {
     M_BITS_FRESH = 40, // res_bits already holds res_idx (set by seed; prepare then skips the hit count)
     M_YG = 41,         // Y|G partial slots written by select_attend this step (0: cluster reduce does it)
     M_YG_ADD = 42,     // bin-D winners (res_idx[M_NABOVE, +n)) whose Y|G the finish kernel adds
+    M_ATT_PARTS = 43,  // softmax partials select_attend left for attention_kernel to merge (parts + 1)
 };
 constexpr int kPrevCrit = 8;
 
 // attention partial slots per head (attention splits, or select_attend parts)
+// attention partial slots per head: attention splits, or select_attend's
+// parts plus its last block
 LRQK_DEV int attn_slots_dev(const lrqk_layer_t &L, int parts) {
     const int splits = (L.s_cap + kAttnRows - 1) / kAttnRows;
-    return splits > parts ? splits : parts;
+    return splits > parts + 1 ? splits : parts + 1;
 }
 
 // compress_prepare reductions, per head: `yg_slots` partials of

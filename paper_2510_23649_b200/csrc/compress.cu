@@ -835,12 +835,11 @@ constexpr int kPcBufs = 4;  // gather buffers per CTA (kPcBufs - 1 sub-chunks in
 
 __host__ __device__ inline size_t pc_part_floats(int R, int d) { return (size_t)R * d + (size_t)R * R; }
 
-__device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L, int yg_slots) {
+__device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L, int yg_slots, int bh) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     extern __shared__ __align__(16) float smem[];
     const int crank = (int)cluster.block_rank();
-    const int bh = blockIdx.y;
     const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
     const int G = L.n_q_heads / L.n_kv_heads, g = h / G;
     const int d = L.dim_stride, R = L.rank_stride;
@@ -985,12 +984,23 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
 // blockIdx.z): every layer's precompute is only needed by its next step, so
 // the engine runs all layers' compress_prepare together at the end of a step
 __global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
-prepare_reduce_cluster_kernel(const lrqk_layer_t L, int yg_slots) { prepare_reduce_body(L, yg_slots); }
+prepare_reduce_cluster_kernel(const lrqk_layer_t L, int yg_slots) { prepare_reduce_body(L, yg_slots, blockIdx.y); }
 __global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
-prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) { prepare_reduce_body(Ls[blockIdx.z], yg_slots); }
+prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls, int n_layers, int yg_slots) {
+    // persistent clusters over (layer, head): heads that select_attend
+    // already reduced (the common case) are skipped with one meta read
+    const int BH = Ls[0].batch * Ls[0].n_q_heads;
+    for (int item = blockIdx.y; item < n_layers * BH; item += gridDim.y) {
+        const lrqk_layer_t &L = Ls[item / BH];
+        const int bh = item % BH;
+        if (__ldcg(L.sel_meta + (size_t)bh * kMetaInts + M_YG) > 0) continue;  // uniform over the cluster
+        prepare_reduce_body(L, yg_slots, bh);
+        __syncthreads();
+    }
+}
 __global__ void __launch_bounds__(kCompressThreads)
 prepare_finish_kernel(const lrqk_layer_t L, int yg_slots) { prepare_finish_body(L, yg_slots); }
-__global__ void __launch_bounds__(kCompressThreads)
+__global__ void __launch_bounds__(kCompressThreads, 4)
 prepare_finish_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) { prepare_finish_body(Ls[blockIdx.z], yg_slots); }
 
 static bool pc_enabled() {
@@ -1392,6 +1402,7 @@ static size_t compress_smem_bytes(const lrqk_layer_t &L) {
 
 int launch_prepare(const lrqk_layer_t &L, cudaStream_t st);
 int yg_slots(const lrqk_layer_t &L);
+int num_sms();
 int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *host_layers, int n_layers,
                           cudaStream_t st) {
     const lrqk_layer_t &L = host_layers[0];
@@ -1399,8 +1410,10 @@ int launch_prepare_layers(const lrqk_layer_t *dev_layers, const lrqk_layer_t *ho
         const size_t s1 = prepare_reduce_smem_bytes(L), s2 = prepare_finish_smem_bytes(L);
         cudaFuncSetAttribute(prepare_reduce_cluster_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
         cudaFuncSetAttribute(prepare_finish_layers_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-        prepare_reduce_cluster_layers_kernel<<<dim3(kPcCtas, L.batch * L.n_q_heads, n_layers), kCompressThreads, s1,
-                                               st>>>(dev_layers, yg_slots(L));
+        const int n_items = L.batch * L.n_q_heads * n_layers;
+        const int clusters = std::max(1, std::min(n_items, num_sms() * 2 / kPcCtas));
+        prepare_reduce_cluster_layers_kernel<<<dim3(kPcCtas, clusters), kCompressThreads, s1, st>>>(
+            dev_layers, n_layers, yg_slots(L));
         prepare_finish_layers_kernel<<<dim3(L.batch * L.n_q_heads, 1, n_layers), kCompressThreads, s2, st>>>(
             dev_layers, yg_slots(L));
         return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;

@@ -429,7 +429,6 @@ select_attend_kernel(const FArgs a) {
     const int n_crit = __ldcg(meta + M_CAND);
     const int lane_ = tid & 31, warp_ = tid >> 5;
     const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && n_crit <= kCritCap;
-    const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, P) * (size_t)(d + 2);
     int *s_list = s_rows;  // the winners of bin D
     uint32_t hint = klo + ((uint32_t)(D + 1) << kWinShift);
     int nwin = 0;
@@ -502,40 +501,10 @@ select_attend_kernel(const FArgs a) {
         attend_list<T, LPR, PPL, 1>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);  // compact code: few rows
         // their Y, G contributions are added by the finish kernel (M_YG_ADD)
     }
-    float *s_part = reinterpret_cast<float *>(stage) + (kFThreads / 32) * d;  // [d + 2]
-    float *s_pml = s_part + d + 2;                                             // [2 * P]
-    block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, s_part);
+    // this block's partial goes to slot P; attention_kernel merges the P + 1
+    block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc,
+                               L.attn_scratch + ((size_t)bh * attn_slots_dev(L, P) + P) * (size_t)(d + 2));
     trace(58);
-    for (int p = tid; p < P; p += blockDim.x) {
-        s_pml[2 * p] = __ldcg(parts + (size_t)p * (d + 2));
-        s_pml[2 * p + 1] = __ldcg(parts + (size_t)p * (d + 2) + 1);
-    }
-    __syncthreads();
-    // merge the P part partials with this block's (the lite rows, in the last
-    // part, are never empty, so the maximum is finite)
-    float MM = s_part[0];
-    for (int p = 0; p < P; ++p) MM = fmaxf(MM, s_pml[2 * p]);
-    const float w0 = s_part[0] == -INFINITY ? 0.f : exp2f(s_part[0] - MM);
-    float den = s_part[1] * w0;
-    for (int p = 0; p < P; ++p)
-        if (s_pml[2 * p] != -INFINITY) den = fmaf(s_pml[2 * p + 1], exp2f(s_pml[2 * p] - MM), den);
-    const float inv = 1.f / den;
-    for (int i = tid; i < d; i += blockDim.x) {
-        float o0 = s_part[2 + i] * w0, o1 = 0.f;
-        int p = 0;
-        for (; p + 1 < P; p += 2) {
-            const float a0 = __ldcg(parts + (size_t)p * (d + 2) + 2 + i);
-            const float a1 = __ldcg(parts + (size_t)(p + 1) * (d + 2) + 2 + i);
-            const float m0 = s_pml[2 * p], m1 = s_pml[2 * p + 2];
-            o0 = fmaf(a0, m0 == -INFINITY ? 0.f : exp2f(m0 - MM), o0);
-            o1 = fmaf(a1, m1 == -INFINITY ? 0.f : exp2f(m1 - MM), o1);
-        }
-        if (p < P) {
-            const float m0 = s_pml[2 * p];
-            o0 = fmaf(__ldcg(parts + (size_t)p * (d + 2) + 2 + i), m0 == -INFINITY ? 0.f : exp2f(m0 - MM), o0);
-        }
-        a.out[(size_t)bh * d + i] = (o0 + o1) * inv;
-    }
     trace(60);
     if (tid == 0) {
         L.res_cnt[bh] = k_eff + (t + 1 - lite_start);
@@ -546,6 +515,7 @@ select_attend_kernel(const FArgs a) {
         // bin-D winners of the common path are added by the finish kernel
         meta[M_YG] = YG ? (nwin > kMmaRows ? P + 1 : P) : 0;
         meta[M_YG_ADD] = YG && nwin <= kMmaRows ? nwin : 0;
+        meta[M_ATT_PARTS] = P + 1;
         meta[M_STAT + 5] += 1;
     }
     uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;  // ready for the next step
