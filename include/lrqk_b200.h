@@ -113,6 +113,9 @@ typedef struct lrqk_layer {
 
     /* ---- persistent residency bitmap (HBM policy hit/miss accounting) ---- */
     uint32_t *res_bits;            /* [B,Hq,ceil(t_max/32)] bit x set <=> x in the fast tier      */
+
+    /* ---- per-step scratch: rows whose score key clears the candidate bound ---- */
+    uint32_t *cmask;               /* [B,Hq,ceil(t_max/32)] one bit per row (lrqk_score)          */
 } lrqk_layer_t;
 
 /* Sizes (bytes) of every buffer in lrqk_layer_t for the given configuration,

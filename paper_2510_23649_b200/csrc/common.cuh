@@ -46,6 +46,7 @@ enum Meta : int {
     M_YG = 41,         // Y|G partial slots written by select_attend this step (0: cluster reduce does it)
     M_YG_ADD = 42,     // bin-D winners (res_idx[M_NABOVE, +n)) whose Y|G the finish kernel adds
     M_ATT_PARTS = 43,  // softmax partials select_attend left for attention_kernel to merge (parts + 1)
+    M_KC = 44,         // this step's candidate bound (key) of cmask; 0xFFFFFFFF: no mask
 };
 constexpr int kPrevCrit = 8;
 

@@ -271,12 +271,14 @@ score_tma_kernel(const ScoreArgs a) {
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     // hint window (persistent meta written by the previous step's select)
     const bool win = meta[M_HINT_OK] != 0;
-    uint32_t klo = 0;
+    uint32_t klo = 0, kc = 0xFFFFFFFFu;
     if (win) {
         const uint32_t hk = (uint32_t)meta[M_HINT];
         klo = hk > kWinKeys / 2 ? hk - kWinKeys / 2 : 0u;
         if (klo > 0xFFFFFFFFu - (kWinKeys - 1)) klo = 0xFFFFFFFFu - (kWinKeys - 1);
+        kc = max(klo, hk > kCandBelow ? hk - kCandBelow : 0u);
     }
+    uint32_t *cmask = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5);
     for (int i = tid; i < kHistBins; i += blockDim.x) { s_hist[i] = 0; s_win[i] = 0; }
     if (tid == 0) {
         s_above = 0;
@@ -335,6 +337,10 @@ score_tma_kernel(const ScoreArgs a) {
                 const int row = tile * 32 + lane;
                 const uint32_t key = score_key(s0 + s1);
                 if (row < n) st_hint_u32(keys + row, key, pol_keys);
+                {   // candidate bit per row (the fused selection's shortlist)
+                    const uint32_t cm = __ballot_sync(0xffffffffu, win && row < lite_start && key >= kc);
+                    if (lane == 0) st_hint_u32(cmask + tile, cm, pol_keys);
+                }
                 if (row < lite_start) {
                     // the sampled coarse histogram only serves the no-hint path
                     if (!win && (tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
@@ -416,10 +422,11 @@ score_tma_kernel(const ScoreArgs a) {
                 const int off = block_exclusive_scan(c, s_scan, &tot);
                 if (tid < P) L.fcnt[(size_t)bh * P + tid] = off;
                 // inconsistent counts, or a threshold bin too large to sort: scan path
-                if (tot != nabove || s_win[D] > kCritCap) mode = 3;
+                if (tot != nabove || s_win[D] > kFCrit) mode = 3;
             }
             if (tid == 0) {
                 meta[M_KLO] = (int)klo;
+                meta[M_KC] = (int)kc;
                 meta[M_FBIN] = D;
                 meta[M_NABOVE] = nabove;
                 meta[M_SPARTS] = P;

@@ -309,6 +309,8 @@ select_attend_kernel(const FArgs a) {
     __shared__ float s_m[kFThreads / 32], s_l[kFThreads / 32];
     __shared__ int s_scan[32];
     __shared__ int s_flag;
+    __shared__ int s_ncrit, s_cbase;
+    __shared__ uint64_t s_crit[kFCrit];
     const int P = a.parts;
     const int bh = blockIdx.x / P, part = blockIdx.x - bh * P;
     const int b = bh / L.n_q_heads, h = bh - b * L.n_q_heads;
@@ -368,7 +370,74 @@ select_attend_kernel(const FArgs a) {
 
     // ---- this part's winners: ordered write, then attention (+ Y, G) -------
     int nloc = 0;
-    for (int base = row0; base < row1; base += kFRows) {
+    if (tid == 0) s_ncrit = 0;
+    __syncthreads();
+    // Shortlist path: when this step's threshold bin lies above the score
+    // kernel's candidate bound, only the rows marked in cmask can win; read
+    // their keys instead of the part's whole key range.
+    const uint32_t kc = (uint32_t)meta[M_KC];
+    const int w0 = row0 >> 5, w1 = (row1 + 31) >> 5, nwrd = w1 - w0;
+    bool shortlist = kc != 0xFFFFFFFFu && klo + ((uint32_t)D << kWinShift) >= kc && nwrd <= 4 * (int)blockDim.x;
+    if (shortlist) {
+        const uint32_t *cmw = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5) + w0;
+        const int wpt = (nwrd + blockDim.x - 1) / blockDim.x;  // <= 4 contiguous words per thread
+        uint32_t wv[4];
+        int cnt = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int wi = tid * wpt + u;
+            wv[u] = (u < wpt && wi < nwrd) ? __ldcg(cmw + wi) : 0u;
+            cnt += __popc(wv[u]);
+        }
+        int *s_c = reinterpret_cast<int *>(stage) + tid * 16;  // this thread's next candidates
+        int wu = 0;
+        uint32_t rem = wv[0];
+        const int rounds = (__reduce_max_sync(0xffffffffu, cnt) + 15) >> 4;
+        __shared__ int s_rounds;
+        if (tid == 0) s_rounds = 0;
+        __syncthreads();
+        if ((tid & 31) == 0) atomicMax(&s_rounds, rounds);
+        __syncthreads();
+        // one round keeps the output order (thread, bit); denser shortlists
+        // take the full key scan below
+        shortlist = s_rounds <= 1;
+        for (int rd = 0; rd < (shortlist ? s_rounds : 0); ++rd) {
+            int nc = 0;
+            while (nc < 16 && wu < 4) {  // next candidates, ascending
+                if (rem == 0u) { if (++wu < 4) rem = wv[wu]; continue; }
+                const int bpos = __ffs(rem) - 1;
+                rem &= rem - 1u;
+                s_c[nc++] = (w0 + tid * wpt + wu) * 32 + bpos;
+            }
+            uint32_t kk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) kk[j] = j < nc ? __ldcg(keys + s_c[j]) : 0u;
+            uint32_t wmask = 0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if (j >= nc || kk[j] < klo) continue;
+                const uint32_t dk = kk[j] - klo;
+                if (dk >= kWinKeys || (int)(dk >> kWinShift) > D) {
+                    wmask |= 1u << j;
+                } else if ((int)(dk >> kWinShift) == D) {
+                    const int q = atomicAdd(&s_ncrit, 1);
+                    if (q < kFCrit) s_crit[q] = make_comp(kk[j], s_c[j]);
+                }
+            }
+            int tot;
+            int o = nloc + block_exclusive_scan(__popc(wmask), s_scan, &tot);
+            while (wmask) {
+                const int j = __ffs(wmask) - 1;
+                wmask &= wmask - 1u;
+                const int x = s_c[j];
+                if (o < L.s_cap) s_rows[o] = x;
+                if (out + o < k_eff) dst[out + o] = x;
+                ++o;
+            }
+            nloc += tot;
+        }
+    }
+    for (int base = row0; base < row1 && !shortlist; base += kFRows) {
         uint4 kv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -386,9 +455,9 @@ select_attend_kernel(const FArgs a) {
                     const uint32_t dk = kk[e] - klo;
                     if (dk >= kWinKeys || (int)(dk >> kWinShift) > D) {
                         smask |= 1u << (u * 4 + e);
-                    } else if ((int)(dk >> kWinShift) == D) {
-                        const int q = atomicAdd(meta + M_CAND, 1);
-                        if (q < L.cand_cap) cand[q] = make_comp(kk[e], i);
+                    } else if ((int)(dk >> kWinShift) == D) {  // threshold bin: block list first
+                        const int q = atomicAdd(&s_ncrit, 1);
+                        if (q < kFCrit) s_crit[q] = make_comp(kk[e], i);
                     }
                 }
             }
@@ -405,6 +474,14 @@ select_attend_kernel(const FArgs a) {
         }
         nloc += tot;
     }
+    {   // this part's threshold-bin rows -> the head's list (one reservation)
+        __syncthreads();
+        const int nc = s_ncrit;
+        if (tid == 0) s_cbase = nc ? atomicAdd(meta + M_CAND, min(nc, kFCrit)) : 0;
+        __syncthreads();
+        for (int j = tid; j < min(nc, kFCrit); j += blockDim.x)
+            if (s_cbase + j < L.cand_cap) cand[s_cbase + j] = s_crit[j];
+    }
     const int nl = t + 1 - lite_start;
     if (part == P - 1) {  // Omega_l = the lite window, attended by the last part
         for (int i = tid; i < nl; i += blockDim.x) {
@@ -414,10 +491,12 @@ select_attend_kernel(const FArgs a) {
         nloc += nl;
     }
     __syncthreads();
+    trace(56);
     attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc, stage, yacc,
                                         gacc);
     trace(52);
     if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)part * PF);
+    trace(57);
     float *s_acc = reinterpret_cast<float *>(stage);  // [nwarps][d]
     float *part_dst = L.attn_scratch + ((size_t)bh * attn_slots_dev(L, P) + part) * (size_t)(d + 2);
     block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, part_dst);

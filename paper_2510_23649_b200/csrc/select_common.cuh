@@ -19,6 +19,12 @@ constexpr uint32_t kIdxMax = (1u << kIdxBits) - 1u;
 constexpr uint32_t kWinKeys = 1u << 25;
 constexpr int kWinShift = 14;
 constexpr int kCritCap = 4096;  // critical bin sorted in shared memory (larger -> exact fallback)
+constexpr int kFCrit = 256;     // threshold-bin rows of the fused path (more -> the general select path)
+// Candidate bound of the fused path: the score kernel marks (cmask) every
+// row whose key is at least hint - kCandBelow (half an octave of |score|
+// under the previous threshold); when this step's threshold bin starts at
+// or above that bound, the selection only needs the marked rows' keys.
+constexpr uint32_t kCandBelow = 1u << 22;
 
 LRQK_DEV uint64_t make_comp(uint32_t key, int idx) {
     return ((uint64_t)key << kIdxBits) | (uint64_t)(kIdxMax - (uint32_t)idx);

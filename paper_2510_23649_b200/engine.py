@@ -34,7 +34,7 @@ from .errors import NonFiniteError, SolveFailedError
 # compress_prepare reduction (all layers' precompute runs in one launch) are
 # per layer
 SHARED_SCRATCH = ("q_hat", "k_hat", "eta", "keys", "hist", "sure_idx", "cand", "attn_scratch", "counters",
-                  "miss_idx", "miss_slot", "miss_cnt", "status", "fcand", "fcnt")
+                  "miss_idx", "miss_slot", "miss_cnt", "status", "fcand", "fcnt", "cmask")
 
 
 def pow2_at_least(x: int, lo: int = 8) -> int:
