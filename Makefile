@@ -6,20 +6,34 @@ PKG := paper_2510_23649_b200
 SRC := $(wildcard $(PKG)/csrc/*.cu)
 OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
 LIB := $(PKG)/liblrqk_b200.so
+# development build with the per-block timeline trace compiled in
+# (tools/step_timeline.py loads it through LRQK_LIB_PATH)
+TOBJ := $(patsubst $(PKG)/csrc/%.cu,build/trace/%.o,$(SRC))
+TLIB := $(PKG)/liblrqk_b200_trace.so
+HDRS := $(PKG)/csrc/common.cuh $(PKG)/csrc/select_common.cuh $(PKG)/csrc/mma_common.cuh include/lrqk_b200.h
 
 all: $(LIB)
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/common.cuh $(PKG)/csrc/select_common.cuh $(PKG)/csrc/mma_common.cuh include/lrqk_b200.h
+build/%.o: $(PKG)/csrc/%.cu $(HDRS)
 	@mkdir -p build
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+	$(NVCC) $(NVFLAGS) -DLRQK_NO_TRACE -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+build/trace/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build/trace
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/trace/$*.ptxas.log || (cat build/trace/$*.ptxas.log; false)
 
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -rdc=true -shared -o $@ $(OBJ) -lcudart_static -lrt -ldl -lpthread
+
+$(TLIB): $(TOBJ)
+	$(NVCC) $(ARCH) -rdc=true -shared -o $@ $(TOBJ) -lcudart_static -lrt -ldl -lpthread
+
+trace: $(TLIB)
 
 sass: $(LIB)
 	cuobjdump -sass $(LIB) > build/lrqk.sass
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(TLIB)
 
-.PHONY: all clean sass
+.PHONY: all trace clean sass

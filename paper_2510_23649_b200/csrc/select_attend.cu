@@ -323,17 +323,22 @@ select_attend_kernel(const FArgs a) {
     pdl_trigger();
     const int t = L.ctx_len[b];
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
-    // prefetch this part's first 32 keys per thread (the score kernel's
+    // prefetch this part's candidate-mask words (the score kernel's
     // partition) and the query row together with the meta loads
     const int lite_start = max(0, t + 1 - L.lite_budget);
     const int tpp = (((t + 1 + 31) >> 5) + P - 1) / P;
     const int row0 = min(lite_start, part * tpp * 32), row1 = min(lite_start, (part + 1) * tpp * 32);
     const uint32_t *keys = L.keys + (size_t)bh * L.t_max;
-    uint4 pf[8];
+    const int w0 = row0 >> 5, w1 = (row1 + 31) >> 5, nwrd = w1 - w0;
+    const int wpt = (nwrd + blockDim.x - 1) / blockDim.x;  // contiguous mask words per thread
+    uint32_t wv[4];
+    {
+        const uint32_t *cmw = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5) + w0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const int i = row0 + tid * 32 + u * 4;
-        pf[u] = i < row1 ? *reinterpret_cast<const uint4 *>(keys + i) : make_uint4(0, 0, 0, 0);
+        for (int u = 0; u < 4; ++u) {
+            const int wi = tid * wpt + u;
+            wv[u] = (u < wpt && wi < nwrd) ? __ldcg(cmw + wi) : 0u;
+        }
     }
     float qv[PPL][N];
     {
@@ -376,32 +381,19 @@ select_attend_kernel(const FArgs a) {
     // kernel's candidate bound, only the rows marked in cmask can win; read
     // their keys instead of the part's whole key range.
     const uint32_t kc = (uint32_t)meta[M_KC];
-    const int w0 = row0 >> 5, w1 = (row1 + 31) >> 5, nwrd = w1 - w0;
-    bool shortlist = kc != 0xFFFFFFFFu && klo + ((uint32_t)D << kWinShift) >= kc && nwrd <= 4 * (int)blockDim.x;
+    bool shortlist = kc != 0xFFFFFFFFu && klo + ((uint32_t)D << kWinShift) >= kc && wpt <= 4;
     if (shortlist) {
-        const uint32_t *cmw = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5) + w0;
-        const int wpt = (nwrd + blockDim.x - 1) / blockDim.x;  // <= 4 contiguous words per thread
-        uint32_t wv[4];
         int cnt = 0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int wi = tid * wpt + u;
-            wv[u] = (u < wpt && wi < nwrd) ? __ldcg(cmw + wi) : 0u;
-            cnt += __popc(wv[u]);
-        }
-        int *s_c = reinterpret_cast<int *>(stage) + tid * 16;  // this thread's next candidates
+        for (int u = 0; u < 4; ++u) cnt += __popc(wv[u]);
+        int *s_c = reinterpret_cast<int *>(stage) + tid * 16;  // this thread's candidates
         int wu = 0;
         uint32_t rem = wv[0];
-        const int rounds = (__reduce_max_sync(0xffffffffu, cnt) + 15) >> 4;
-        __shared__ int s_rounds;
-        if (tid == 0) s_rounds = 0;
-        __syncthreads();
-        if ((tid & 31) == 0) atomicMax(&s_rounds, rounds);
-        __syncthreads();
-        // one round keeps the output order (thread, bit); denser shortlists
-        // take the full key scan below
-        shortlist = s_rounds <= 1;
-        for (int rd = 0; rd < (shortlist ? s_rounds : 0); ++rd) {
+        // one round of <= 16 candidates per thread keeps the output order
+        // (thread, bit); denser shortlists take the full key scan below
+        shortlist = !__syncthreads_or(cnt > 16);
+        trace(46);
+        if (shortlist) {
             int nc = 0;
             while (nc < 16 && wu < 4) {  // next candidates, ascending
                 if (rem == 0u) { if (++wu < 4) rem = wv[wu]; continue; }
@@ -409,6 +401,7 @@ select_attend_kernel(const FArgs a) {
                 rem &= rem - 1u;
                 s_c[nc++] = (w0 + tid * wpt + wu) * 32 + bpos;
             }
+            trace(47);
             uint32_t kk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) kk[j] = j < nc ? __ldcg(keys + s_c[j]) : 0u;
@@ -424,8 +417,10 @@ select_attend_kernel(const FArgs a) {
                     if (q < kFCrit) s_crit[q] = make_comp(kk[j], s_c[j]);
                 }
             }
+            trace(48);
             int tot;
             int o = nloc + block_exclusive_scan(__popc(wmask), s_scan, &tot);
+            trace(49);
             while (wmask) {
                 const int j = __ffs(wmask) - 1;
                 wmask &= wmask - 1u;
@@ -442,7 +437,7 @@ select_attend_kernel(const FArgs a) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = base + tid * 32 + u * 4;
-            kv[u] = base == row0 ? pf[u] : (i < row1 ? *reinterpret_cast<const uint4 *>(keys + i) : make_uint4(0, 0, 0, 0));
+            kv[u] = i < row1 ? *reinterpret_cast<const uint4 *>(keys + i) : make_uint4(0, 0, 0, 0);
         }
         uint32_t smask = 0;
 #pragma unroll
@@ -474,6 +469,7 @@ select_attend_kernel(const FArgs a) {
         }
         nloc += tot;
     }
+    trace(44);
     {   // this part's threshold-bin rows -> the head's list (one reservation)
         __syncthreads();
         const int nc = s_ncrit;
@@ -482,6 +478,7 @@ select_attend_kernel(const FArgs a) {
         for (int j = tid; j < min(nc, kFCrit); j += blockDim.x)
             if (s_cbase + j < L.cand_cap) cand[s_cbase + j] = s_crit[j];
     }
+    trace(45);
     const int nl = t + 1 - lite_start;
     if (part == P - 1) {  // Omega_l = the lite window, attended by the last part
         for (int i = tid; i < nl; i += blockDim.x) {
