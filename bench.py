@@ -47,6 +47,16 @@ WORKLOADS = {
 }
 
 
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum of the score kernel from the
+    committed ncu --set full capture (profiles/roofline_traffic.json), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")) as f:
+            return int(json.load(f)["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -372,7 +382,7 @@ def run_ours(args, world, rank, local):
                     l2="no flush: each step streams %.1f GB (> 126 MB L2)" % (byt["total"] * L / 1e9)),
         roofline=dict(bound="hbm", kernel="score_kernel (proxy scores + radix histogram)",
                       achieved=round(score_gbs, 1), peak=hbm_peak, unit="GB/s",
-                      frac=round(score_gbs / hbm_peak, 4), traffic=None,
+                      frac=round(score_gbs / hbm_peak, 4), traffic=_ncu_traffic(),
                       algorithmic_bytes_per_launch=score_bytes, avg_launch_ms=round(score_ms, 5),
                       step_frac_of_hbm=round(step_gbs / hbm_peak, 4), step_algorithmic_GBps=round(step_gbs, 1),
                       peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"),

@@ -5,7 +5,7 @@
 # Usage (from the repo root, on the GPU box): bash tools/gpu_round.sh TAG
 tag=${1:-r1}
 mkdir -p gpurun_out
-make -j8 >/dev/null 2>&1
+make -j8 all trace >/dev/null 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu_$tag.txt 2>&1
 lscpu | head -20 >> gpurun_out/gpu_$tag.txt
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$tag.log
@@ -18,3 +18,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:^sco
   python bench.py --profile-steps 6 > gpurun_out/ncu_full_$tag.log 2>&1; echo "ncu full exit $?" >> gpurun_out/ncu_full_$tag.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:^select_attend -s 160 -c 1 -o gpurun_out/sa_$tag \
   python bench.py --profile-steps 6 > gpurun_out/ncu_full_sa_$tag.log 2>&1
+timeout 300 python tools/step_timeline.py > gpurun_out/timeline_$tag.txt 2>&1
