@@ -273,6 +273,58 @@ __device__ void gram_rows(const float *X, int r, int d, int ldx, float *out, int
     __syncthreads();
 }
 
+// The two grams X0 X0^T and X1 X1^T in one pass (one barrier pair, twice the
+// threads busy); tmp holds 4 * NP * 16 floats.
+__device__ void gram_rows2(const float *X0, const float *X1, int r, int d, int ldx, float *out0, float *out1, int ldo,
+                           float *tmp) {
+    const int RB = (r + 3) / 4;
+    const int NP = RB * (RB + 1) / 2;
+    const int halves = (4 * NP <= (int)blockDim.x) ? 2 : 1;
+    const int dh = d / halves;
+    for (int w = threadIdx.x; w < 2 * NP * halves; w += blockDim.x) {
+        const int mat = w / (NP * halves), w2 = w - mat * NP * halves;
+        const int pair = w2 % NP, hf = w2 / NP;
+        const float *X = mat ? X1 : X0;
+        int pb = 0, rem = pair;
+        while (rem >= RB - pb) { rem -= RB - pb; ++pb; }
+        const int qb = pb + rem;
+        float acc[16] = {};
+        const int i0 = hf * dh, i1 = i0 + dh;
+#pragma unroll 4
+        for (int i = i0; i < i1; ++i) {
+            float xp[4], xq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                xp[u] = (pb * 4 + u < r) ? X[(pb * 4 + u) * ldx + i] : 0.f;
+                xq[u] = (qb * 4 + u < r) ? X[(qb * 4 + u) * ldx + i] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u * 4 + v] = fmaf(xp[u], xq[v], acc[u * 4 + v]);
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) tmp[((mat * halves + hf) * NP + pair) * 16 + e] = acc[e];
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < 2 * NP * 16; w += blockDim.x) {
+        const int mat = w / (NP * 16), w2 = w - mat * NP * 16;
+        const int pair = w2 / 16, uv = w2 - pair * 16;
+        int pb = 0, rem = pair;
+        while (rem >= RB - pb) { rem -= RB - pb; ++pb; }
+        const int qb = pb + rem;
+        const int p = pb * 4 + uv / 4, q = qb * 4 + (uv & 3);
+        float sv = tmp[(mat * halves * NP + pair) * 16 + uv];
+        if (halves == 2) sv += tmp[((mat * 2 + 1) * NP + pair) * 16 + uv];
+        float *out = mat ? out1 : out0;
+        if (p < r && q < r && (pb < qb || p <= q)) {
+            out[p * ldo + q] = sv;
+            out[q * ldo + p] = sv;
+        }
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------
 // K2p reduce on tensor cores (bf16 storage): per 64-row sub-chunk of Omega,
 //     Y += A_sub^T K_sub   (M = r, N = d, K = 64)      G += A_sub^T A_sub
@@ -784,12 +836,18 @@ prepare_kernel(const lrqk_layer_t L) {
 // staged in shared memory (row stride ldB): resid = x_hat B - x,
 // eta = (resid . s) / (s . s) with s = |x_hat|^2 resid (0 under the
 // reference's floor), B -= eta x_hat^T resid.  X = [q | k | q_hat | k_hat].
-// Writes the updated rows back to B_Q / B_K and eta.  scratch: 2 * d floats.
+// Writes the updated rows back to B_Q / B_K and eta.  scratch: 4 * d + 2 * R floats.
 __device__ void apply_deferred_b_update(const lrqk_layer_t &L, int bh, const float *X, float *sBQ, float *sBK,
                                         int ldB, float *scratch, float *s_red) {
     const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     float *resid = scratch;  // [2][d]
+    {   // X to shared memory once: the loops below read it repeatedly
+        float *xs = scratch + 2 * d;
+        for (int i = tid; i < 2 * d + 2 * R; i += blockDim.x) xs[i] = __ldcg(X + i);
+        __syncthreads();
+        X = xs;
+    }
     for (int w = tid; w < 2 * d; w += blockDim.x) {
         const int side = w / d, i = w - side * d;
         const float *xh = X + 2 * d + side * R;
@@ -797,18 +855,18 @@ __device__ void apply_deferred_b_update(const lrqk_layer_t &L, int bh, const flo
         float a0 = 0.f, a1 = 0.f;
         int p = 0;
         for (; p + 1 < r; p += 2) {
-            a0 = fmaf(__ldcg(xh + p), Bm[p * ldB + i], a0);
-            a1 = fmaf(__ldcg(xh + p + 1), Bm[(p + 1) * ldB + i], a1);
+            a0 = fmaf(xh[p], Bm[p * ldB + i], a0);
+            a1 = fmaf(xh[p + 1], Bm[(p + 1) * ldB + i], a1);
         }
-        if (p < r) a0 = fmaf(__ldcg(xh + p), Bm[p * ldB + i], a0);
-        resid[w] = a0 + a1 - __ldcg(X + side * d + i);
+        if (p < r) a0 = fmaf(xh[p], Bm[p * ldB + i], a0);
+        resid[w] = a0 + a1 - X[side * d + i];
     }
     __syncthreads();
     if (warp < 2) {
         const int side = warp;
         const float *xh = X + 2 * d + side * R;
         float nx = 0.f;
-        for (int p = lane; p < r; p += 32) nx = fmaf(__ldcg(xh + p), __ldcg(xh + p), nx);
+        for (int p = lane; p < r; p += 32) nx = fmaf(xh[p], xh[p], nx);
         nx = warp_sum(nx);
         float ss = 0.f;
         for (int i = lane; i < d; i += 32) ss = fmaf(resid[side * d + i], resid[side * d + i], ss);
@@ -822,7 +880,7 @@ __device__ void apply_deferred_b_update(const lrqk_layer_t &L, int bh, const flo
         const int p = e / d, i = e - p * d;
         const float eta = s_red[side];
         float *Bm = side ? sBK : sBQ;
-        const float v = Bm[p * ldB + i] - eta * __ldcg(X + 2 * d + side * R + p) * resid[side * d + i];
+        const float v = Bm[p * ldB + i] - eta * X[2 * d + side * R + p] * resid[side * d + i];
         Bm[p * ldB + i] = v;
         (side ? L.B_K : L.B_Q)[(size_t)bh * R * d + p * d + i] = v;
     }
@@ -922,23 +980,26 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
     float *sBK = sBQ + R * ldB;          // [R][ldB]
     float *b0 = sBK + R * ldB;           // [R][ldM]  R, then R^-1
     float *b1 = b0 + R * ldM;            // [R][ldM]  P, then P^-1
-    float *tmp = b1 + R * ldM;           // [2 * NP * 16] gram scratch
+    float *tmp = b1 + R * ldM;           // [4 * NP * 16] gram scratch
     trace(13);
     if (!host) count_hits_hbm(L, bh, n, s_rc);
+    trace(35);
     stage_rows_f32(sBQ, ldB, L.B_Q + (size_t)bh * R * d, R, d);
     stage_rows_f32(sBK, ldB, L.B_K + (size_t)bh * R * d, R, d);
     if (pre[PL.flags + 2] != 0.f) {  // the step's deferred line-search B update
         __syncthreads();
+        trace(36);
         apply_deferred_b_update(L, bh, pre + PL.X, sBQ, sBK, ldB, tmp, s_rc);
         if (tid == 0) pre[PL.flags + 2] = 0.f;
     }
+    trace(37);
     for (int e = tid; e < R * R; e += blockDim.x) {  // identity padding
         const int i = e / R, j = e - i * R;
         if (i >= r || j >= r) { b0[i * ldM + j] = (i == j) ? 1.f : 0.f; b1[i * ldM + j] = (i == j) ? 1.f : 0.f; }
     }
     __syncthreads();
-    gram_rows(sBK, r, d, ldB, b0, ldM, tmp);  // R (exactly symmetric)
-    gram_rows(sBQ, r, d, ldB, b1, ldM, tmp);  // B_Q B_Q^T
+    gram_rows2(sBK, sBQ, r, d, ldB, b0, b1, ldM, tmp);  // R (exactly symmetric), B_Q B_Q^T
+    trace(38);
     const float l2 = L.lambda_2;
     const bool have_res = n > 0;
     const float *Gs = YG + (size_t)R * d;
@@ -1022,7 +1083,8 @@ static size_t prepare_reduce_smem_bytes(const lrqk_layer_t &L) {
 static size_t prepare_finish_smem_bytes(const lrqk_layer_t &L) {
     const size_t d = L.dim_stride, R = L.rank_stride;
     const size_t ldB = d + 4, ldM = R + 4, RB = R / 4, NP = RB * (RB + 1) / 2;
-    return (2 * R * ldB + 2 * R * ldM + 2 * NP * 16) * sizeof(float);
+    const size_t scratch = 4 * NP * 16 > 4 * d + 2 * R ? 4 * NP * 16 : 4 * d + 2 * R;
+    return (2 * R * ldB + 2 * R * ldM + scratch) * sizeof(float);
 }
 
 // ---------------------------------------------------------------------------
