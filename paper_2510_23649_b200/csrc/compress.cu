@@ -141,6 +141,72 @@ __device__ bool block_gj(float *M, int R, int ld, float *s_rc) {
     return block_gj_t<1>(M, R, ld, s_rc);
 }
 
+// Both inverses of the finish kernel (R and P) in one Gauss-Jordan sweep:
+// one barrier per pivot for the pair.  s_rc: 512 floats.  ok[m] is
+// block-uniform; a failed matrix stops updating, the other goes on.
+template <int E>
+__device__ void block_gj2_t(float *M0, float *M1, int R, int ld, float *s_rc, bool (&ok)[2]) {
+    const int tid = threadIdx.x;
+    const int e0 = tid * E;
+    const bool act = e0 < R * R;
+    const int i = act ? e0 / R : 0, c0 = act ? e0 - (e0 / R) * R : 0;
+    float own[2][E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        own[0][e] = act ? M0[i * ld + c0 + e] : 0.f;
+        own[1][e] = act ? M1[i * ld + c0 + e] : 0.f;
+    }
+    ok[0] = ok[1] = true;
+    __syncthreads();
+    for (int k = 0; k < R; ++k) {
+        float *buf = s_rc + (k & 1) * 256;  // [m][row 64 | col 64]
+        if (act) {
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                if (i == k) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) buf[m * 128 + c0 + e] = own[m][e];
+                }
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (c0 + e == k) buf[m * 128 + 64 + i] = own[m][e];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            const float *rowb = buf + m * 128, *colb = rowb + 64;
+            const float p = rowb[k];
+            if (!(p > 0.f) || !isfinite(p)) ok[m] = false;  // block-uniform
+            if (act && ok[m]) {
+                const float ip = __frcp_rn(p);
+                const float f = colb[i] * ip;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int j = c0 + e;
+                    const float piv = rowb[j];
+                    if (i == k) own[m][e] = (j == k) ? ip : own[m][e] * ip;
+                    else own[m][e] = (j == k) ? -f : fmaf(-f, piv, own[m][e]);
+                }
+            }
+        }
+    }
+    if (act) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if (ok[0]) M0[i * ld + c0 + e] = own[0][e];
+            if (ok[1]) M1[i * ld + c0 + e] = own[1][e];
+        }
+    }
+    __syncthreads();
+}
+__device__ void block_gj2(float *M0, float *M1, int R, int ld, float *s_rc, bool (&ok)[2]) {
+    const int nn = R * R;
+    if (nn >= 16 * kCompressThreads) block_gj2_t<16>(M0, M1, R, ld, s_rc, ok);
+    else if (nn >= 4 * kCompressThreads) block_gj2_t<4>(M0, M1, R, ld, s_rc, ok);
+    else block_gj2_t<1>(M0, M1, R, ld, s_rc, ok);
+}
+
 // Fill b0 with M (r x r, row stride ldm) + jit on the diagonal, padded with
 // the identity to R x R (stride ld).  Whole block; ends with a barrier.
 __device__ void fill_padded(float *b0, const float *M, int ldm, int r, int R, int ld, float jit) {
@@ -941,7 +1007,7 @@ __device__ __forceinline__ void prepare_reduce_body(const lrqk_layer_t &L, int y
 
 __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int yg_slots) {
     extern __shared__ __align__(16) float smem[];
-    __shared__ float s_rc[256];
+    __shared__ float s_rc[512];
     const int bh = blockIdx.x;
     const int d = L.dim_stride, R = L.rank_stride, r = L.rank;
     const int tid = threadIdx.x;
@@ -1026,8 +1092,9 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
     }
     __syncthreads();
     trace(14);
-    const bool okR = block_gj(b0, R, ldM, s_rc);
-    const bool okP = block_gj(b1, R, ldM, s_rc);
+    bool okRP[2];
+    block_gj2(b0, b1, R, ldM, s_rc, okRP);
+    const bool okR = okRP[0], okP = okRP[1];
     for (int e = tid; e < R * R; e += blockDim.x) {
         const int i = e / R, j = e - i * R;
         const bool in = i < r && j < r;
