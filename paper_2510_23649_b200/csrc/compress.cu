@@ -252,6 +252,20 @@ __device__ void stage_rows_f32(float *dst, int ldx, const float *src, int rows, 
     const int n4 = rows * d / 4;
     const float4 *s4 = reinterpret_cast<const float4 *>(src);
     constexpr int U = 8;
+    const int d4 = d / 4;
+    if ((int)blockDim.x % d4 == 0) {  // fixed column per thread: no divisions in the loop
+        const int c = (int)threadIdx.x % d4, rstep = blockDim.x / d4;
+        for (int p0 = threadIdx.x / d4; p0 < rows; p0 += rstep * U) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (p0 + u * rstep < rows) v[u] = __ldcg(s4 + (p0 + u * rstep) * d4 + c);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (p0 + u * rstep < rows) *reinterpret_cast<float4 *>(dst + (p0 + u * rstep) * ldx + c * 4) = v[u];
+        }
+        return;
+    }
     for (int base = threadIdx.x; base < n4; base += blockDim.x * U) {
         float4 v[U];
 #pragma unroll
@@ -941,14 +955,19 @@ __device__ void apply_deferred_b_update(const lrqk_layer_t &L, int bh, const flo
         if (lane == 0) s_red[side] = (den <= 1e-14f * (1.f + fabsf(num))) ? 0.f : num / den;
     }
     __syncthreads();
-    for (int w = tid; w < 2 * r * d; w += blockDim.x) {
-        const int side = w / (r * d), e = w - side * r * d;
-        const int p = e / d, i = e - p * d;
-        const float eta = s_red[side];
-        float *Bm = side ? sBK : sBQ;
-        const float v = Bm[p * ldB + i] - eta * X[2 * d + side * R + p] * resid[side * d + i];
-        Bm[p * ldB + i] = v;
-        (side ? L.B_K : L.B_Q)[(size_t)bh * R * d + p * d + i] = v;
+    {   // B -= eta x_hat^T resid, float4 columns; rows 0..r-1 of B_Q then of B_K
+        const int d4 = d / 4, rstep = blockDim.x / d4;  // d4 divides blockDim (d is a power of two <= 4 * blockDim)
+        const int i = (tid - (tid / d4) * d4) * 4;
+        for (int rr = tid / d4; rr < 2 * r; rr += rstep) {
+            const int side = rr >= r, p = rr - side * r;
+            const float c = s_red[side] * X[2 * d + side * R + p];
+            float *Bm = (side ? sBK : sBQ) + p * ldB + i;
+            const float *rs = resid + side * d + i;
+            float4 v = *reinterpret_cast<float4 *>(Bm);
+            v.x -= c * rs[0]; v.y -= c * rs[1]; v.z -= c * rs[2]; v.w -= c * rs[3];
+            *reinterpret_cast<float4 *>(Bm) = v;
+            *reinterpret_cast<float4 *>((side ? L.B_K : L.B_Q) + (size_t)bh * R * d + p * d + i) = v;
+        }
     }
     if (tid < 2) L.eta[(size_t)bh * 2 + tid] = s_red[tid];
     __syncthreads();
@@ -1021,11 +1040,21 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
     float *YG = L.red_scratch + (size_t)bh * yg_slots * PF;
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     const int nyg = meta[M_YG];
-    if (nyg > 1) {
-        for (size_t e = tid; e < PF; e += blockDim.x) {
-            float acc = 0.f;
-            for (int c2 = 0; c2 < nyg; ++c2) acc += __ldcg(YG + (size_t)c2 * PF + e);
-            YG[e] = acc;
+    if (nyg > 1) {  // slots summed in order; 8 slots' loads in flight per float4
+        const size_t PF4 = PF / 4;
+        float4 *YG4 = reinterpret_cast<float4 *>(YG);
+        for (size_t e4 = tid; e4 < PF4; e4 += blockDim.x) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int c0 = 0; c0 < nyg; c0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (c0 + u < nyg) v[u] = __ldcg(YG4 + (size_t)(c0 + u) * PF4 + e4);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (c0 + u < nyg) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+            }
+            YG4[e4] = acc;
         }
         __syncthreads();
     }
@@ -1116,14 +1145,30 @@ prepare_reduce_cluster_kernel(const lrqk_layer_t L, int yg_slots) { prepare_redu
 __global__ void __cluster_dims__(kPcCtas, 1, 1) __launch_bounds__(kCompressThreads, 2)
 prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls, int n_layers, int yg_slots) {
     // persistent clusters over (layer, head): heads that select_attend
-    // already reduced (the common case) are skipped with one meta read
+    // already reduced (the common case) are skipped: one parallel flag read
+    // per blockDim items, compacted in item order (identical in every CTA of
+    // the cluster, so the cluster stays on the same item)
+    __shared__ int s_items[kCompressThreads];
+    __shared__ int s_scan[32];
     const int BH = Ls[0].batch * Ls[0].n_q_heads;
-    for (int item = blockIdx.y; item < n_layers * BH; item += gridDim.y) {
-        const lrqk_layer_t &L = Ls[item / BH];
-        const int bh = item % BH;
-        if (__ldcg(L.sel_meta + (size_t)bh * kMetaInts + M_YG) > 0) continue;  // uniform over the cluster
-        prepare_reduce_body(L, yg_slots, bh);
+    const int n_mine = (n_layers * BH - (int)blockIdx.y + (int)gridDim.y - 1) / (int)gridDim.y;
+    for (int k0 = 0; k0 < n_mine; k0 += blockDim.x) {
+        const int k = k0 + threadIdx.x;
+        const int item = blockIdx.y + k * gridDim.y;
+        bool need = false;
+        if (k < n_mine) {
+            const int *meta = Ls[item / BH].sel_meta + (size_t)(item % BH) * kMetaInts;
+            need = __ldcg(meta + M_YG) <= 0;
+        }
+        int tot;
+        const int pos = block_exclusive_scan(need ? 1 : 0, s_scan, &tot);
+        if (need) s_items[pos] = item;
         __syncthreads();
+        for (int j = 0; j < tot; ++j) {
+            const int it = s_items[j];
+            prepare_reduce_body(Ls[it / BH], yg_slots, it % BH);
+            __syncthreads();
+        }
     }
 }
 __global__ void __launch_bounds__(kCompressThreads)
