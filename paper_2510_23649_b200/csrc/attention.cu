@@ -12,7 +12,35 @@ struct AttnArgs {
     lrqk_layer_t L;
     const void *q;
     float *out;
+    int yg_slots;  // red_scratch slots per head (compress.cu yg_slots)
 };
+
+// A mode-5 head's blocks other than split 0 have no rows to attend; they sum
+// select_attend's Y|G slot partials (in slot order, as the finish kernel
+// would) into slot 0, each block one float4 slice, so the end-of-step finish
+// kernel reads one slot instead of parts + 1.
+__device__ void fold_yg_slots(const lrqk_layer_t &L, int bh, int yg_slots, int blk, int nblk) {
+    const int *meta = L.sel_meta + (size_t)bh * kMetaInts;
+    const int nyg = meta[M_YG];
+    if (nyg <= 1) return;
+    const size_t PF4 = yg_part_floats(L.rank_stride, L.dim_stride) / 4;
+    float4 *YG4 = reinterpret_cast<float4 *>(L.red_scratch + (size_t)bh * yg_slots * PF4 * 4);
+    const size_t per = (PF4 + nblk - 1) / nblk, e0 = (size_t)blk * per, e1 = min(PF4, e0 + per);
+    for (size_t e4 = e0 + threadIdx.x; e4 < e1; e4 += blockDim.x) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c0 = 0; c0 < nyg; c0 += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (c0 + u < nyg) v[u] = __ldcg(YG4 + (size_t)(c0 + u) * PF4 + e4);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (c0 + u < nyg) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+        }
+        YG4[e4] = acc;
+    }
+    if (blk == 0 && threadIdx.x == 0) const_cast<int *>(meta)[M_YG_FOLD] = 1;
+}
 
 // One block = one split of kAttnRows selected rows of one (b, h).  Lanes are
 // grouped LPR per row (16-byte packs across d); each group runs an online
@@ -44,18 +72,28 @@ __device__ void merge_select_attend_partials(const lrqk_layer_t &L, int bh, floa
     const float inv = 1.f / s_den;
     for (int i = threadIdx.x; i < d; i += blockDim.x) {
         float o = 0.f;
-        for (int p = 0; p < np; ++p) {
-            float w;
-            if (p < 64) {
-                w = s_w[p];
-            } else {
-                const float pm = __ldcg(parts + (size_t)p * (d + 2));
-                w = pm == -INFINITY ? 0.f : exp2f(pm - s_mx);
+        for (int p0 = 0; p0 < np; p0 += 8) {  // 8 partials' loads in flight, summed in order
+            float v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (p0 + u < np) v[u] = __ldcg(parts + (size_t)(p0 + u) * (d + 2) + 2 + i);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int p = p0 + u;
+                if (p >= np) break;
+                float w;
+                if (p < 64) {
+                    w = s_w[p];
+                } else {
+                    const float pm = __ldcg(parts + (size_t)p * (d + 2));
+                    w = pm == -INFINITY ? 0.f : exp2f(pm - s_mx);
+                }
+                o = fmaf(v[u], w, o);
             }
-            o = fmaf(__ldcg(parts + (size_t)p * (d + 2) + 2 + i), w, o);
         }
         out[(size_t)bh * d + i] = o * inv;
     }
+    trace(39);
 }
 
 template <typename T, int LPR, int PPL>
@@ -81,6 +119,7 @@ attention_kernel(const AttnArgs a) {
     if (L.sel_meta[(size_t)bh * kMetaInts + M_MODE] == 5) {
         // select_attend_kernel left parts + 1 softmax partials: merge them
         if (split == 0) merge_select_attend_partials(L, bh, a.out);
+        else if (a.yg_slots > 0) fold_yg_slots(L, bh, a.yg_slots, split - 1, gridDim.x - 1);
         return;
     }
     const int S = L.res_cnt[bh];
@@ -279,8 +318,9 @@ static int launch_attention_t(const AttnArgs &a, cudaStream_t st) {
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
+int yg_slots(const lrqk_layer_t &L);
 int launch_attention(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st) {
-    AttnArgs a{L, q, out};
+    AttnArgs a{L, q, out, L.red_scratch ? yg_slots(L) : 0};
     return L.dtype == LRQK_BF16 ? launch_attention_t<__nv_bfloat16>(a, st) : launch_attention_t<float>(a, st);
 }
 

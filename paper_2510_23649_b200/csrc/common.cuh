@@ -47,6 +47,7 @@ enum Meta : int {
     M_YG_ADD = 42,     // bin-D winners (res_idx[M_NABOVE, +n)) whose Y|G the finish kernel adds
     M_ATT_PARTS = 43,  // softmax partials select_attend left for attention_kernel to merge (parts + 1)
     M_KC = 44,         // this step's candidate bound (key) of cmask; 0xFFFFFFFF: no mask
+    M_YG_FOLD = 45,    // attention_kernel already summed the M_YG slots into slot 0
 };
 constexpr int kPrevCrit = 8;
 

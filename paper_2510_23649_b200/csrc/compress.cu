@@ -1040,7 +1040,7 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
     float *YG = L.red_scratch + (size_t)bh * yg_slots * PF;
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     const int nyg = meta[M_YG];
-    if (nyg > 1) {  // slots summed in order; 8 slots' loads in flight per float4
+    if (nyg > 1 && meta[M_YG_FOLD] == 0) {  // slots summed in order; 8 slots' loads in flight per float4
         const size_t PF4 = PF / 4;
         float4 *YG4 = reinterpret_cast<float4 *>(YG);
         for (size_t e4 = tid; e4 < PF4; e4 += blockDim.x) {
@@ -1068,7 +1068,7 @@ __device__ __forceinline__ void prepare_finish_body(const lrqk_layer_t &L, int y
                       L.res_idx + (size_t)bh * L.s_cap + meta[M_NABOVE], nadd, smem, YG);
     }
     __syncthreads();
-    if (tid == 0) { meta[M_YG] = 0; meta[M_YG_ADD] = 0; }
+    if (tid == 0) { meta[M_YG] = 0; meta[M_YG_ADD] = 0; meta[M_YG_FOLD] = 0; }
     const int ldB = d + 4, ldM = R + 4;
     const int RB = R / 4, NP = RB * (RB + 1) / 2;
     float *sBQ = smem;                   // [R][ldB]
@@ -1150,6 +1150,7 @@ prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls, int n_layers, int y
     // the cluster, so the cluster stays on the same item)
     __shared__ int s_items[kCompressThreads];
     __shared__ int s_scan[32];
+    trace(8);
     const int BH = Ls[0].batch * Ls[0].n_q_heads;
     const int n_mine = (n_layers * BH - (int)blockIdx.y + (int)gridDim.y - 1) / (int)gridDim.y;
     for (int k0 = 0; k0 < n_mine; k0 += blockDim.x) {
@@ -1170,11 +1171,15 @@ prepare_reduce_cluster_layers_kernel(const lrqk_layer_t *Ls, int n_layers, int y
             __syncthreads();
         }
     }
+    trace(9);
 }
 __global__ void __launch_bounds__(kCompressThreads)
 prepare_finish_kernel(const lrqk_layer_t L, int yg_slots) { prepare_finish_body(L, yg_slots); }
 __global__ void __launch_bounds__(kCompressThreads, 4)
-prepare_finish_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) { prepare_finish_body(Ls[blockIdx.z], yg_slots); }
+prepare_finish_layers_kernel(const lrqk_layer_t *Ls, int yg_slots) {
+    trace(7);
+    prepare_finish_body(Ls[blockIdx.z], yg_slots);
+}
 
 static bool pc_enabled() {
     static const bool on = [] { const char *e = getenv("LRQK_PREPARE_CLUSTER"); return !(e && e[0] == '0'); }();

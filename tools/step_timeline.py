@@ -59,7 +59,7 @@ tags = (rec[:, 0] >> 48).astype(int)
 names = {0: "compress start", 1: "compress staged", 4: "compress B-update done", 40: "score start", 41: "score stream done",
          42: "score last-block", 43: "score end", 50: "sel_attend start", 51: "sel_attend meta", 52: "sel_attend part done",
          53: "sel_attend last-block", 54: "sel_attend end", 55: "sa crit sorted", 56: "sa part scanned", 44: "sa classified", 45: "sa crit flushed", 46: "sa cmask read", 47: "sa cands listed", 48: "sa keys classified", 49: "sa scanned",
-         57: "sa part YG written", 58: "sa own partial", 59: "sa parts max", 60: "sa merged", 20: "select start", 30: "attention start", 10: "prepare start", 13: "finish YG summed", 35: "finish hits counted", 36: "finish B staged", 37: "finish B updated", 38: "finish grams",
+         57: "sa part YG written", 58: "sa own partial", 59: "sa parts max", 60: "sa merged", 20: "select start", 30: "attention start", 10: "prepare start", 13: "finish YG summed", 7: "finish kernel start", 39: "attention merged (mode 5)", 8: "reduce kernel start", 9: "reduce kernel end", 35: "finish hits counted", 36: "finish B staged", 37: "finish B updated", 38: "finish grams",
          11: "prepare reduce done", 14: "prepare finish start", 16: "prepare end", 17: "prep idx staged", 18: "prep first chunk in", 19: "prep mma done", 61: "prep R gram", 62: "prep R GJ", 63: "prep pre-sync"}
 for tag in sorted(set(tags), key=lambda x: np.median(rec[tags == x, 1])):
     ts = (rec[tags == tag, 1] - t0) / 1e3
