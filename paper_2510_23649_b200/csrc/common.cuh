@@ -330,7 +330,9 @@ LRQK_DEV void trace(int tag) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         const unsigned blk = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
         const unsigned i = ((blk & 1023u) << 6) | (unsigned)(tag & 63);
-        g_lrqk_trace[i][0] = ((unsigned long long)tag << 48) | blk;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_lrqk_trace[i][0] = ((unsigned long long)tag << 48) | ((unsigned long long)(smid & 0xFFFFu) << 32) | blk;
         g_lrqk_trace[i][1] = t;
     }
 }

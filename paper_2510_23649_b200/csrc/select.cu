@@ -234,7 +234,8 @@ constexpr int kCW = 8;  // consumer warps
 template <int NPK> struct ScoreStages {
     static constexpr int kTileBytes = NPK * 512;
     static constexpr int kStageBytes = kCW * kTileBytes;
-    static constexpr int kStages = (80 * 1024 / kStageBytes) < 2 ? 2 : ((80 * 1024 / kStageBytes) > 6 ? 6 : 80 * 1024 / kStageBytes);
+    // 64 KB: two score blocks stay co-resident with a compress block (68 KB)
+    static constexpr int kStages = (64 * 1024 / kStageBytes) < 2 ? 2 : ((64 * 1024 / kStageBytes) > 6 ? 6 : 64 * 1024 / kStageBytes);
     static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
 };
 

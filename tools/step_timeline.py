@@ -66,7 +66,8 @@ for tag in sorted(set(tags), key=lambda x: np.median(rec[tags == x, 1])):
     print(f"tag {tag:3d} {names.get(tag, ''):24s} n={len(ts):4d} min={ts.min():7.1f} med={np.median(ts):7.1f} max={ts.max():7.1f} us")
 print("graph step (events): %.1f us" % (s.elapsed_time(e) * 1e3))
 if os.environ.get("TL_DUMP_TAG"):
-    tg = int(os.environ["TL_DUMP_TAG"])
     blk = (rec[:, 0] & 0xFFFFFF).astype(int)
-    sel = tags == tg
-    np.save("gpurun_out/tl_dump.npy", np.stack([blk[sel], (rec[sel, 1] - t0) / 1e3], 1))
+    sm = ((rec[:, 0] >> 32) & 0xFFFF).astype(int)
+    for tg in [int(x) for x in os.environ["TL_DUMP_TAG"].split(",")]:
+        sel = tags == tg
+        np.save("gpurun_out/tl_dump_%d.npy" % tg, np.stack([blk[sel], (rec[sel, 1] - t0) / 1e3, sm[sel]], 1))
