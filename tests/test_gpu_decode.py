@@ -336,3 +336,42 @@ def test_engine_matches_per_layer_steps():
             assert torch.equal(eng.out_buf[i][..., :d], outs[i]), f"layer {i} step {step}"
             for name in ("res_cnt", "step_miss", "c_miss", "B_Q", "B_K"):
                 assert torch.equal(eng.layers[i].view(name), ref[i].view(name)), (name, i, step)
+
+
+@pytest.mark.parametrize("r,kb", [(16, 256), (32, 1024), (64, 4096)])
+def test_rank_topk_sweep_selection_and_output(r, kb):
+    """SURVEY §8 C5 shapes (r in {16, 32, 64}, k in {256, 1024, 4096}) at a
+    shortened context: every step's selection is the exact top-k of the GPU's
+    own scores, and the output equals fp32 attention over that selection
+    (bf16 K/V, rtol 2e-2 as north_star states for bf16)."""
+    from paper_2510_23649_b200.engine import prefill_factorize_device
+
+    torch.manual_seed(1)
+    B, Hq, Hkv, d, lb, ctx = 1, 4, 1, 128, 16, 24000
+    dev = torch.device("cuda")
+    Qp = torch.randn(B * Hq, ctx, d, device=dev).to(torch.bfloat16)
+    Kp = torch.randn(B * Hkv, ctx, d, device=dev).to(torch.bfloat16)
+    Vp = torch.randn(B * Hkv, ctx, d, device=dev).to(torch.bfloat16)
+    res = prefill_factorize_device(Qp, Kp, r, dtype="bf16", group=Hq // Hkv)
+    layer = make_layer(B, Hq, Hkv, d, r, kb, lb, t_max=ctx + 16, dtype="bf16")
+    layer.load_prompt(res["A_K"].reshape(B, Hq, ctx, r), res["B_Q"].reshape(B, Hq, r, d),
+                      res["B_K"].reshape(B, Hq, r, d), Kp.view(B, Hkv, ctx, d), Vp.view(B, Hkv, ctx, d))
+    out = torch.zeros(B, Hq, d, device=dev)
+    Kall, Vall = Kp.view(B, Hkv, ctx, d).float(), Vp.view(B, Hkv, ctx, d).float()
+    for t in range(ctx, ctx + 4):
+        q = torch.randn(B, Hq, d, device=dev).to(torch.bfloat16)
+        k = torch.randn(B, Hkv, d, device=dev).to(torch.bfloat16)
+        v = torch.randn(B, Hkv, d, device=dev).to(torch.bfloat16)
+        layer.step(q, k, v, out)
+        torch.cuda.synchronize()
+        layer.raise_status()
+        _select_exact_check(layer, t, kb, lb)
+        Kall = torch.cat([Kall, k.float()[:, :, None]], 2)
+        Vall = torch.cat([Vall, v.float()[:, :, None]], 2)
+        cnt = layer.view("res_cnt").cpu()
+        idx = layer.view("res_idx").cpu()
+        for h in range(Hq):
+            sel = idx[0, h, : int(cnt[0, h])].long().to(dev)
+            Ks, Vs = Kall[0, h // (Hq // Hkv)][sel], Vall[0, h // (Hq // Hkv)][sel]
+            w = torch.softmax(q[0, h].float() @ Ks.T / d ** 0.5, -1)
+            torch.testing.assert_close(out[0, h], w @ Vs, rtol=2e-2, atol=2e-3)
