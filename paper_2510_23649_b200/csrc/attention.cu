@@ -13,6 +13,9 @@ struct AttnArgs {
     const void *q;
     float *out;
     int yg_slots;  // red_scratch slots per head (compress.cu yg_slots)
+    int slots;     // attn_scratch partial slots per head (attn_scratch_slots): the
+                   // stride select_attend_kernel uses too, so heads of the two
+                   // paths in one step never write each other's partials
 };
 
 // A mode-5 head's blocks other than split 0 have no rows to attend; they sum
@@ -225,7 +228,7 @@ attention_kernel(const AttnArgs a) {
         for (int e = 0; e < N; ++e) s_acc[gidx * d + (sl + pp * LPR) * N + e] = acc[pp][e];
     __syncthreads();
     // merge groups -> split partial
-    float *part = L.attn_scratch + ((size_t)bh * gridDim.x + split) * (size_t)(d + 2);
+    float *part = L.attn_scratch + ((size_t)bh * a.slots + split) * (size_t)(d + 2);
     float M = -INFINITY;
     for (int i = 0; i < NW * RPW; ++i) M = fmaxf(M, s_m[i]);
     for (int i = tid; i < d; i += blockDim.x) {
@@ -248,7 +251,7 @@ attention_kernel(const AttnArgs a) {
     __shared__ float s_ms[64], s_w[64];
     __shared__ float s_den;
     const int nsp = gridDim.x;
-    const float *parts = L.attn_scratch + (size_t)bh * nsp * (size_t)(d + 2);
+    const float *parts = L.attn_scratch + (size_t)bh * a.slots * (size_t)(d + 2);
     for (int sp = tid; sp < nsp; sp += blockDim.x) {
         s_ms[sp] = __ldcg(parts + (size_t)sp * (d + 2));
         s_w[sp] = __ldcg(parts + (size_t)sp * (d + 2) + 1);
@@ -319,8 +322,9 @@ static int launch_attention_t(const AttnArgs &a, cudaStream_t st) {
 }
 
 int yg_slots(const lrqk_layer_t &L);
+int attn_scratch_slots(const lrqk_layer_t &L);
 int launch_attention(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st) {
-    AttnArgs a{L, q, out, L.red_scratch ? yg_slots(L) : 0};
+    AttnArgs a{L, q, out, L.red_scratch ? yg_slots(L) : 0, attn_scratch_slots(L)};
     return L.dtype == LRQK_BF16 ? launch_attention_t<__nv_bfloat16>(a, st) : launch_attention_t<float>(a, st);
 }
 

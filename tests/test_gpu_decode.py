@@ -375,3 +375,43 @@ def test_rank_topk_sweep_selection_and_output(r, kb):
             Ks, Vs = Kall[0, h // (Hq // Hkv)][sel], Vall[0, h // (Hq // Hkv)][sel]
             w = torch.softmax(q[0, h].float() @ Ks.T / d ** 0.5, -1)
             torch.testing.assert_close(out[0, h], w @ Vs, rtol=2e-2, atol=2e-3)
+
+
+def test_mixed_paths_in_one_step_keep_outputs_apart():
+    """One head misses its threshold window (general select + attention
+    kernels) while the others take the fused select_attend path in the same
+    step: the two paths share attn_scratch and must use one slot stride, or
+    the general path's split partials land on a fused head's part partials."""
+    from paper_2510_23649_b200.engine import prefill_factorize_device
+
+    torch.manual_seed(5)
+    B, Hq, Hkv, d, r, kb, lb, ctx = 1, 8, 2, 128, 16, 256, 16, 24000
+    dev = torch.device("cuda")
+    Qp = torch.randn(B * Hq, ctx, d, device=dev).to(torch.bfloat16)
+    Kp = torch.randn(B * Hkv, ctx, d, device=dev).to(torch.bfloat16)
+    Vp = torch.randn(B * Hkv, ctx, d, device=dev).to(torch.bfloat16)
+    res = prefill_factorize_device(Qp, Kp, r, dtype="bf16", group=Hq // Hkv)
+    layer = make_layer(B, Hq, Hkv, d, r, kb, lb, t_max=ctx + 16, dtype="bf16")
+    layer.load_prompt(res["A_K"].reshape(B, Hq, ctx, r), res["B_Q"].reshape(B, Hq, r, d),
+                      res["B_K"].reshape(B, Hq, r, d), Kp.view(B, Hkv, ctx, d), Vp.view(B, Hkv, ctx, d))
+    out = torch.zeros(B, Hq, d, device=dev)
+    Kall, Vall = Kp.view(B, Hkv, ctx, d).float(), Vp.view(B, Hkv, ctx, d).float()
+    G = Hq // Hkv
+    for t in range(ctx, ctx + 5):
+        q = torch.randn(B, Hq, d, device=dev).to(torch.bfloat16)
+        if t >= ctx + 2:  # head 3's scores jump ~10 octaves: its hint misses, the rest stay fused
+            q[:, 3] = (q[:, 3].float() * 1000.0).to(torch.bfloat16)
+        k = torch.randn(B, Hkv, d, device=dev).to(torch.bfloat16)
+        v = torch.randn(B, Hkv, d, device=dev).to(torch.bfloat16)
+        layer.step(q, k, v, out)
+        torch.cuda.synchronize()
+        layer.raise_status()
+        _select_exact_check(layer, t, kb, lb)
+        Kall = torch.cat([Kall, k.float()[:, :, None]], 2)
+        Vall = torch.cat([Vall, v.float()[:, :, None]], 2)
+        cnt = layer.view("res_cnt").cpu()
+        idx = layer.view("res_idx").cpu()
+        for h in range(Hq):
+            sel = idx[0, h, : int(cnt[0, h])].long().to(dev)
+            w = torch.softmax(q[0, h].float() @ Kall[0, h // G][sel].T / d ** 0.5, -1)
+            torch.testing.assert_close(out[0, h], w @ Vall[0, h // G][sel], rtol=2e-2, atol=2e-3)
