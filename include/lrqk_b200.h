@@ -245,6 +245,31 @@ int lrqk_prefill_factorize(const lrqk_prefill_t *P, void *stream);
 /* Copy the status word to host memory (synchronises the stream). */
 int lrqk_read_status(const uint32_t *status, uint32_t *host_out, void *stream);
 
+/* ---- SURVEY §8(b) entry-point names -------------------------------------
+ * The scope table names a minimum export list; these are those names over
+ * the entry points above (same semantics, same status codes). */
+
+/* Total device bytes of one layer's buffers (the sum of
+ * lrqk_layer_buffer_bytes), 0 for an invalid configuration. */
+size_t lrqk_workspace_size(const lrqk_layer_t *cfg);
+
+/* Proxy scores over A_K[0..t] (k_hat_t was appended by
+ * lrqk_decode_compress) = lrqk_score.  ref: cache.py:141-146, 211. */
+int lrqk_score_append(const lrqk_layer_t *L, void *stream);
+
+/* Fast-tier update after the selection: the host policy copies the step's
+ * missed rows into their slots (= lrqk_gather_misses); the HBM policy's
+ * residency/counter update is folded into lrqk_compress_prepare, so this is
+ * a no-op for it.  ref: cache.py:174-196. */
+int lrqk_cache_update(const lrqk_layer_t *L, void *stream);
+
+/* The layer's status word to host (= lrqk_read_status(L->status, ...)). */
+int lrqk_get_status(const lrqk_layer_t *L, uint32_t *host_out, void *stream);
+
+/* CacheStats counters to host: c_miss and c_total, [B, Hq] int64 each
+ * (synchronises the stream).  ref: cache.py:63-81. */
+int lrqk_counters(const lrqk_layer_t *L, int64_t *c_miss_out, int64_t *c_total_out, void *stream);
+
 /* Name of the last CUDA error seen by the library (thread-local). */
 const char *lrqk_last_error(void);
 

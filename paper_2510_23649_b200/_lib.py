@@ -80,6 +80,11 @@ SIGNATURES = {
     "lrqk_attention": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_compress_prepare_layers": (C.c_int, [_P, C.POINTER(LayerStruct), C.c_int32, _P]),
     "lrqk_select_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
+    "lrqk_workspace_size": (C.c_size_t, [C.POINTER(LayerStruct)]),
+    "lrqk_score_append": (C.c_int, [C.POINTER(LayerStruct), _P]),
+    "lrqk_cache_update": (C.c_int, [C.POINTER(LayerStruct), _P]),
+    "lrqk_get_status": (C.c_int, [C.POINTER(LayerStruct), _P, _P]),
+    "lrqk_counters": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_decode_step": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P, _P, C.c_int, _P]),
     "lrqk_advance": (C.c_int, [_P, C.c_int32, _P]),
     "lrqk_proxy_scores_f32": (C.c_int, [_P, C.c_int32, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P]),

@@ -367,6 +367,37 @@ int lrqk_read_status(const uint32_t *status, uint32_t *host_out, void *stream) {
     return LRQK_OK;
 }
 
+size_t lrqk_workspace_size(const lrqk_layer_t *cfg) {
+    size_t sizes[64];
+    const int n = lrqk_layer_buffer_bytes(cfg, sizes, 64);
+    if (n <= 0) return 0;
+    size_t tot = 0;
+    for (int i = 0; i < n; ++i) tot += sizes[i];
+    return tot;
+}
+
+int lrqk_score_append(const lrqk_layer_t *L, void *stream) { return lrqk_score(L, stream); }
+
+int lrqk_cache_update(const lrqk_layer_t *L, void *stream) { return lrqk_gather_misses(L, stream); }
+
+int lrqk_get_status(const lrqk_layer_t *L, uint32_t *host_out, void *stream) {
+    if (!L) return LRQK_EINVAL;
+    return lrqk_read_status(L->status, host_out, stream);
+}
+
+int lrqk_counters(const lrqk_layer_t *L, int64_t *c_miss_out, int64_t *c_total_out, void *stream) {
+    int rc = validate(L);
+    if (rc) return rc;
+    if (!c_miss_out || !c_total_out || !L->c_miss || !L->c_total) return LRQK_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)L->batch * L->n_q_heads * sizeof(int64_t);
+    if (cudaMemcpyAsync(c_miss_out, L->c_miss, n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(c_total_out, L->c_total, n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+        return check(LRQK_ECUDA);
+    return LRQK_OK;
+}
+
 }  // extern "C"
 
 // ---- development tracing (see common.cuh) --------------------------------

@@ -53,6 +53,7 @@ def test_buffer_sizes_for_north_star_layer():
     assert got["proxy"] == 32 * (131072 + 256) * 32 * 2
     assert got["slow_k"] == 8 * (131072 + 256) * 128 * 2
     assert got["slot_k"] == 0  # HBM policy keeps no slots
+    assert lib.lrqk_workspace_size(ctypes.byref(s)) == sum(sizes[:n])
 
 
 def test_invalid_configuration_rejected():

@@ -415,3 +415,15 @@ def test_mixed_paths_in_one_step_keep_outputs_apart():
             sel = idx[0, h, : int(cnt[0, h])].long().to(dev)
             w = torch.softmax(q[0, h].float() @ Kall[0, h // G][sel].T / d ** 0.5, -1)
             torch.testing.assert_close(out[0, h], w @ Vall[0, h // G][sel], rtol=2e-2, atol=2e-3)
+    # the SURVEY §8(b) accessor names read the same state
+    import ctypes
+    from paper_2510_23649_b200 import _lib
+    lib = _lib.lib()
+    n = B * Hq
+    cm, ct = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+    assert lib.lrqk_counters(layer.ptr, ctypes.addressof(cm), ctypes.addressof(ct), _lib.stream_ptr()) == 0
+    assert list(cm) == layer.view("c_miss").flatten().tolist()
+    assert list(ct) == layer.view("c_total").flatten().tolist()
+    st = ctypes.c_uint32(7)
+    assert lib.lrqk_get_status(layer.ptr, ctypes.addressof(st), _lib.stream_ptr()) == 0
+    assert st.value == 0
