@@ -47,12 +47,16 @@ WORKLOADS = {
 }
 
 
-def _ncu_traffic():
+def _ncu_traffic(algorithmic_bytes):
     """dram__bytes_read.sum + dram__bytes_write.sum of the score kernel from the
-    committed ncu --set full capture (profiles/roofline_traffic.json), or None."""
+    committed ncu --set full capture (profiles/roofline_traffic.json) when that
+    capture was taken on this launch shape (same algorithmic bytes), or None."""
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")) as f:
-            return int(json.load(f)["dram_bytes_per_launch"])
+            rec = json.load(f)
+        if int(rec["algorithmic_bytes_per_launch"]) != int(algorithmic_bytes):
+            return None
+        return int(rec["dram_bytes_per_launch"])
     except (OSError, ValueError, KeyError):
         return None
 
@@ -87,6 +91,11 @@ def workload(args):
         w["r"] = args.rank
     if args.topk:
         w["k"] = args.topk
+    base = WORKLOADS[args.workload]
+    over = [f"{name}={w[key]}" for key, name in (("ctx", "ctx"), ("layers", "layers"), ("r", "r"), ("k", "top-k"))
+            if w[key] != base[key]]
+    if over:  # the description names the overrides
+        w["desc"] = base["desc"] + " [overridden: " + ", ".join(over) + "]"
     return w
 
 
@@ -382,7 +391,7 @@ def run_ours(args, world, rank, local):
                     l2="no flush: each step streams %.1f GB (> 126 MB L2)" % (byt["total"] * L / 1e9)),
         roofline=dict(bound="hbm", kernel="score_kernel (proxy scores + radix histogram)",
                       achieved=round(score_gbs, 1), peak=hbm_peak, unit="GB/s",
-                      frac=round(score_gbs / hbm_peak, 4), traffic=_ncu_traffic(),
+                      frac=round(score_gbs / hbm_peak, 4), traffic=_ncu_traffic(score_bytes),
                       algorithmic_bytes_per_launch=score_bytes, avg_launch_ms=round(score_ms, 5),
                       step_frac_of_hbm=round(step_gbs / hbm_peak, 4), step_algorithmic_GBps=round(step_gbs, 1),
                       peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"),
