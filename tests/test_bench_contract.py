@@ -1,0 +1,44 @@
+"""Host-side pieces of bench.py that the JSON line depends on (CPU only):
+the algorithmic-bytes model of SURVEY §8(d), workload overrides, and the
+ncu traffic lookup being tied to the captured launch shape."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+
+
+def _args(**kw):
+    a = argparse.Namespace(workload="c4", ctx=None, layers=None, rank=None, topk=None)
+    for k, v in kw.items():
+        setattr(a, k, v)
+    return a
+
+
+def test_step_bytes_match_survey_budget():
+    """C4 per sequence: 359 MB per layer, 11.49 GB per token over 32 layers
+    (SURVEY §8(d)); A_K is ~81 % of it (here t = ctx + 1 scores)."""
+    w = bench.workload(_args())
+    t, S = w["ctx"], w["k"] + w["lite"]
+    b = bench.step_bytes(w, 1, t, S, 2)
+    assert abs(b["total"] / 1e6 - 359.2) < 1.0
+    assert abs(b["total"] * w["layers"] / 1e9 - 11.49) < 0.03
+    assert 0.74 < b["a_k"] / b["total"] < 0.76 or 0.80 < b["a_k"] / b["total"] < 0.82
+
+
+def test_workload_overrides_are_named():
+    w = bench.workload(_args(rank=64, topk=4096))
+    assert w["r"] == 64 and w["k"] == 4096
+    assert "overridden" in w["desc"] and "r=64" in w["desc"] and "top-k=4096" in w["desc"]
+    assert "overridden" not in bench.workload(_args())["desc"]
+
+
+def test_ncu_traffic_only_for_the_captured_shape():
+    import json
+    rec = json.load(open(os.path.join(os.path.dirname(bench.__file__), "profiles", "roofline_traffic.json")))
+    alg = int(rec["algorithmic_bytes_per_launch"])
+    assert alg % (32 * (32 * 2 + 4)) == 0  # B*Hq*(t+1)*(R*e + 4) at C4
+    got = bench._ncu_traffic(alg)
+    assert got == int(rec["dram_bytes_per_launch"]) and 0 < got <= alg * 1.05
+    assert bench._ncu_traffic(alg + 32 * 68) is None  # another context length
