@@ -120,10 +120,11 @@ __device__ void attend_list(const T *kb, const T *vb, const int *rows, int n, co
 // the tensor-core reduction Y += A^T K, G += A^T A that the next step's
 // compression needs over Omega_t (compress.cu K2p), so compress_prepare
 // does not gather these rows again.
-template <typename T, int LPR, int PPL, bool YG>
+template <typename T, int LPR, int PPL, int YGM>
 __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *vb, const T *proxy, const int *rows,
                                    int n, const float (&qv)[PPL][Pack<T>::N], float c, float &m, float &l,
-                                   float (&acc)[PPL][Pack<T>::N], uint8_t *stage, float (&yacc)[2][2][4],
+                                   float (&acc)[PPL][Pack<T>::N], uint8_t *stage,
+                                   float (&yacc)[YGM > 0 ? YGM : 1][2][4],
                                    float (&gacc)[4][4]) {
     constexpr int N = Pack<T>::N;
     constexpr int RPW = 32 / LPR;
@@ -133,13 +134,15 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
     const int ng = nw * RPW, gidx = warp * RPW + sub;
     const int ldk = d * (int)sizeof(T) + 16, lda = R * 2 + 16;  // bytes (padded rows)
     const int kp = d * (int)sizeof(T) / 16;
+    constexpr bool YG = YGM > 0;
+    constexpr int PA = 2 * YGM;  // 16-byte packs per proxy row (R = 16 * YGM, bf16)
     const int tile_kv = kMmaRows * ldk, buf = 2 * tile_kv + (YG ? kMmaRows * lda : 0);
     const int nch = (n + kMmaRows - 1) / kMmaRows;
     auto issue = [&](int ch) {
         uint8_t *kS = stage + (ch & 1) * buf, *vS = kS + tile_kv, *aS = vS + tile_kv;
         const int r0 = ch * kMmaRows, nr = min(kMmaRows, n - r0);
         if constexpr (YG) {
-            // bf16, d = 128, R = 32: 16 packs per K/V row, 4 per proxy row (shifts only)
+            // bf16, d = 128, R = 16 * YGM: 16 packs per K/V row, PA per proxy row (shifts only)
             for (int e = tid; e < kMmaRows * 16; e += blockDim.x) {
                 const int j = e >> 4, pk = e & 15;
                 uint8_t *dk = kS + j * ldk + pk * 16, *dv = vS + j * ldk + pk * 16;
@@ -152,10 +155,10 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
                     *reinterpret_cast<uint4 *>(dv) = make_uint4(0, 0, 0, 0);
                 }
             }
-            for (int e = tid; e < kMmaRows * 4; e += blockDim.x) {
-                const int j = e >> 2, pk = e & 3;
+            for (int e = tid; e < kMmaRows * PA; e += blockDim.x) {
+                const int j = e / PA, pk = e % PA;
                 uint8_t *da = aS + j * lda + pk * 16;
-                if (j < nr) cp_async16(da, proxy + proxy_pack_offset(rows[r0 + j], pk, 4) * 8);
+                if (j < nr) cp_async16(da, proxy + proxy_pack_offset(rows[r0 + j], pk, PA) * 8);
                 else *reinterpret_cast<uint4 *>(da) = make_uint4(0, 0, 0, 0);
             }
         } else {
@@ -234,7 +237,7 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
                 m = mx;
             }
         }
-        if constexpr (YG) mma_reduce_tile<2, 2>(kS, ldk, aS, lda, R, yacc, gacc);
+        if constexpr (YG) mma_reduce_tile<YGM, 2>(kS, ldk, aS, lda, R, yacc, gacc);
         __syncthreads();
     }
 }
@@ -298,7 +301,7 @@ __device__ void block_partial(float m, float l, float (&acc)[PPL][Pack<T>::N], i
     __syncthreads();
 }
 
-template <typename T, int LPR, int PPL, bool YG>
+template <typename T, int LPR, int PPL, int YGM>
 __global__ void __launch_bounds__(kFThreads, 2)
 select_attend_kernel(const FArgs a) {
     const lrqk_layer_t &L = a.L;
@@ -368,9 +371,13 @@ select_attend_kernel(const FArgs a) {
     for (int pp = 0; pp < PPL; ++pp)
 #pragma unroll
         for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
-    float yacc[2][2][4], gacc[4][4];
+    constexpr bool YG = YGM > 0;
+    constexpr int MT = YGM > 0 ? YGM : 1;
+    float yacc[MT][2][4], gacc[4][4];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) { yacc[i / 8][(i / 4) & 1][i & 3] = 0.f; gacc[i / 4][i & 3] = 0.f; }
+    for (int i = 0; i < MT * 8; ++i) yacc[i / 8][(i / 4) & 1][i & 3] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) gacc[i / 4][i & 3] = 0.f;
     trace(51);
 
     // ---- this part's winners: ordered write, then attention (+ Y, G) -------
@@ -489,10 +496,10 @@ select_attend_kernel(const FArgs a) {
     }
     __syncthreads();
     trace(56);
-    attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc, stage, yacc,
+    attend_reduce_list<T, LPR, PPL, YGM>(L, kb, vb, proxy, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc, stage, yacc,
                                         gacc);
     trace(52);
-    if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)part * PF);
+    if constexpr (YG) mma_write_partial<MT, 2>(yacc, gacc, R, d, yg + (size_t)part * PF);
     trace(57);
     float *s_acc = reinterpret_cast<float *>(stage);  // [nwarps][d]
     float *part_dst = L.attn_scratch + ((size_t)bh * attn_slots_dev(L, P) + part) * (size_t)(d + 2);
@@ -568,10 +575,12 @@ select_attend_kernel(const FArgs a) {
     m = -INFINITY;
     l = 0.f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) { yacc[i / 8][(i / 4) & 1][i & 3] = 0.f; gacc[i / 4][i & 3] = 0.f; }
+    for (int i = 0; i < MT * 8; ++i) yacc[i / 8][(i / 4) & 1][i & 3] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) gacc[i / 4][i & 3] = 0.f;
     if (nwin > kMmaRows) {
-        attend_reduce_list<T, LPR, PPL, YG>(L, kb, vb, proxy, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
-        if constexpr (YG) mma_write_partial<2, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
+        attend_reduce_list<T, LPR, PPL, YGM>(L, kb, vb, proxy, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
+        if constexpr (YG) mma_write_partial<MT, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
     } else {
         // a handful of rows: attention from registers; Y, G on the CUDA cores
         attend_list<T, LPR, PPL, 1>(kb, vb, s_list, nwin, qv, c, d, m, l, acc);  // compact code: few rows
@@ -606,8 +615,8 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
     const int packs = L.dim_stride / N;
     const int lpr = packs < 32 ? packs : 32;
     const int ppl = packs / lpr;
-    // the Y|G reduction rides along for the bf16 rank-32, d-128 layout
-    const bool yg = sizeof(T) == 2 && L.rank_stride == 32 && L.dim_stride == 128;
+    // the Y|G reduction rides along for the bf16 rank-32/64, d-128 layouts
+    const bool yg = sizeof(T) == 2 && (L.rank_stride == 32 || L.rank_stride == 64) && L.dim_stride == 128;
     const size_t ldk = (size_t)L.dim_stride * sizeof(T) + 16, lda = (size_t)L.rank_stride * 2 + 16;
     const size_t stage = 2 * (2 * kMmaRows * ldk + (yg ? kMmaRows * lda : 0));
     const size_t last = (size_t)kCritCap * 8 > stage ? (size_t)kCritCap * 8 : stage;  // crit sort reuses it
@@ -621,19 +630,22 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
         launch_kernel(fn, grid, kFThreads, smem, st, true, a);                                    \
     } while (0)
     if (yg && ppl == 1 && lpr == 16) {
-        if constexpr (sizeof(T) == 2) LRQK_F(16, 1, true);
+        if constexpr (sizeof(T) == 2) {
+            if (L.rank_stride == 64) LRQK_F(16, 1, 4);
+            else LRQK_F(16, 1, 2);
+        }
     } else if (ppl == 1) {
         switch (lpr) {
-            case 1: LRQK_F(1, 1, false); break;
-            case 2: LRQK_F(2, 1, false); break;
-            case 4: LRQK_F(4, 1, false); break;
-            case 8: LRQK_F(8, 1, false); break;
-            case 16: LRQK_F(16, 1, false); break;
-            case 32: LRQK_F(32, 1, false); break;
+            case 1: LRQK_F(1, 1, 0); break;
+            case 2: LRQK_F(2, 1, 0); break;
+            case 4: LRQK_F(4, 1, 0); break;
+            case 8: LRQK_F(8, 1, 0); break;
+            case 16: LRQK_F(16, 1, 0); break;
+            case 32: LRQK_F(32, 1, 0); break;
             default: return LRQK_EUNSUPPORTED;
         }
     } else if (ppl == 2 && lpr == 32) {
-        LRQK_F(32, 2, false);
+        LRQK_F(32, 2, 0);
     } else {
         return LRQK_EUNSUPPORTED;
     }

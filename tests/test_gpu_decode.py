@@ -427,3 +427,52 @@ def test_mixed_paths_in_one_step_keep_outputs_apart():
     st = ctypes.c_uint32(7)
     assert lib.lrqk_get_status(layer.ptr, ctypes.addressof(st), _lib.stream_ptr()) == 0
     assert st.value == 0
+
+
+@pytest.mark.parametrize("r", [32, 64])
+def test_fused_resident_reduction_matches_torch(r):
+    """The tensor-core Y = A_res^T K_res, G = A_res^T A_res that
+    select_attend accumulates while it attends (plus the finish kernel's
+    bin-D rows and slot sums) must equal a torch fp32 reduction over the
+    step's resident set: after a step, pre.W - B_Q = l2 Y and
+    pre.P - B_Q B_Q^T = l2 G (decode.py:84-108's resident terms)."""
+    from paper_2510_23649_b200.engine import prefill_factorize_device
+
+    torch.manual_seed(2)
+    B, Hq, Hkv, d, lb, kb, ctx = 1, 4, 1, 128, 16, 1024, 24000
+    dev = torch.device("cuda")
+    Qp = torch.randn(B * Hq, ctx, d, device=dev).to(torch.bfloat16)
+    Kp = torch.randn(B * Hkv, ctx, d, device=dev).to(torch.bfloat16)
+    Vp = torch.randn(B * Hkv, ctx, d, device=dev).to(torch.bfloat16)
+    res = prefill_factorize_device(Qp, Kp, r, dtype="bf16", group=Hq // Hkv)
+    layer = make_layer(B, Hq, Hkv, d, r, kb, lb, t_max=ctx + 16, dtype="bf16")
+    layer.load_prompt(res["A_K"].reshape(B, Hq, ctx, r), res["B_Q"].reshape(B, Hq, r, d),
+                      res["B_K"].reshape(B, Hq, r, d), Kp.view(B, Hkv, ctx, d), Vp.view(B, Hkv, ctx, d))
+    out = torch.zeros(B, Hq, d, device=dev)
+    R = layer.shape.rank_stride
+    total = (4 * R * R + 3 * R * d + 4 + 2 * d + 2 * R + 3) & ~3  # compress.cu pre_layout
+    offP, offW = 2 * R * R, 4 * R * R + 2 * R * d
+    for t in range(ctx, ctx + 3):
+        q = torch.randn(B, Hq, d, device=dev).to(torch.bfloat16)
+        k = torch.randn(B, Hkv, d, device=dev).to(torch.bfloat16)
+        v = torch.randn(B, Hkv, d, device=dev).to(torch.bfloat16)
+        layer.step(q, k, v, out)
+        torch.cuda.synchronize()
+        layer.raise_status()
+        if t == ctx:
+            continue  # the first step after the prompt takes the general path
+        pre = layer.buf["pre"].view(torch.float32)
+        A = layer.proxy_rows()[0].float()
+        Kr = layer.view("slow_k")[0].float()
+        BQ = layer.view("B_Q")[0]
+        cnt = layer.view("res_cnt")[0]
+        idx = layer.view("res_idx")[0]
+        for h in range(Hq):
+            sel = idx[h, : int(cnt[h])].long()
+            Ah, Kh = A[h][sel][:, :R], Kr[h // (Hq // Hkv)][sel]
+            Y, G = Ah.T @ Kh, Ah.T @ Ah
+            base = h * total
+            W = pre[base + offW: base + offW + R * d].view(R, d)
+            P = pre[base + offP: base + offP + R * R].view(R, R)
+            torch.testing.assert_close(W - BQ[h], Y, rtol=1e-4, atol=1e-3 * Y.abs().max().item())
+            torch.testing.assert_close(P - BQ[h] @ BQ[h].T, G, rtol=1e-4, atol=1e-3 * G.abs().max().item())
