@@ -1201,7 +1201,9 @@ static size_t prepare_finish_smem_bytes(const lrqk_layer_t &L) {
     const size_t d = L.dim_stride, R = L.rank_stride;
     const size_t ldB = d + 4, ldM = R + 4, RB = R / 4, NP = RB * (RB + 1) / 2;
     const size_t scratch = 4 * NP * 16 > 4 * d + 2 * R ? 4 * NP * 16 : 4 * d + 2 * R;
-    return (2 * R * ldB + 2 * R * ldM + scratch) * sizeof(float);
+    const size_t main = 2 * R * ldB + 2 * R * ldM + scratch;
+    const size_t small_yg = (size_t)kMmaRows * (d + R);  // yg_rows_small's fp32 staging of the bin-D rows
+    return (main > small_yg ? main : small_yg) * sizeof(float);
 }
 
 // ---------------------------------------------------------------------------

@@ -615,8 +615,9 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
     const int packs = L.dim_stride / N;
     const int lpr = packs < 32 ? packs : 32;
     const int ppl = packs / lpr;
-    // the Y|G reduction rides along for the bf16 rank-32/64, d-128 layouts
-    const bool yg = sizeof(T) == 2 && (L.rank_stride == 32 || L.rank_stride == 64) && L.dim_stride == 128;
+    // the Y|G reduction rides along for the bf16 rank-16/32/64, d-128 layouts
+    const bool yg = sizeof(T) == 2 && (L.rank_stride == 16 || L.rank_stride == 32 || L.rank_stride == 64) &&
+                    L.dim_stride == 128;
     const size_t ldk = (size_t)L.dim_stride * sizeof(T) + 16, lda = (size_t)L.rank_stride * 2 + 16;
     const size_t stage = 2 * (2 * kMmaRows * ldk + (yg ? kMmaRows * lda : 0));
     const size_t last = (size_t)kCritCap * 8 > stage ? (size_t)kCritCap * 8 : stage;  // crit sort reuses it
@@ -632,7 +633,8 @@ static int launch_select_attend_t(const FArgs &a, cudaStream_t st) {
     if (yg && ppl == 1 && lpr == 16) {
         if constexpr (sizeof(T) == 2) {
             if (L.rank_stride == 64) LRQK_F(16, 1, 4);
-            else LRQK_F(16, 1, 2);
+            else if (L.rank_stride == 32) LRQK_F(16, 1, 2);
+            else LRQK_F(16, 1, 1);
         }
     } else if (ppl == 1) {
         switch (lpr) {

@@ -429,7 +429,7 @@ def test_mixed_paths_in_one_step_keep_outputs_apart():
     assert st.value == 0
 
 
-@pytest.mark.parametrize("r", [32, 64])
+@pytest.mark.parametrize("r", [16, 32, 64])
 def test_fused_resident_reduction_matches_torch(r):
     """The tensor-core Y = A_res^T K_res, G = A_res^T A_res that
     select_attend accumulates while it attends (plus the finish kernel's
