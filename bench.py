@@ -281,6 +281,7 @@ def run_ours(args, world, rank, local):
     time.sleep(0.3)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    miss0 = eng.counters()[0].sum().item()  # cumulative c_miss over layers (CacheStats)
     if world > 1:
         dist.barrier()
     start.record()
@@ -293,6 +294,10 @@ def run_ours(args, world, rank, local):
         dist.barrier()
     clock_info = clocks.stop()
     ms = start.elapsed_time(stop)
+    # miss transfers of the timed steps: with the host slow tier every miss is
+    # one K row + one V row read from pinned host memory over PCIe (K5b)
+    misses = eng.counters()[0].sum().item() - miss0
+    miss_bytes = misses * 2 * d * (2 if w["dtype"] == "bf16" else 4)
     eng.raise_status()
     t_now = int(eng.ctx[0].item())
     # selection path statistics (head-steps per mode, since the prompt)
@@ -395,6 +400,11 @@ def run_ours(args, world, rank, local):
                       algorithmic_bytes_per_launch=score_bytes, avg_launch_ms=round(score_ms, 5),
                       step_frac_of_hbm=round(step_gbs / hbm_peak, 4), step_algorithmic_GBps=round(step_gbs, 1),
                       peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"),
+        miss_transfers=dict(misses_per_step=round(misses / max(args.steps, 1), 1),
+                            bytes_per_step=int(miss_bytes / max(args.steps, 1)),
+                            host_tier_GBps=round(miss_bytes / (ms / 1e3) / 1e9, 2) if args.policy == "host" else None,
+                            note="host policy: K5b zero-copy PCIe reads of the missed K/V rows; "
+                                 "HBM policy: misses are counted, the rows are already in HBM"),
         e2e=dict(value=round(e2e_tok_s, 3), unit="tokens/s", h2d_bytes_per_step=int(h2d),
                  d2h_bytes_per_step=int(d2h), steps=e2e_steps,
                  path="Engine public API: pinned host q/k/v -> H2D -> graph replay -> D2H outputs"),
