@@ -82,7 +82,9 @@ typedef struct lrqk_layer {
     void *slow_k, *slow_v;         /* [B,Hkv,t_max,dim_stride] dtype (device or mapped host) */
     void *slot_k, *slot_v;         /* [B,Hq,n_slots,dim_stride] dtype (host policy only)     */
     int32_t *ctx_len;              /* [B] tokens stored; the new token gets index ctx_len[b]  */
-    int32_t *res_idx;              /* [B,Hq,s_cap] fast-tier index set, ascending            */
+    int32_t *res_idx;              /* [B,Hq,s_cap] fast-tier index set Omega_t: ascending under   */
+                                   /* LRQK_SLOW_HOST; under LRQK_SLOW_HBM unordered (certain     */
+                                   /* winners | threshold-bin winners | lite window)            */
     int32_t *res_slot;             /* [B,Hq,s_cap] slot of each resident row (host policy)   */
     int32_t *res_cnt;              /* [B,Hq]                                                 */
     int32_t *spare_slot;           /* [B,Hq] free slot that receives the next appended row   */
@@ -96,7 +98,7 @@ typedef struct lrqk_layer {
     float *eta;                    /* [B,Hq,2] line-search steps (eta_Q, eta_K) */
     uint32_t *keys;                /* [B,Hq,t_max] order-preserving score keys */
     uint32_t *hist;                /* [B,Hq,3,2048] coarse | fine / part counts | hint window (zero between steps) */
-    int32_t *sel_meta;             /* [B,Hq,32] selection state (incl. the persistent threshold hint) */
+    int32_t *sel_meta;             /* [B,Hq,48] selection state (incl. the persistent threshold hint; common.cuh Meta) */
     int32_t *sure_idx;             /* [B,Hq,select_parts,k_budget]            */
     uint64_t *cand;                /* [B,Hq,cand_cap]                          */
     float *red_scratch;            /* [B,Hq,red_chunks,rank_stride*(rank_stride+1)] */

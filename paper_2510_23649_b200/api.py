@@ -680,8 +680,12 @@ class DecodeSession:
         old = self._layer
         new = self._alloc(2 * old.shape.t_max)
         t = self._t
-        for nm in ("B_Q", "B_K", "res_idx", "res_cnt", "c_miss", "c_total", "ctx_len"):
+        for nm in ("B_Q", "B_K", "res_idx", "res_cnt", "c_miss", "c_total", "ctx_len", "sel_meta"):
             new.view(nm).copy_(old.view(nm))
+        # the residency bitmap of Omega_{t-1}: the next step's hit/miss count
+        # reads it (compress.cu count_hits_hbm); its per-head stride grows
+        ow = old.view("res_bits").shape[-1]
+        new.view("res_bits")[..., :ow].copy_(old.view("res_bits"))
         new.view("slow_k")[:, :, :t].copy_(old.view("slow_k")[:, :, :t])
         new.view("slow_v")[:, :, :t].copy_(old.view("slow_v")[:, :, :t])
         tl = (t + 31) // 32
@@ -702,9 +706,17 @@ class DecodeSession:
         kd = pad_last(_f32(step.k, dev), ds).contiguous()
         vd = pad_last(_f32(step.v, dev), ds).contiguous()
         out = torch.zeros(1, 1, ds, dtype=torch.float32, device=dev)
+        snap = L.snapshot()
         L.step(qd, kd, vd, out, advance=True)
         torch.cuda.synchronize()
-        L.raise_status()
+        try:
+            L.raise_status()
+        except (NonFiniteError, SolveFailedError, IndexError, RuntimeError):
+            # a failed step leaves the session as it was, like the reference,
+            # which raises before it mutates any state (session.py:94-101)
+            L.restore(snap)
+            torch.cuda.synchronize()
+            raise
         t = self._t
         self._t += 1
         n = int(L.view("res_cnt")[0, 0])

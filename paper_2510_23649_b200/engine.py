@@ -192,6 +192,8 @@ class LayerState:
             "eta": (torch.float32, (B, Hq, 2)),
             "keys": (torch.int32, (B, Hq, T)),
             "status": (torch.int32, (1,)),
+            "res_bits": (torch.int32, (B, Hq, (T + 31) // 32)),
+            "sel_meta": (torch.int32, (B, Hq, 48)),
         }[name]
         dt, shp = spec
         if name in self.host_tiers:
@@ -234,6 +236,20 @@ class LayerState:
         if st & _lib.ST_CAPACITY:
             raise RuntimeError("LRQK store capacity (t_max) exhausted")
         return st
+
+    # ---- step atomicity (the reference raises before mutating a session) ------
+    STEP_STATE = ("B_Q", "B_K", "ctx_len", "res_idx", "res_slot", "res_cnt", "spare_slot", "c_miss", "c_total",
+                  "step_miss", "step_total", "res_bits", "sel_meta", "pre", "eta")
+
+    def snapshot(self):
+        """Device copies of every persistent buffer a decode step mutates
+        (the appended rows are not included: the step's ctx_len is restored,
+        so they are overwritten by the next append)."""
+        return {nm: self.buf[nm].clone() for nm in self.STEP_STATE if nm in self.buf}
+
+    def restore(self, snap):
+        for nm, t in snap.items():
+            self.buf[nm].copy_(t)
 
     # ---- prompt ----------------------------------------------------------------
     def load_prompt(self, A_K, B_Q, B_K, K, V):

@@ -19,97 +19,16 @@ import pytest
 import torch
 
 from oracle import lrqk_oracle as O
-from tests.lrqk_testlib import make_layer, near_tie_ok, quantize, rows_dev, seed_layer
+from tests.lrqk_testlib import (ParityLog, StepLocked, check_scores_on_device, keys_to_scores, make_layer, quantize,
+                                rows_dev, seed_layer)
 
 pytestmark = pytest.mark.gpu
 
 RTOL = {"f32": 1e-4, "bf16": 2e-2}
 
 
-def _gpu_state(layer, b, h, t):
-    g = h // layer.shape.group
-    d, r = layer.shape.head_dim, layer.shape.rank
-    n = int(layer.view("res_cnt")[b, h])
-    res = np.sort(layer.view("res_idx")[b, h, :n].cpu().numpy().astype(np.int64))
-    K = layer.view("slow_k")[b, g, :t, :d].float().cpu().numpy().astype(np.float64)
-    V = layer.view("slow_v")[b, g, :t, :d].float().cpu().numpy().astype(np.float64)
-    P = layer.proxy_rows()[b, h, :t, :r].float().cpu().numpy().astype(np.float64)
-    BQ = layer.view("B_Q")[b, h, :r, :d].cpu().numpy().astype(np.float64)
-    BK = layer.view("B_K")[b, h, :r, :d].cpu().numpy().astype(np.float64)
-    return res, K, V, P, BQ, BK
-
-
 def _keys_to_scores(keys_u32):
-    k = keys_u32.astype(np.uint32)
-    u = np.where(k & 0x80000000, k & 0x7FFFFFFF, ~k & 0xFFFFFFFF).astype(np.uint32)
-    return u.view(np.float32).astype(np.float64)
-
-
-def run_step_locked(layer, Q, K, V, prompt, steps, dtype, kb, lb, rtol_hat=2e-3, tie_eps=None):
-    """Q [B,Hq,T,d], K/V [B,Hkv,T,d] float64 (already storage-representable)."""
-    sh = layer.shape
-    B, Hq = sh.batch, sh.n_q_heads
-    d = sh.head_dim
-    out = torch.zeros(B, Hq, sh.dim_stride, dtype=torch.float32, device="cuda")
-    stats = dict(ties=0, steps=0)
-    for t in range(prompt, prompt + steps):
-        before = {}
-        for b in range(B):
-            for h in range(Hq):
-                before[(b, h)] = _gpu_state(layer, b, h, t)
-        q = rows_dev(Q[:, :, t], layer)
-        k = rows_dev(K[:, :, t], layer)
-        v = rows_dev(V[:, :, t], layer)
-        layer.step(q, k, v, out, advance=True)
-        torch.cuda.synchronize()
-        layer.raise_status()
-        res_cnt = layer.view("res_cnt").cpu().numpy()
-        res_idx = layer.view("res_idx").cpu().numpy()
-        keys = layer.view("keys").cpu().numpy().view(np.uint32)
-        qh = layer.view("q_hat").cpu().numpy().astype(np.float64)
-        kh = layer.view("k_hat").cpu().numpy().astype(np.float64)
-        miss = layer.view("step_miss").cpu().numpy()
-        tot = layer.view("step_total").cpu().numpy()
-        outs = out.cpu().numpy().astype(np.float64)
-        for b in range(B):
-            for h in range(Hq):
-                g = h // sh.group
-                res, Kh, Vh, Ph, BQ, BK = before[(b, h)]
-                st = O.HeadState(K=Kh, V=Vh, proxy=Ph, B_Q=BQ, B_K=BK, resident=res, k_budget=kb,
-                                 lite_budget=lb)
-                qr, kr, vr = quantize(Q[b, h, t], dtype), quantize(K[b, g, t], dtype), quantize(V[b, g, t], dtype)
-                ref = O.head_step(st, qr, kr, vr)
-                # compression outputs
-                np.testing.assert_allclose(qh[b, h, : sh.rank], ref.q_hat.ravel(), rtol=rtol_hat,
-                                           atol=rtol_hat * np.abs(ref.q_hat).max())
-                np.testing.assert_allclose(kh[b, h, : sh.rank], ref.k_hat.ravel(), rtol=rtol_hat,
-                                           atol=rtol_hat * np.abs(ref.k_hat).max())
-                # selection: exact w.r.t. the GPU's own scores
-                n = int(res_cnt[b, h])
-                got = np.sort(res_idx[b, h, :n].astype(np.int64))  # HBM policy: unordered
-                gscores = _keys_to_scores(keys[b, h, : t + 1])
-                _, _, exact = O.select(gscores, t, kb, lb)
-                np.testing.assert_array_equal(got, exact)
-                # ... and equal to the fp64 oracle except at near-ties
-                lite_lo = max(0, t + 1 - lb)
-                k_eff = min(kb, lite_lo)
-                eps = tie_eps if tie_eps is not None else 1e-4 * (np.abs(ref.scores).max() + 1e-30)
-                ok, nd = near_tie_ok(ref.scores[:lite_lo], got[got < lite_lo], ref.omega[ref.omega < lite_lo],
-                                     k_eff, eps)
-                assert ok, f"selection differs beyond near-ties at t={t} (b={b}, h={h}, {nd} indices)"
-                stats["ties"] += nd
-                # counters: the reference replay rule on the GPU's own selection
-                prev = set(res.tolist()) | {t}
-                assert int(miss[b, h]) == len(set(got.tolist()) - prev)
-                assert int(tot[b, h]) == len(got)
-                # attention on the identical index set
-                K_all = np.vstack([Kh, kr])
-                V_all = np.vstack([Vh, vr])
-                want, _ = O.attend(qr, K_all[got], V_all[got])
-                np.testing.assert_allclose(outs[b, h, :d], want.ravel(), rtol=RTOL[dtype],
-                                           atol=RTOL[dtype] * np.abs(want).max())
-        stats["steps"] += 1
-    return stats
+    return keys_to_scores(keys_u32)
 
 
 def _session_case(i):
@@ -176,9 +95,16 @@ def test_step_locked_parity(dtype, cfg):
             BK[b, h] = run.factors.B_K
     layer = make_layer(B, Hq, Hkv, d, r, cfg["kb"], cfg["lb"], t_max=T + 4, dtype=dtype)
     seed_layer(layer, A_K, BQ, BK, K[:, :, :l], V[:, :, :l])
-    stats = run_step_locked(layer, Q, K, V, l, cfg["steps"], dtype, cfg["kb"], cfg["lb"],
-                            rtol_hat=2e-3 if dtype == "f32" else 5e-2)
-    assert stats["steps"] == cfg["steps"]
+    lock = StepLocked(layer, Q, K, V, l)
+    log = ParityLog(f"small_{dtype}_{B}x{Hq}x{d}")
+    out = torch.zeros(B, Hq, layer.shape.dim_stride, dtype=torch.float32, device="cuda")
+    for t in range(l, T):
+        layer.step(rows_dev(Q[:, :, t], layer), rows_dev(K[:, :, t], layer), rows_dev(V[:, :, t], layer), out)
+        torch.cuda.synchronize()
+        layer.raise_status()
+        lock.check_step(out, log, dtype, rtol_hat=2e-3 if dtype == "f32" else 5e-2)
+    log.write()
+    assert log.rec["steps"] == cfg["steps"]
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -256,6 +182,7 @@ def test_selection_exact_at_long_context(kind):
         layer.step(rows_dev(Q[:, :, t], layer), rows_dev(K[:, :, t], layer), rows_dev(V[:, :, t], layer), out)
         torch.cuda.synchronize()
         layer.raise_status()
+        check_scores_on_device(layer, t)
         _select_exact_check(layer, t, kb, lb)
 
 
@@ -291,6 +218,7 @@ def test_selection_exact_with_prefill_factors(ctx):
         assert (cnt == kb + lb).all()
         assert idx.min() >= 0 and idx.max() <= t
         layer.raise_status()
+        check_scores_on_device(layer, t)
         _select_exact_check(layer, t, kb, lb)
 
 
@@ -365,6 +293,7 @@ def test_rank_topk_sweep_selection_and_output(r, kb):
         layer.step(q, k, v, out)
         torch.cuda.synchronize()
         layer.raise_status()
+        check_scores_on_device(layer, t)
         _select_exact_check(layer, t, kb, lb)
         Kall = torch.cat([Kall, k.float()[:, :, None]], 2)
         Vall = torch.cat([Vall, v.float()[:, :, None]], 2)
@@ -406,6 +335,7 @@ def test_mixed_paths_in_one_step_keep_outputs_apart():
         layer.step(q, k, v, out)
         torch.cuda.synchronize()
         layer.raise_status()
+        check_scores_on_device(layer, t)
         _select_exact_check(layer, t, kb, lb)
         Kall = torch.cat([Kall, k.float()[:, :, None]], 2)
         Vall = torch.cat([Vall, v.float()[:, :, None]], 2)
@@ -459,6 +389,7 @@ def test_fused_resident_reduction_matches_torch(r):
         layer.step(q, k, v, out)
         torch.cuda.synchronize()
         layer.raise_status()
+        check_scores_on_device(layer, t)
         if t == ctx:
             continue  # the first step after the prompt takes the general path
         pre = layer.buf["pre"].view(torch.float32)
