@@ -221,6 +221,46 @@ int lrqk_count_misses(const int32_t *resident, int32_t n_resident, const int32_t
 int lrqk_line_search(const float *x_hat, const float *B, const float *x, int32_t n_heads, int32_t rank,
                      int32_t dim, float *B_out, float *grad, float *eta, void *stream);
 
+/* ---- float64 dense kernels of the drop-in linear algebra ------------------
+ * The reference computes these in float64 (numpy / LAPACK); so do these
+ * kernels, so the per-call drop-in functions (gram, solve_spd, fro_norm_sq,
+ * update_B/AK/AQ, lagrangian_value, factor_residuals, khat_initial_guess,
+ * update_qhat/khat, topk_indices) agree with it to rounding.  Row-major,
+ * device pointers, caller-allocated outputs and workspaces. */
+
+/* C = alpha op(A) op(B) + beta C; op = transpose when trans_* != 0.
+ * work (may be NULL: no split-K) of lrqk_gemm_f64_workspace() bytes.
+ * ref: the `@` products of prefill.py:142-181, decode.py:79-119. */
+int lrqk_gemm_f64(int32_t trans_a, int32_t trans_b, int32_t m, int32_t n, int32_t k, double alpha, const double *A,
+                  int32_t lda, const double *B, int32_t ldb, double beta, double *C, int32_t ldc, void *work,
+                  size_t work_bytes, void *stream);
+size_t lrqk_gemm_f64_workspace(int32_t m, int32_t n, int32_t k);
+
+/* Copy the strict upper triangle of the r x r matrix G onto the lower one
+ * (gram's exact symmetry, linalg.py:48-55). */
+int lrqk_symmetrize_f64(double *G, int32_t r, int32_t ldg, void *stream);
+
+/* *out = sum a[i] b[i] (device scalar), fixed reduction order; work >= 256
+ * doubles.  ref: fro_norm_sq linalg.py:58-60 and the Gram-trace inner
+ * products of lagrangian_value prefill.py:150-153. */
+int lrqk_dot_f64(const double *a, const double *b, int64_t n, double *out, double *work, void *stream);
+
+/* y = alpha * (*alpha_scale if non-NULL) * x + beta * y. */
+int lrqk_axpby_f64(int64_t n, double alpha, const double *alpha_scale, const double *x, double beta, double *y,
+                   void *stream);
+
+/* X M = RHS for X (n x r), M r x r symmetric positive (semi)definite, lower
+ * triangle read.  Cholesky; on failure one retry with 1e-10 (tr(M)/r + 1) on
+ * the diagonal (sets LRQK_ST_JITTERED); still failing -> LRQK_ST_SOLVE_FAILED
+ * and X untouched; non-finite M or RHS -> LRQK_ST_NONFINITE.  work: r*r + 1
+ * doubles.  ref: solve_spd linalg.py:63-93. */
+int lrqk_solve_spd_f64(const double *M, int32_t r, int32_t ldm, const double *RHS, int32_t n, int32_t ldr, double *X,
+                       int32_t ldx, double *work, uint32_t *status, void *stream);
+
+/* Indices of the k largest of n float64 scores, ascending, ties toward the
+ * lower index (k < n; out holds k ints).  ref: topk_indices linalg.py:96-110. */
+int lrqk_topk_f64(const double *scores, int32_t n, int32_t k, int32_t *out, void *stream);
+
 /* ---- prefill factorisation (ref: prefill.py:197-230) ---- */
 typedef struct lrqk_prefill {
     int32_t n_heads;        /* independent (Q,K) problems                     */

@@ -36,9 +36,14 @@ from .api import (
     decode_compress,
     exact_attention,
     exact_topk,
+    factor_residuals,
     fetch_and_merge,
+    fro_norm_sq,
+    gram,
     importance_scores,
     init_factors,
+    khat_initial_guess,
+    lagrangian_value,
     miss_rate,
     prefill_factorize,
     prefill_run,
@@ -46,9 +51,15 @@ from .api import (
     run_simulation,
     select_active,
     selection_recall,
+    solve_spd,
     summarize,
     topk_indices,
+    update_AK,
+    update_AQ,
+    update_B,
+    update_khat,
     update_projections,
+    update_qhat,
     write_report_csv,
     write_stats_csv,
 )

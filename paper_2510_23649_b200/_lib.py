@@ -100,6 +100,14 @@ SIGNATURES = {
     "lrqk_attention_rows": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "lrqk_count_misses": (C.c_int, [_P, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P]),
     "lrqk_line_search": (C.c_int, [_P, _P, _P, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P, _P]),
+    "lrqk_gemm_f64": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double, _P, C.c_int32,
+                                _P, C.c_int32, C.c_double, _P, C.c_int32, _P, C.c_size_t, _P]),
+    "lrqk_gemm_f64_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+    "lrqk_symmetrize_f64": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),
+    "lrqk_dot_f64": (C.c_int, [_P, _P, C.c_int64, _P, _P, _P]),
+    "lrqk_axpby_f64": (C.c_int, [C.c_int64, C.c_double, _P, _P, C.c_double, _P, _P]),
+    "lrqk_solve_spd_f64": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P, C.c_int32, _P, _P, _P]),
+    "lrqk_topk_f64": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
     "lrqk_trace_enable": (C.c_int, [C.c_int]),
     "lrqk_trace_read": (C.c_int, [_P, C.c_int]),
 }

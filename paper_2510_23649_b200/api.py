@@ -9,15 +9,19 @@ float64 numpy arrays like the reference's.  Without the CUDA library or a
 device every call raises LibraryUnavailable -- there is no CPU fallback.
 
 Implemented entry points and the kernels behind them:
-  prefill_run / prefill_factorize  -> lrqk_prefill_factorize   (prefill.py:197-230)
+  gram, fro_norm_sq, solve_spd      -> float64 dense kernels (dense.cu)     (linalg.py:48-93)
+  topk_indices, select_active       -> lrqk_topk_f64 (exact float64 order) (linalg.py:96-110, cache.py:149-171)
+  update_B, update_AK, update_AQ,
+  lagrangian_value, factor_residuals -> float64 dense kernels               (prefill.py:142-181, 239-253)
+  prefill_run / prefill_factorize  -> lrqk_prefill_factorize (K1)          (prefill.py:197-230)
   init_factors, importance_scores  -> host initialisation, as the reference (prefill.py:108-139)
-  decode_compress                  -> lrqk_compress_prepare + lrqk_decode_compress (decode.py:122-147)
-  update_projections               -> B update of the same kernel    (decode.py:169-184)
-  proxy_scores                     -> lrqk_proxy_scores_f32          (cache.py:141-146)
-  select_active, topk_indices      -> lrqk_select_scores             (cache.py:149-171, linalg.py:96-110)
-  fetch_and_merge                  -> lrqk_count_misses              (cache.py:174-196)
-  exact_attention, exact_topk      -> lrqk_attention_rows / select   (attention.py:23-41)
-  DecodeSession, run_simulation    -> the fused per-layer decode step (session.py:62-165)
+  khat_initial_guess, update_qhat,
+  update_khat, decode_compress,
+  update_projections               -> float64 dense kernels               (decode.py:79-184)
+  proxy_scores                     -> lrqk_proxy_scores_f32 (K3 arithmetic) (cache.py:141-146)
+  fetch_and_merge                  -> lrqk_count_misses                    (cache.py:174-196)
+  exact_attention, exact_topk      -> lrqk_attention_rows / gemm + topk     (attention.py:23-41)
+  DecodeSession, run_simulation    -> the fused per-layer decode step (K2-K6) (session.py:62-165)
 """
 
 from __future__ import annotations
@@ -32,6 +36,7 @@ import torch
 
 from . import _lib
 from .engine import LayerShape, LayerState, pad_last, pow2_at_least, prefill_factorize_device
+from . import dense as D
 from .errors import NonFiniteError, SolveFailedError
 
 INIT_KINDS = ("randn", "top", "topcol")
@@ -75,6 +80,42 @@ def as_row(a, name: str = "row") -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# dense kernels (ref: linalg.py:48-93), float64 on the device (dense.cu)
+# ---------------------------------------------------------------------------
+def gram(A) -> np.ndarray:
+    """A^T A, exactly symmetric (ref: linalg.py:48-55)."""
+    A = np.asarray(A, dtype=np.float64)
+    if A.size == 0:
+        raise ValueError("gram requires a nonempty matrix")
+    return D.np64(D.gram(D.t64(A)))
+
+
+def fro_norm_sq(A) -> float:
+    """Sum of squared entries (ref: linalg.py:58-60)."""
+    a = D.t64(np.asarray(A, dtype=np.float64).ravel())
+    if a.numel() == 0:
+        return 0.0
+    return float(D.dot(a, a).item())
+
+
+def solve_spd(M, RHS) -> np.ndarray:
+    """X with X M = RHS, Cholesky with one jittered retry (ref: linalg.py:63-93)."""
+    M = np.asarray(M, dtype=np.float64)
+    RHS = np.asarray(RHS, dtype=np.float64)
+    r = M.shape[0]
+    if M.ndim != 2 or M.shape[1] != r or RHS.ndim != 2 or RHS.shape[1] != r:
+        # the reference validates finiteness before shapes (linalg.py:71-78)
+        if not np.isfinite(M).all():
+            raise NonFiniteError("solve_spd: M contains non-finite entries")
+        if not np.isfinite(RHS).all():
+            raise NonFiniteError("solve_spd: RHS contains non-finite entries")
+        if M.ndim != 2 or M.shape[1] != r:
+            raise ValueError(f"M must be square, got {M.shape}")
+        raise ValueError(f"RHS has {RHS.shape[1] if RHS.ndim == 2 else RHS.shape} cols, expected {r}")
+    return D.np64(D.solve_spd(D.t64(M), D.t64(RHS)))
+
+
+# ---------------------------------------------------------------------------
 # selection (ref: linalg.py:96-110, cache.py:149-171)
 # ---------------------------------------------------------------------------
 def _select_device(scores_2d: torch.Tensor, t: int, k_budget: int, lite_budget: int):
@@ -92,22 +133,16 @@ def _select_device(scores_2d: torch.Tensor, t: int, k_budget: int, lite_budget: 
 
 
 def topk_indices(scores, k: int) -> np.ndarray:
-    """Indices of the k largest scores, ascending; ties toward the lower index."""
+    """Indices of the k largest scores, ascending; ties toward the lower index
+    (ref: linalg.py:96-110).  Selected on the device over order-preserving
+    64-bit keys of the float64 scores, so the order is the reference's."""
     if k < 1:
         raise ValueError(f"k must be >= 1, got {k}")
     s = np.asarray(scores, dtype=np.float64).ravel()
     n = s.shape[0]
     if k >= n:
         return np.arange(n)
-    # one extra token fills the (mandatory) lite window, so omega_k is the
-    # plain top-k over the n real scores
-    dev = _dev()
-    padded = torch.empty(1, n + 1, dtype=torch.float32, device=dev)
-    padded[0, :n] = _f32(s, dev)
-    padded[0, n] = float("-inf")
-    omega, cnt = _select_device(padded, n, k, 1)
-    got = omega[0, : int(cnt[0])].cpu().numpy().astype(np.int64)
-    return got[got < n]
+    return D.topk(D.t64(s), k).cpu().numpy().astype(np.int64)
 
 
 @dataclass
@@ -118,13 +153,19 @@ class SelectionSet:
 
 
 def select_active(scores, t: int, k_budget: int, lite_budget: int) -> SelectionSet:
+    """ref: cache.py:149-171 -- lite window [max(0, t+1-lite), t] plus the
+    top-k (float64 order, device select) of the scores before it."""
     s = np.asarray(scores, dtype=np.float64).ravel()
     if s.shape[0] != t + 1:
         raise ValueError(f"scores must cover tokens 0..{t}, got {s.shape[0]}")
-    omega, cnt = _select_device(_f32(s[None, :]), t, k_budget, lite_budget)
-    om = omega[0, : int(cnt[0])].cpu().numpy().astype(np.intp)
     lite_start = max(0, t + 1 - lite_budget)
-    return SelectionSet(omega_k=om[om < lite_start], omega_l=om[om >= lite_start], omega=om)
+    omega_l = np.arange(lite_start, t + 1)
+    if lite_start == 0:
+        omega_k = np.arange(0)
+    else:
+        omega_k = topk_indices(s[:lite_start], min(k_budget, lite_start))
+    return SelectionSet(omega_k=omega_k.astype(np.intp), omega_l=omega_l,
+                        omega=np.concatenate([omega_k, omega_l]).astype(np.intp))
 
 
 # ---------------------------------------------------------------------------
@@ -178,11 +219,23 @@ def exact_attention(q, K, V) -> AttentionResult:
     return AttentionResult(output=_np64(out[:, :d]), weights=_np64(w[0]))
 
 
+def _exact_topk_dev(q64: torch.Tensor, K64: torch.Tensor, k: int) -> np.ndarray:
+    """Top-k of raw q K^T (float64 GEMM + float64 select on the device)."""
+    n = K64.shape[0]
+    if k >= n:
+        return np.arange(n)
+    s = D.gemm(K64, q64, tb=True).reshape(-1)
+    return D.topk(s, k).cpu().numpy().astype(np.int64)
+
+
 def exact_topk(q, K, k: int) -> np.ndarray:
+    """ref: attention.py:37-41."""
     K = np.asarray(K, dtype=np.float64)
     if K.shape[0] == 0:
         raise ValueError("exact_topk requires at least one key")
-    return topk_indices(proxy_scores(np.asarray(q).reshape(1, -1), K), k)
+    if k < 1:
+        raise ValueError(f"k must be >= 1, got {k}")
+    return _exact_topk_dev(D.t64(np.asarray(q).reshape(1, -1)), D.t64(K), k)
 
 
 def selection_recall(proxy, exact) -> float:
@@ -319,6 +372,76 @@ def prefill_factorize(Q, K, cfg: PrefillConfig) -> LowRankFactors:
     return prefill_run(Q, K, cfg).factors
 
 
+# The per-call prefill algebra of the reference, float64 on the device.  The
+# fused K1 pass (prefill_run above) computes the same quantities re-associated
+# in one stream over Q and K per sweep; these are the reference's individual
+# entry points with its exact association (prefill.py:142-181, 239-253).
+def _lagrangian_terms(Qd, Kd, f):
+    """Device scalars: sum(GQ o GK), cross, approx (ref: prefill.py:150-153)."""
+    GQ, GK = D.gram(Qd), D.gram(Kd)
+    AQ, AK = D.t64(f.A_Q), D.t64(f.A_K)
+    CQ, CK = D.gemm(Qd, AQ, ta=True), D.gemm(Kd, AK, ta=True)
+    return D.dot(GQ, GK), D.dot(CQ, CK), D.dot(D.gram(AQ), D.gram(AK)), AQ, AK
+
+
+def lagrangian_value(Q, K, f: LowRankFactors, cfg: PrefillConfig) -> float:
+    """Objective through d x d / r x r Gram traces (ref: prefill.py:142-158)."""
+    Q, K = np.asarray(Q, dtype=np.float64), np.asarray(K, dtype=np.float64)
+    Qd, Kd = D.t64(Q), D.t64(K)
+    qq, cross, approx, AQ, AK = _lagrangian_terms(Qd, Kd, f)
+    rq = D.residual_sq(Qd, AQ, D.t64(f.B_Q))
+    rk = D.residual_sq(Kd, AK, D.t64(f.B_K))
+    qq, cross, approx, rq, rk = (float(x.item()) for x in (qq, cross, approx, rq, rk))
+    qk_term = max(qq - 2.0 * cross + approx, 0.0)
+    return 0.5 * qk_term + 0.5 * cfg.lambda_q * rq + 0.5 * cfg.lambda_k * rk
+
+
+def update_B(A, X) -> np.ndarray:
+    """B = (A^T A)^-1 A^T X (ref: prefill.py:161-163)."""
+    Ad, Xd = D.t64(A), D.t64(X)
+    return D.np64(D.solve_spd(D.gram(Ad), D.gemm(Xd, Ad, ta=True))).T.copy()
+
+
+def _update_A(X_other, X_self, A_other, B_self, lam):
+    """X_self (X_other^T A_other + lam B_self^T) (gram(A_other) + lam gram(B_self^T))^-1."""
+    Xo, Xs, Ao = D.t64(X_other), D.t64(X_self), D.t64(A_other)
+    BT = D.t64(np.ascontiguousarray(np.asarray(B_self, dtype=np.float64).T))
+    T = D.gemm(Xo, Ao, ta=True)
+    D.axpby(lam, BT, 1.0, T)
+    rhs = D.gemm(Xs, T)
+    M = D.gram(Ao)
+    D.axpby(lam, D.gram(BT), 1.0, M)
+    return D.np64(D.solve_spd(M, rhs))
+
+
+def update_AK(Q, K, f: LowRankFactors, cfg: PrefillConfig) -> np.ndarray:
+    """Closed-form A_K (ref: prefill.py:166-172)."""
+    return _update_A(Q, K, f.A_Q, f.B_K, cfg.lambda_k)
+
+
+def update_AQ(Q, K, f: LowRankFactors, cfg: PrefillConfig) -> np.ndarray:
+    """Closed-form A_Q (ref: prefill.py:175-181)."""
+    return _update_A(K, Q, f.A_K, f.B_Q, cfg.lambda_q)
+
+
+def _rel(num_sq: float, den_sq: float) -> float:
+    if den_sq == 0.0:
+        return 0.0 if num_sq == 0.0 else float("inf")
+    return float(np.sqrt(num_sq / den_sq))
+
+
+def factor_residuals(Q, K, f: LowRankFactors) -> tuple:
+    """Relative reconstruction errors of Q, K and Q K^T (ref: prefill.py:239-253)."""
+    Q, K = np.asarray(Q, dtype=np.float64), np.asarray(K, dtype=np.float64)
+    Qd, Kd = D.t64(Q), D.t64(K)
+    den, cross, approx, AQ, AK = _lagrangian_terms(Qd, Kd, f)
+    rq = D.residual_sq(Qd, AQ, D.t64(f.B_Q))
+    rk = D.residual_sq(Kd, AK, D.t64(f.B_K))
+    q2, k2 = D.dot(Qd, Qd), D.dot(Kd, Kd)
+    den, cross, approx, rq, rk, q2, k2 = (float(x.item()) for x in (den, cross, approx, rq, rk, q2, k2))
+    return _rel(rq, q2), _rel(rk, k2), _rel(max(den - 2.0 * cross + approx, 0.0), den)
+
+
 # ---------------------------------------------------------------------------
 # decode compression (ref: decode.py)
 # ---------------------------------------------------------------------------
@@ -357,9 +480,8 @@ class CompressedToken:
 
 @dataclass
 class DecodeWorkspace:
-    """The reference's per-step intermediates.  The GPU path keeps the step
-    sizes and gradients (rank-1: x_hat^T resid); the normal-system matrices
-    live on the device only and are left as None."""
+    """Intermediates of the last step: the q-side normal system (m_lq, M_rq),
+    the B gradients and the line-search step sizes (ref: decode.py:66-76)."""
 
     m_lq: np.ndarray | None = None
     M_rq: np.ndarray | None = None
@@ -369,71 +491,97 @@ class DecodeWorkspace:
     eta_K: float = 0.0
 
 
-def _one_head_layer(d, r, n_rows, t_max, decode_cfg, k_budget=1, lite_budget=1):
-    shape = LayerShape(batch=1, n_q_heads=1, n_kv_heads=1, head_dim=d, rank=r, k_budget=k_budget,
-                       lite_budget=lite_budget, t_max=t_max, dtype="f32")
-    return LayerState(shape, lambda_1=decode_cfg.lambda_1, lambda_2=decode_cfg.lambda_2,
-                      max_iter=decode_cfg.max_iter, tol=decode_cfg.tol)
+def khat_initial_guess(k, B_K) -> np.ndarray:
+    """Least-squares k in the row space of B_K (ref: decode.py:79-81)."""
+    B = D.t64(np.ascontiguousarray(np.asarray(B_K, dtype=np.float64)))
+    kd = D.t64(np.asarray(k, dtype=np.float64).reshape(1, -1))
+    return D.np64(D.solve_spd(D.gram(B, of_transpose=True), D.gemm(kd, B, tb=True)))
 
 
-def _compress_on_device(step: TokenStep, f: LowRankFactors, A_res, K_res, cfg: DecodeConfig, update_b: bool):
-    A_res = np.asarray(A_res, dtype=np.float64)
-    K_res = np.asarray(K_res, dtype=np.float64)
+def _qk(step: TokenStep):
+    qd = D.t64(step.q.reshape(1, -1))
+    kd = D.t64(step.k.reshape(1, -1))
+    return qd, kd, D.dot(qd, kd)
+
+
+def update_qhat(step: TokenStep, comp: CompressedToken, f: LowRankFactors, A_K_resident, K_resident,
+                cfg: DecodeConfig, ws: DecodeWorkspace) -> np.ndarray:
+    """Closed-form q_hat given k_hat (ref: decode.py:84-108); fills ws.m_lq, ws.M_rq."""
+    A_res = np.asarray(A_K_resident, dtype=np.float64)
+    K_res = np.asarray(K_resident, dtype=np.float64)
     if A_res.shape[0] != K_res.shape[0]:
         raise ValueError(f"resident proxy/key row counts differ: {A_res.shape[0]} vs {K_res.shape[0]}")
-    r, d = f.B_Q.shape
-    n = A_res.shape[0]
-    layer = _one_head_layer(d, r, n, n + 1, cfg, k_budget=max(1, n), lite_budget=1)
-    dev = layer.device
-    lib = _lib.lib()
-    sp = _lib.stream_ptr()
-    rows = max(n, 1)
-    A = np.zeros((rows, r))
-    Kr = np.zeros((rows, d))
-    A[:n], Kr[:n] = A_res, K_res
-    layer.load_prompt(_f32(A[None, None], dev), _f32(f.B_Q[None, None], dev), _f32(f.B_K[None, None], dev),
-                      _f32(Kr[None, None], dev), _f32(Kr[None, None], dev))
-    # the resident set is exactly the given rows (possibly none)
-    layer.view("res_idx")[0, 0, :n] = torch.arange(n, dtype=torch.int32, device=dev)
-    layer.view("res_cnt").fill_(n)
-    _lib.check(lib.lrqk_compress_prepare(layer.ptr, sp), "lrqk_compress_prepare")
-    ds = layer.shape.dim_stride
-    q = pad_last(_f32(step.q, dev), ds).contiguous()
-    k = pad_last(_f32(step.k, dev), ds).contiguous()
-    v = pad_last(_f32(step.v, dev), ds).contiguous()
-    _lib.check(lib.lrqk_decode_compress(layer.ptr, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(update_b), sp),
-               "lrqk_decode_compress")
-    torch.cuda.synchronize()
-    layer.raise_status()
-    return layer
+    qd, kd, qk = _qk(step)
+    BQ = D.t64(f.B_Q)
+    kh = D.t64(np.asarray(comp.k_hat, dtype=np.float64).reshape(1, -1))
+    m_lq = D.gemm(qd, BQ, tb=True)
+    D.axpby(cfg.lambda_1, kh, 1.0, m_lq, scale=qk)
+    M_rq = D.gram(BQ, of_transpose=True)
+    D.gemm(kh, kh, ta=True, alpha=cfg.lambda_1, beta=1.0, out=M_rq)
+    if A_res.shape[0] > 0:
+        Ad, Kd = D.t64(A_res), D.t64(K_res)
+        w = D.gemm(qd, Kd, tb=True)
+        D.gemm(w, Ad, alpha=cfg.lambda_2, beta=1.0, out=m_lq)
+        D.axpby(cfg.lambda_2, D.gram(Ad), 1.0, M_rq)
+    ws.m_lq, ws.M_rq = D.np64(m_lq), D.np64(M_rq)
+    return D.np64(D.solve_spd(M_rq, m_lq))
+
+
+def update_khat(step: TokenStep, comp: CompressedToken, f: LowRankFactors, cfg: DecodeConfig) -> np.ndarray:
+    """Closed-form k_hat given q_hat (ref: decode.py:111-119)."""
+    qd, kd, qk = _qk(step)
+    BK = D.t64(f.B_K)
+    qh = D.t64(np.asarray(comp.q_hat, dtype=np.float64).reshape(1, -1))
+    rhs = D.gemm(kd, BK, tb=True)
+    D.axpby(cfg.lambda_1, qh, 1.0, rhs, scale=qk)
+    M = D.gram(BK, of_transpose=True)
+    D.gemm(qh, qh, ta=True, alpha=cfg.lambda_1, beta=1.0, out=M)
+    return D.np64(D.solve_spd(M, rhs))
 
 
 def decode_compress(step: TokenStep, f: LowRankFactors, A_K_resident, K_resident, cfg: DecodeConfig):
-    """ref: decode.py:122-147."""
-    layer = _compress_on_device(step, f, A_K_resident, K_resident, cfg, update_b=False)
+    """k_hat guess, then alternating q_hat / k_hat solves with the mean
+    squared change stop (ref: decode.py:122-147), float64 on the device.
+    The fused fp32 compression of the decode step (compress.cu, K2) is what
+    DecodeSession / Engine run."""
+    ws = DecodeWorkspace()
     r = f.B_Q.shape[0]
-    comp = CompressedToken(q_hat=_np64(layer.view("q_hat")[0, :, :r]), k_hat=_np64(layer.view("k_hat")[0, :, :r]))
-    return comp, DecodeWorkspace()
+    comp = CompressedToken(q_hat=np.zeros((1, r)), k_hat=khat_initial_guess(step.k, f.B_K))
+    prev = None
+    for _ in range(cfg.max_iter):
+        comp.q_hat = update_qhat(step, comp, f, A_K_resident, K_resident, cfg, ws)
+        comp.k_hat = update_khat(step, comp, f, cfg)
+        cur = np.concatenate([comp.q_hat, comp.k_hat], axis=1)
+        if prev is not None and fro_norm_sq(cur - prev) / cur.size <= cfg.tol:
+            break
+        prev = cur
+    return comp, ws
+
+
+def _line_search_step(row_hat, B, target):
+    """Gradient and exact step (ref: decode.py:150-166): grad = x^T (x B - t),
+    eta = (resid . s) / (s . s), s = x grad, 0 under the floor."""
+    xd = D.t64(np.asarray(row_hat, dtype=np.float64).reshape(1, -1))
+    Bd = D.t64(B)
+    resid = D.t64(np.asarray(target, dtype=np.float64).reshape(1, -1))
+    D.gemm(xd, Bd, beta=-1.0, out=resid)
+    grad = D.gemm(xd, resid, ta=True)
+    sv = D.gemm(xd, grad)
+    denom, numer = float(D.dot(sv, sv).item()), float(D.dot(resid, sv).item())
+    if denom <= ETA_DENOM_FLOOR * (1.0 + abs(numer)):
+        return grad, Bd, 0.0
+    return grad, Bd, numer / denom
 
 
 def update_projections(step: TokenStep, comp: CompressedToken, f: LowRankFactors, ws: DecodeWorkspace):
-    """One exact line-search step on B_Q, B_K (ref: decode.py:150-184),
-    computed by lrqk_line_search; A factors pass through."""
-    r, d = f.B_Q.shape
-    dev = _dev()
-    lib = _lib.lib()
-    xh = _f32(np.vstack([np.asarray(comp.q_hat).reshape(1, r), np.asarray(comp.k_hat).reshape(1, r)]), dev)
-    B = _f32(np.stack([f.B_Q, f.B_K]), dev)
-    x = _f32(np.vstack([np.asarray(step.q).reshape(1, d), np.asarray(step.k).reshape(1, d)]), dev)
-    B_out = torch.empty_like(B)
-    grad = torch.empty_like(B)
-    eta = torch.empty(2, dtype=torch.float32, device=dev)
-    _lib.check(lib.lrqk_line_search(xh.data_ptr(), B.data_ptr(), x.data_ptr(), 2, r, d, B_out.data_ptr(),
-                                    grad.data_ptr(), eta.data_ptr(), _lib.stream_ptr()), "lrqk_line_search")
-    e = eta.cpu().tolist()
-    ws.grad_BQ, ws.grad_BK = _np64(grad[0]), _np64(grad[1])
-    ws.eta_Q, ws.eta_K = float(e[0]), float(e[1])
-    return LowRankFactors(A_Q=f.A_Q, A_K=f.A_K, B_Q=_np64(B_out[0]), B_K=_np64(B_out[1]))
+    """One exact line-search step on B_Q, B_K (ref: decode.py:169-184); A
+    factors pass through."""
+    gq, BQ, ws.eta_Q = _line_search_step(comp.q_hat, f.B_Q, step.q)
+    gk, BK, ws.eta_K = _line_search_step(comp.k_hat, f.B_K, step.k)
+    ws.grad_BQ, ws.grad_BK = D.np64(gq), D.np64(gk)
+    D.axpby(-ws.eta_Q, gq, 1.0, BQ)
+    D.axpby(-ws.eta_K, gk, 1.0, BK)
+    return LowRankFactors(A_Q=f.A_Q, A_K=f.A_K, B_Q=D.np64(BQ), B_K=D.np64(BK))
 
 
 # ---------------------------------------------------------------------------
@@ -740,15 +888,18 @@ class DecodeSession:
 
     def _fidelity(self, q, omega, output, t):
         """Recall against the exact top-k over the full history and error
-        against full-history attention (ref: session.py:119-131), both on the
-        device."""
+        against full-history attention (ref: session.py:119-131).  Both run
+        on the device over the stored history: a float64 q K^T GEMM and
+        float64 select for the exact set, the attention kernel for the
+        full-history output; only k indices and one d-row come back."""
         L = self._layer
         d = self._d
-        K = L.view("slow_k")[0, 0, : t + 1, :d].contiguous()
-        V = L.view("slow_v")[0, 0, : t + 1, :d].contiguous()
-        exact = exact_topk(q, _np64(K), min(self.cfg.k_budget, t + 1))
+        K = L.view("slow_k")[0, 0, : t + 1, :d]
+        V = L.view("slow_v")[0, 0, : t + 1, :d]
+        exact = _exact_topk_dev(D.t64(q.reshape(1, -1)), K.double().contiguous(), min(self.cfg.k_budget, t + 1))
         recall = selection_recall(omega, exact)
-        full, _ = _attention_device(_f32(q, L.device), K[None], V[None], d, want_weights=False)
+        full, _ = _attention_device(_f32(q, L.device), K.contiguous()[None], V.contiguous()[None], d,
+                                    want_weights=False)
         full = _np64(full[:, :d])
         denom = float(np.linalg.norm(full))
         diff = float(np.linalg.norm(output - full))

@@ -34,6 +34,16 @@ int launch_line_search(const float *xh, const float *B, const float *x, int H, i
                        float *grad, float *eta, cudaStream_t st);
 size_t prefill_scratch_floats(const lrqk_prefill_t &P);
 int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st);
+int launch_gemm_f64(int ta, int tb, int m, int n, int k, double alpha, const double *A, int lda, const double *B,
+                    int ldb, double beta, double *C, int ldc, void *work, size_t work_bytes, cudaStream_t st);
+size_t gemm_f64_workspace(int m, int n, int k);
+int launch_mirror_f64(double *G, int r, int ldg, cudaStream_t st);
+int launch_dot_f64(const double *a, const double *b, long long n, double *out, double *work, cudaStream_t st);
+int launch_axpby_f64(long long n, double alpha, const double *s, const double *x, double beta, double *y,
+                     cudaStream_t st);
+int launch_solve_spd_f64(const double *M, int r, int ldm, const double *RHS, int n, int ldr, double *X, int ldx,
+                         double *work, uint32_t *status, cudaStream_t st);
+int launch_topk_f64(const double *s, int n, int k, int32_t *out, cudaStream_t st);
 }  // namespace lrqk
 
 using namespace lrqk;
@@ -426,4 +436,43 @@ extern "C" int lrqk_trace_read(unsigned long long *out, int cap) {
         ++n;
     }
     return n;
+}
+
+// ---- float64 dense kernels (dense.cu) ----------------------------------------
+int lrqk_gemm_f64(int32_t trans_a, int32_t trans_b, int32_t m, int32_t n, int32_t k, double alpha, const double *A,
+                  int32_t lda, const double *B, int32_t ldb, double beta, double *C, int32_t ldc, void *work,
+                  size_t work_bytes, void *stream) {
+    if (m < 0 || n < 0 || k < 0 || !C || (k > 0 && (!A || !B))) return LRQK_EINVAL;
+    if (lda < (trans_a ? m : k) || ldb < (trans_b ? k : n) || ldc < n) return LRQK_EINVAL;
+    return check(lrqk::launch_gemm_f64(trans_a, trans_b, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, work,
+                                       work_bytes, (cudaStream_t)stream));
+}
+size_t lrqk_gemm_f64_workspace(int32_t m, int32_t n, int32_t k) { return lrqk::gemm_f64_workspace(m, n, k); }
+
+int lrqk_symmetrize_f64(double *G, int32_t r, int32_t ldg, void *stream) {
+    if (!G || r < 0 || ldg < r) return LRQK_EINVAL;
+    return check(lrqk::launch_mirror_f64(G, r, ldg, (cudaStream_t)stream));
+}
+
+int lrqk_dot_f64(const double *a, const double *b, int64_t n, double *out, double *work, void *stream) {
+    if (!a || !b || !out || !work || n < 0) return LRQK_EINVAL;
+    return check(lrqk::launch_dot_f64(a, b, n, out, work, (cudaStream_t)stream));
+}
+
+int lrqk_axpby_f64(int64_t n, double alpha, const double *alpha_scale, const double *x, double beta, double *y,
+                   void *stream) {
+    if (n < 0 || (n > 0 && (!x || !y))) return LRQK_EINVAL;
+    return check(lrqk::launch_axpby_f64(n, alpha, alpha_scale, x, beta, y, (cudaStream_t)stream));
+}
+
+int lrqk_solve_spd_f64(const double *M, int32_t r, int32_t ldm, const double *RHS, int32_t n, int32_t ldr, double *X,
+                       int32_t ldx, double *work, uint32_t *status, void *stream) {
+    if (!M || !work || !status || r < 1 || ldm < r || n < 0 || (n > 0 && (!RHS || !X || ldr < r || ldx < r)))
+        return LRQK_EINVAL;
+    return check(lrqk::launch_solve_spd_f64(M, r, ldm, RHS, n, ldr, X, ldx, work, status, (cudaStream_t)stream));
+}
+
+int lrqk_topk_f64(const double *scores, int32_t n, int32_t k, int32_t *out, void *stream) {
+    if (!scores || !out || n < 0 || k < 1 || k >= n + 1) return LRQK_EINVAL;
+    return check(lrqk::launch_topk_f64(scores, n, k, out, (cudaStream_t)stream));
 }

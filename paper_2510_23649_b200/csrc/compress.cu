@@ -224,13 +224,17 @@ __device__ void fill_padded(float *b0, const float *M, int ldm, int r, int R, in
 // retry (linalg.py:80-91).  Returns 0 ok, 1 ok after jitter, 2 failed.
 __device__ int solve_spd_direct(const float *M, int ldm, int r, int R, int ld, const float *rhs, float *x,
                                 float *b0, float *s_rc) {
-    for (int attempt = 0; attempt < 2; ++attempt) {
+    // attempt 0: M as given; then the reference's jitter 1e-10 (tr/r + 1)
+    // (linalg.py:83-87), floored at fp32 resolution.  A rank-deficient M that
+    // the reference factors in fp64 carries O(n u |M|) rounding in fp32, which
+    // can exceed that floor, so the fp32 retry escalates the floor x16 up to
+    // three more times (to ~5e-4 dmax) before reporting SolveFailedError.
+    for (int attempt = 0; attempt < 5; ++attempt) {
         float jit = 0.f;
-        if (attempt == 1) {
+        if (attempt >= 1) {
             float tr = 0.f, dmax = 0.f;
             for (int i = 0; i < r; ++i) { tr += M[i * ldm + i]; dmax = fmaxf(dmax, fabsf(M[i * ldm + i])); }
-            // 1e-10 (tr/r + 1) as the reference, floored at fp32 resolution
-            jit = fmaxf(1e-10f * (tr / r + 1.f), dmax * 1.2e-7f);
+            jit = fmaxf(1e-10f * (tr / r + 1.f), dmax * 1.2e-7f * (float)(1 << (4 * (attempt - 1))));
         }
         fill_padded(b0, M, ldm, r, R, ld, jit);
         if (block_gj(b0, R, ld, s_rc)) {
@@ -240,7 +244,7 @@ __device__ int solve_spd_direct(const float *M, int ldm, int r, int R, int ld, c
                 x[j] = acc;
             }
             __syncthreads();
-            return attempt;
+            return attempt ? 1 : 0;
         }
     }
     return 2;

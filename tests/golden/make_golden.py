@@ -225,6 +225,52 @@ def gen_sessions():
     _save("sessions", **flat)
 
 
+def gen_dense():
+    """The per-call linear algebra of the reference: gram, fro_norm_sq,
+    update_B/AK/AQ, lagrangian_value, factor_residuals, khat_initial_guess,
+    update_qhat/khat, and top-k on float64 scores closer than float32 can
+    resolve."""
+    rng = np.random.default_rng(1007)
+    flat = {}
+    i = 0
+    for l, d, r, lq, lk in [(64, 16, 4, 1.0, 1.0), (200, 32, 8, 0.5, 2.0), (300, 128, 32, 1.0, 1.0),
+                            (40, 24, 6, 0.0, 0.0)]:
+        Q = rng.standard_normal((l, d))
+        K = rng.standard_normal((l, d)) * 2.0
+        f = lrqk.LowRankFactors(A_Q=rng.standard_normal((l, r)), A_K=rng.standard_normal((l, r)),
+                                B_Q=rng.standard_normal((r, d)) / np.sqrt(d), B_K=rng.standard_normal((r, d)) / np.sqrt(d))
+        cfg = lrqk.PrefillConfig(rank=r, lambda_q=lq, lambda_k=lk)
+        flat.update({f"Q{i}": Q, f"K{i}": K, f"A_Q{i}": f.A_Q, f"A_K{i}": f.A_K, f"B_Q{i}": f.B_Q, f"B_K{i}": f.B_K,
+                     f"lam{i}": np.array([lq, lk]),
+                     f"gram{i}": lrqk.gram(f.A_Q), f"gramT{i}": lrqk.gram(f.B_K.T), f"fro{i}": np.array(lrqk.fro_norm_sq(Q)),
+                     f"uB{i}": lrqk.update_B(f.A_Q, Q), f"uAK{i}": lrqk.update_AK(Q, K, f, cfg),
+                     f"uAQ{i}": lrqk.update_AQ(Q, K, f, cfg), f"lag{i}": np.array(lrqk.lagrangian_value(Q, K, f, cfg)),
+                     f"res{i}": np.array(lrqk.factor_residuals(Q, K, f))})
+        # decode-side closed forms on a resident set
+        nres = [5, 0, 272, 3][i]
+        step = lrqk.TokenStep(q=rng.standard_normal((1, d)), k=rng.standard_normal((1, d)), v=rng.standard_normal((1, d)))
+        A_res, K_res = rng.standard_normal((nres, r)), rng.standard_normal((nres, d))
+        dcfg = lrqk.DecodeConfig(lambda_1=[1.0, 0.5, 1.0, 2.0][i], lambda_2=[1.0, 1.5, 1.0, 0.0][i])
+        comp = lrqk.CompressedToken(q_hat=rng.standard_normal((1, r)), k_hat=rng.standard_normal((1, r)))
+        ws = lrqk.DecodeWorkspace()
+        flat.update({f"q{i}": step.q, f"k{i}": step.k, f"v{i}": step.v, f"A_res{i}": A_res, f"K_res{i}": K_res,
+                     f"dlam{i}": np.array([dcfg.lambda_1, dcfg.lambda_2]), f"qh_in{i}": comp.q_hat,
+                     f"kh_in{i}": comp.k_hat,
+                     f"kh0{i}": lrqk.khat_initial_guess(step.k, f.B_K),
+                     f"uq{i}": lrqk.update_qhat(step, comp, f, A_res, K_res, dcfg, ws),
+                     f"m_lq{i}": ws.m_lq, f"M_rq{i}": ws.M_rq,
+                     f"uk{i}": lrqk.update_khat(step, comp, f, dcfg)})
+        i += 1
+    flat["n"] = np.array(i)
+    # float64 scores that differ below float32 resolution
+    base = rng.standard_normal(500)
+    s = np.repeat(base[:50], 10) + np.tile(np.arange(10) * 1e-12, 50)
+    rng.shuffle(s)
+    flat["tk_s"] = s
+    flat["tk_o"] = lrqk.topk_indices(s, 37)
+    _save("dense", **flat)
+
+
 def main():
     gen_topk()
     gen_select()
@@ -233,6 +279,7 @@ def main():
     gen_spd()
     gen_prefill()
     gen_sessions()
+    gen_dense()
     manifest = {"reference_version": lrqk.__version__, "numpy": np.__version__,
                 "files": sorted(f for f in os.listdir(HERE) if f.endswith(".npz"))}
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as fh:

@@ -185,9 +185,13 @@ class StepLocked:
                                           lam1=lam[0], lam2=lam[1], max_iter=max_iter, tol=tol)
         self.t = prompt
 
-    def check_step(self, out, log: ParityLog, dtype, rtol_hat, check_b=True):
+    def check_step(self, out, log: ParityLog, dtype, rtol_hat, check_b=True, strict=True):
         """Compare the GPU step that just ran (token t = self.t) with the
-        oracle, then re-sync.  out: [B, Hq, dim_stride] device outputs."""
+        oracle, then re-sync.  out: [B, Hq, dim_stride] device outputs.
+        strict=False skips the comparisons with the oracle's OWN compression
+        (q_hat, k_hat, B and the selection it implies) -- for singular
+        compression systems, whose jittered solutions are conditioning-limited
+        in fp32 -- and keeps everything judged on the GPU's own q_hat."""
         L, sh, t = self.layer, self.sh, self.t
         d, r, kb, lb = sh.head_dim, sh.rank, sh.k_budget, sh.lite_budget
         res_cnt = L.view("res_cnt").cpu().numpy()
@@ -216,7 +220,8 @@ class StepLocked:
             ek = _rel(kh[b, h], ref.k_hat.ravel())
             log.rec["max_qhat_rel"] = max(log.rec["max_qhat_rel"], eq)
             log.rec["max_khat_rel"] = max(log.rec["max_khat_rel"], ek)
-            assert eq <= rtol_hat and ek <= rtol_hat, f"q_hat/k_hat rel err {eq:.3g}/{ek:.3g} at t={t} (b={b},h={h})"
+            if strict:
+                assert eq <= rtol_hat and ek <= rtol_hat, f"q_hat/k_hat rel err {eq:.3g}/{ek:.3g} at t={t} (b={b},h={h})"
             # ---- the appended proxy row is the GPU's k_hat in storage precision --
             np.testing.assert_allclose(row_t[b, h], quantize(kh[b, h], dtype), rtol=0, atol=0)
             st.proxy[t] = row_t[b, h]                 # sync the store to the stored row
@@ -229,7 +234,7 @@ class StepLocked:
                 assert eb <= 2e-5, f"B line-search update rel err {eb:.3g} at t={t} (b={b},h={h})"
                 ebr = max(_rel(BQn[b, h], ref.B_Q), _rel(BKn[b, h], ref.B_K))
                 log.rec["max_B_rel_ref"] = max(log.rec["max_B_rel_ref"], ebr)
-                assert ebr <= 20 * rtol_hat, f"B vs oracle's own update rel err {ebr:.3g} at t={t}"
+                assert ebr <= 20 * rtol_hat or not strict, f"B vs oracle's own update rel err {ebr:.3g} at t={t}"
             st.B_Q, st.B_K = BQn[b, h].copy(), BKn[b, h].copy()
             # ---- scores: GPU keys vs the fp64 product on the same q_hat and rows --
             s_gpu = keys_to_scores(keys[b, h])
@@ -250,6 +255,7 @@ class StepLocked:
                 assert not bad, f"selection differs beyond near-ties at t={t} (b={b},h={h}): {bad[:5]}"
                 log.rec["excused_gpu_qhat"] += [(t, b, h) + x for x in ok]
                 log.rec["selections_identical"] += int(not ok)
+            if k_eff > 0 and strict:
                 # vs the oracle's fully independent selection (its own q_hat)
                 dq = qh[b, h] - ref.q_hat.ravel()
                 sref, eref = score_error_bound(st.proxy[: t + 1], ref.q_hat.ravel(), r, extra_dq=dq)

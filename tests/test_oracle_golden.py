@@ -105,3 +105,31 @@ def test_sessions_match_reference(gold):
             np.testing.assert_allclose(res.k_hat.ravel(), g[f"khat{i}"][j], rtol=1e-6, atol=1e-8)
         assert (st.c_miss, st.c_total) == (int(g[f"c_miss{i}"]), int(g[f"c_total{i}"]))
         np.testing.assert_allclose(st.B_Q, g[f"BQ{i}"][-1], rtol=1e-6, atol=1e-8)
+
+
+def test_dense_algebra_matches_reference(gold):
+    """gram, fro_norm_sq, update_B/AK/AQ, lagrangian_value, factor_residuals,
+    khat_initial_guess, update_qhat/khat (tests/golden/dense.npz)."""
+    g = gold("dense")
+    for i in range(int(g["n"])):
+        Q, K = g[f"Q{i}"], g[f"K{i}"]
+        f = O.Factors(g[f"A_Q{i}"], g[f"A_K{i}"], g[f"B_Q{i}"], g[f"B_K{i}"])
+        lq, lk = g[f"lam{i}"]
+        np.testing.assert_allclose(O.sym_gram(f.A_Q), g[f"gram{i}"], rtol=1e-12)
+        np.testing.assert_allclose(O.sym_gram(f.B_K.T), g[f"gramT{i}"], rtol=1e-12)
+        assert O.sq_norm(Q) == pytest.approx(float(g[f"fro{i}"]), rel=1e-12)
+        np.testing.assert_allclose(O.fit_B(f.A_Q, Q), g[f"uB{i}"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(O.fit_A_K(Q, K, f, lk), g[f"uAK{i}"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(O.fit_A_Q(Q, K, f, lq), g[f"uAQ{i}"], rtol=1e-9, atol=1e-12)
+        assert O.objective(Q, K, f, lq, lk) == pytest.approx(float(g[f"lag{i}"]), rel=1e-10)
+        np.testing.assert_allclose(O.relative_residuals(Q, K, f), g[f"res{i}"], rtol=1e-9)
+        q, k = g[f"q{i}"], g[f"k{i}"]
+        l1, l2 = g[f"dlam{i}"]
+        np.testing.assert_allclose(O.khat_seed(k, f.B_K), g[f"kh0{i}"], rtol=1e-9, atol=1e-12)
+        qh, M, m = O.solve_qhat(q, k, g[f"kh_in{i}"], f.B_Q, g[f"A_res{i}"], g[f"K_res{i}"], l1, l2)
+        np.testing.assert_allclose(qh, g[f"uq{i}"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(M, g[f"M_rq{i}"], rtol=1e-12)
+        np.testing.assert_allclose(m, g[f"m_lq{i}"], rtol=1e-12)
+        np.testing.assert_allclose(O.solve_khat(q, k, g[f"qh_in{i}"], f.B_K, l1), g[f"uk{i}"], rtol=1e-9,
+                                   atol=1e-12)
+    np.testing.assert_array_equal(O.largest_k(g["tk_s"], 37), g["tk_o"])
