@@ -13,7 +13,8 @@ Implemented entry points and the kernels behind them:
   topk_indices, select_active       -> lrqk_topk_f64 (exact float64 order) (linalg.py:96-110, cache.py:149-171)
   update_B, update_AK, update_AQ,
   lagrangian_value, factor_residuals -> float64 dense kernels               (prefill.py:142-181, 239-253)
-  prefill_run / prefill_factorize  -> lrqk_prefill_factorize (K1)          (prefill.py:197-230)
+  prefill_run / prefill_factorize  -> float64 dense kernels, reference order (prefill.py:197-230);
+                                      the engine's batched prefill is K1 (lrqk_prefill_factorize)
   init_factors, importance_scores  -> host initialisation, as the reference (prefill.py:108-139)
   khat_initial_guess, update_qhat,
   update_khat, decode_compress,
@@ -351,21 +352,69 @@ def init_factors(Q, K, cfg: PrefillConfig) -> LowRankFactors:
     return LowRankFactors(A_Q=A_Q, A_K=A_K, B_Q=np.zeros((r, d)), B_K=np.zeros((r, d)))
 
 
+def _factor_sweep_f64(Qd, Kd, f, cfg):
+    """One BCD sweep B_Q, B_K, A_K, A_Q in the reference's association
+    (prefill.py:211-214), float64 device tensors in f (dict)."""
+    def update_b(A, X):
+        return D.solve_spd(D.gram(A), D.gemm(X, A, ta=True)).t().contiguous()
+
+    def update_a(Xo, Xs, Ao, Bs, lam):
+        T = D.gemm(Xo, Ao, ta=True)
+        D.axpby(lam, Bs.t().contiguous(), 1.0, T)
+        M = D.gram(Ao)
+        D.axpby(lam, D.gram(Bs, of_transpose=True), 1.0, M)
+        return D.solve_spd(M, D.gemm(Xs, T))
+
+    f["B_Q"] = update_b(f["A_Q"], Qd)
+    f["B_K"] = update_b(f["A_K"], Kd)
+    f["A_K"] = update_a(Qd, Kd, f["A_Q"], f["B_K"], cfg.lambda_k)
+    f["A_Q"] = update_a(Kd, Qd, f["A_K"], f["B_Q"], cfg.lambda_q)
+
+
+def _objective_f64(Qd, Kd, f, cfg):
+    """lagrangian_value on device factors (prefill.py:142-158)."""
+    GQ, GK = D.gram(Qd), D.gram(Kd)
+    qq = D.dot(GQ, GK)
+    cross = D.dot(D.gemm(Qd, f["A_Q"], ta=True), D.gemm(Kd, f["A_K"], ta=True))
+    approx = D.dot(D.gram(f["A_Q"]), D.gram(f["A_K"]))
+    rq = D.residual_sq(Qd, f["A_Q"], f["B_Q"])
+    rk = D.residual_sq(Kd, f["A_K"], f["B_K"])
+    qq, cross, approx, rq, rk = (float(x.item()) for x in (qq, cross, approx, rq, rk))
+    return 0.5 * max(qq - 2.0 * cross + approx, 0.0) + 0.5 * cfg.lambda_q * rq + 0.5 * cfg.lambda_k * rk
+
+
 def prefill_run(Q, K, cfg: PrefillConfig) -> PrefillRun:
+    """The alternating sweeps with the objective trajectory and the
+    mean-squared-change stop (ref: prefill.py:197-223), in float64 on the
+    device, so sweeps / converged / objective follow the reference's to
+    rounding.  The batched bf16 / fp32 engine prefill is the fused K1 pass
+    (engine.prefill_factorize_device)."""
     Q = as_matrix(Q, "Q")
     K = as_matrix(K, "K")
     if Q.shape != K.shape:
         raise ValueError(f"Q and K must share a shape, got {Q.shape} vs {K.shape}")
     f0 = init_factors(Q, K, cfg)
-    dev = _dev()
-    res = prefill_factorize_device(_f32(Q[None], dev), _f32(K[None], dev), cfg.rank, lambda_q=cfg.lambda_q,
-                                   lambda_k=cfg.lambda_k, max_iter=cfg.max_iter, tol=cfg.tol, A_Q0=f0.A_Q,
-                                   A_K0=f0.A_K, want_objective=True, dtype="f32")
-    sweeps = int(res["sweeps"][0])
-    obj = [float(x) for x in res["objective"][0, : sweeps + 1].cpu()]
-    f = LowRankFactors(A_Q=_np64(res["A_Q"][0]), A_K=_np64(res["A_K"][0]), B_Q=_np64(res["B_Q"][0]),
-                       B_K=_np64(res["B_K"][0]))
-    return PrefillRun(factors=f, objective=obj, sweeps=sweeps, converged=bool(res["converged"][0]))
+    Qd, Kd = D.t64(Q), D.t64(K)
+    f = {nm: D.t64(getattr(f0, nm)) for nm in ("A_Q", "A_K", "B_Q", "B_K")}
+    objective = [_objective_f64(Qd, Kd, f, cfg)]
+    converged, sweeps = False, 0
+    for _ in range(cfg.max_iter):
+        prev = {nm: t.clone() for nm, t in f.items()}
+        _factor_sweep_f64(Qd, Kd, f, cfg)
+        sweeps += 1
+        for nm in ("A_Q", "A_K", "B_Q", "B_K"):
+            if not math.isfinite(float(D.dot(f[nm], f[nm]).item())):
+                raise NonFiniteError(f"factor {nm} diverged at sweep {sweeps}")
+        objective.append(_objective_f64(Qd, Kd, f, cfg))
+        delta = 0.0
+        for nm in ("A_Q", "A_K", "B_Q", "B_K"):
+            diff = D.axpby(-1.0, prev[nm], 1.0, f[nm].clone())
+            delta += float(D.dot(diff, diff).item()) / diff.numel()
+        if delta / 4.0 <= cfg.tol:
+            converged = True
+            break
+    fac = LowRankFactors(**{nm: D.np64(t) for nm, t in f.items()})
+    return PrefillRun(factors=fac, objective=objective, sweeps=sweeps, converged=converged)
 
 
 def prefill_factorize(Q, K, cfg: PrefillConfig) -> LowRankFactors:

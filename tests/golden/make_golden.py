@@ -271,6 +271,36 @@ def gen_dense():
     _save("dense", **flat)
 
 
+CLI_SYNTH = ["--length", "128", "--dim", "32", "--rank-true", "32", "--decay", "0.95", "--recency", "2.0", "--scale", "11.3",
+             "--seed", "5", "--heads", "3"]
+CLI_SIM = ["--rank", "8", "--topk", "24", "--lite", "8", "--prompt-len", "64"]
+
+
+def gen_cli():
+    """Outputs of the reference CLI (`lrqk synth / factorize / simulate`) on a
+    small recency-biased workload: the trace bytes and every output file."""
+    import shutil
+    import tempfile
+
+    from lrqk.cli import main as cli_main
+
+    root = os.path.join(HERE, "cli")
+    shutil.rmtree(root, ignore_errors=True)
+    os.makedirs(root)
+    trace = os.path.join(root, "workload.lrqk")
+    assert cli_main(["synth", *CLI_SYNTH, "--out", trace]) == 0
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, argv in (("simulate_nometrics", ["simulate", "--trace", trace, *CLI_SIM, "--no-metrics"]),
+                           ("simulate_metrics", ["simulate", "--trace", trace, *CLI_SIM, "--steps", "24"]),
+                           ("factorize", ["factorize", "--trace", trace, "--rank", "8", "--max-iter", "6",
+                                          "--tol", "1e-9"])):
+            out = os.path.join(tmp, name)
+            assert cli_main([*argv, "--out-dir", out]) == 0
+            shutil.copytree(out, os.path.join(root, name))
+    with open(os.path.join(root, "ARGS.json"), "w") as fh:
+        json.dump({"synth": CLI_SYNTH, "simulate": CLI_SIM}, fh, indent=1)
+
+
 def main():
     gen_topk()
     gen_select()
@@ -280,6 +310,7 @@ def main():
     gen_prefill()
     gen_sessions()
     gen_dense()
+    gen_cli()
     manifest = {"reference_version": lrqk.__version__, "numpy": np.__version__,
                 "files": sorted(f for f in os.listdir(HERE) if f.endswith(".npz"))}
     with open(os.path.join(HERE, "MANIFEST.json"), "w") as fh:
