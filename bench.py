@@ -47,18 +47,24 @@ WORKLOADS = {
 }
 
 
-def _ncu_traffic(algorithmic_bytes):
-    """dram__bytes_read.sum + dram__bytes_write.sum of the score kernel from the
-    committed ncu --set full capture (profiles/roofline_traffic.json) when that
-    capture was taken on this launch shape (same algorithmic bytes), or None."""
+def _ncu_traffic(workload_key, algorithmic_bytes):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the score
+    kernel, from the committed ncu --set full capture of this workload
+    (profiles/roofline_traffic.json, keyed by workload).  The capture was
+    taken a few decode steps into the run; when this run's launch has the
+    same algorithmic bytes within 2 % (same workload, context within a few
+    hundred tokens), the captured DRAM bytes are scaled by the ratio of
+    algorithmic bytes.  Returns (bytes, source) or (None, reason)."""
     try:
         with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")) as f:
-            rec = json.load(f)
-        if int(rec["algorithmic_bytes_per_launch"]) != int(algorithmic_bytes):
-            return None
-        return int(rec["dram_bytes_per_launch"])
-    except (OSError, ValueError, KeyError):
-        return None
+            rec = json.load(f)[workload_key]
+        alg0 = int(rec["algorithmic_bytes_per_launch"])
+        if abs(algorithmic_bytes - alg0) > 0.02 * alg0:
+            return None, f"no capture within 2% of {algorithmic_bytes} algorithmic bytes"
+        dram = int(rec["dram_bytes_per_launch"])
+        return int(round(dram * algorithmic_bytes / alg0)), rec["source"] + f" (scaled x{algorithmic_bytes / alg0:.5f})"
+    except (OSError, ValueError, KeyError) as e:
+        return None, f"no ncu capture for {workload_key}: {e.__class__.__name__}"
 
 
 def parse():
@@ -74,6 +80,9 @@ def parse():
     p.add_argument("--rank", type=int, default=None)
     p.add_argument("--topk", type=int, default=None)
     p.add_argument("--policy", choices=["hbm", "host"], default="hbm")
+    p.add_argument("--data", choices=["random", "recency", "drift"], default="random",
+                   help="random: i.i.d. N(0,1) Q/K/V; recency: the reference's gen_recency_biased structure; "
+                        "drift: AR(1)-correlated queries (paper-like top-k miss rate)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-s", type=float, default=15.0)
     p.add_argument("--profile-steps", type=int, default=0,
@@ -97,6 +106,20 @@ def workload(args):
     if over:  # the description names the overrides
         w["desc"] = base["desc"] + " [overridden: " + ", ".join(over) + "]"
     return w
+
+
+def config_dict(args, world):
+    """The `config` object of the JSON line; identical for both arms."""
+    w = workload(args)
+    B = args.batch_per_gpu
+    return dict(workload=w["desc"], ctx=w["ctx"], layers=w["layers"], n_q_heads=w["hq"], n_kv_heads=w["hkv"],
+                head_dim=w["d"], rank=w["r"], top_k=w["k"], lite=w["lite"], batch_per_gpu=B, global_batch=B * world,
+                slow_tier=args.policy, data=args.data,
+                parallelism=(f"batch-sharded over {world} GPU(s), no collective inside the step; NCCL all-gather of "
+                             f"last-layer outputs per step") if world > 1 else "1 GPU",
+                l2="no flush: each step streams %.1f GB (> 126 MB L2)" % (
+                    step_bytes(w, B, w["ctx"], w["k"] + w["lite"], 2 if w["dtype"] == "bf16" else 4)["total"]
+                    * w["layers"] / 1e9))
 
 
 # --------------------------------------------------------------------------
@@ -185,6 +208,78 @@ def step_bytes(w, B, t, S, e):
 
 
 # --------------------------------------------------------------------------
+# structured synthetic data: the reference's gen_recency_biased
+# (workload.py:87-107) with r_true=64, decay 0.95, recency 2.0, scale sqrt(T),
+# drawn on the GPU (input synthesis only).  The q-heads of one KV group share
+# the group's query directions (plus 10 % independent noise), so every one of
+# them sees the recency structure of the shared keys.
+# --------------------------------------------------------------------------
+def recency_biased_heads(B, Hq, Hkv, T, d, gen, dev, r_true=64, decay=0.95, strength=2.0):
+    import torch
+
+    G = Hq // Hkv
+    sig = math.sqrt(T) * decay ** torch.arange(r_true, device=dev, dtype=torch.float32)
+
+    def lowrank():
+        U = torch.linalg.qr(torch.randn(T, r_true, device=dev, generator=gen))[0]
+        W = torch.linalg.qr(torch.randn(d, r_true, device=dev, generator=gen))[0]
+        return (U * sig) @ W.T
+
+    Q = torch.empty(B * Hq, T, d, device=dev)
+    K = torch.empty(B * Hkv, T, d, device=dev)
+    V = torch.randn(B * Hkv, T, d, device=dev, generator=gen)
+    for bg in range(B * Hkv):
+        Qg = lowrank()
+        Kg = lowrank()
+        Qn = Qg / (Qg * Qg).sum(1, keepdim=True).add_(1e-30)
+        for lag in range(min(T - 1, 40) + 1):
+            Kg[: T - lag].add_(Qn[lag:], alpha=strength * math.exp(-lag) * math.sqrt(d))
+        K[bg] = Kg
+        for j in range(G):
+            h = (bg // Hkv) * Hq + (bg % Hkv) * G + j
+            Q[h] = Qg + 0.1 * Qg.std() * torch.randn(T, d, device=dev, generator=gen)
+    return Q, K, V
+
+
+def drift_heads(B, Hq, Hkv, T, d, gen, dev, rho=0.9, r_true=64, decay=0.95, strength=2.0):
+    """Temporally correlated queries: each q-head's latent coefficients follow
+    an AR(1) process z_t = rho z_{t-1} + sqrt(1 - rho^2) e_t over the KV
+    group's rank-64 key subspace, so consecutive queries pick overlapping
+    top-k sets.  rho = 0.9 gives a top-k miss rate of ~0.45 per step, the
+    regime the paper reports (~0.40) and the one the GPU
+    cache (K5) and the pinned host tier (K5b) are built for.  Keys: the
+    group's low-rank subspace plus the reference's recency bias toward the
+    group's queries (workload.py:87-107)."""
+    import torch
+
+    G = Hq // Hkv
+    sq = decay ** torch.arange(r_true, device=dev, dtype=torch.float32)
+    sk = math.sqrt(T) * sq
+    Q = torch.empty(B * Hq, T, d, device=dev)
+    K = torch.empty(B * Hkv, T, d, device=dev)
+    V = torch.randn(B * Hkv, T, d, device=dev, generator=gen)
+    for bg in range(B * Hkv):
+        W = torch.linalg.qr(torch.randn(d, r_true, device=dev, generator=gen))[0]
+        U = torch.linalg.qr(torch.randn(T, r_true, device=dev, generator=gen))[0]
+        Kg = (U * sk) @ W.T
+        for j in range(G):
+            z = math.sqrt(1 - rho * rho) * torch.randn(T, r_true, device=dev, generator=gen)
+            z[0] /= math.sqrt(1 - rho * rho)
+            shift = 1
+            while shift < T:  # z_t = sum_j rho^j e_{t-j}, by doubling
+                z[shift:] += rho ** shift * z[:-shift].clone()
+                shift *= 2
+            h = (bg // Hkv) * Hq + (bg % Hkv) * G + j
+            Q[h] = (z * sq) @ W.T
+        Qg = Q[(bg // Hkv) * Hq + (bg % Hkv) * G]
+        Qn = Qg / (Qg * Qg).sum(1, keepdim=True).add_(1e-30)
+        for lag in range(min(T - 1, 40) + 1):
+            Kg[: T - lag].add_(Qn[lag:], alpha=strength * math.exp(-lag) * math.sqrt(d))
+        K[bg] = Kg
+    return Q, K, V
+
+
+# --------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------
 def run_ours(args, world, rank, local):
@@ -210,14 +305,29 @@ def run_ours(args, world, rank, local):
     gen.manual_seed(1234 + rank)
 
     # ---- prompt: synthetic Q/K/V, factorised by the GPU prefill kernels ----
+    # recency data: `pool` rows past the prompt are the decode rows, so the
+    # decode queries continue the prompt's structure
+    pool = 8 if args.data == "random" else 64
     torch.cuda.synchronize()
     t0 = time.time()
     prefill_ms = 0.0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q_pool = torch.empty(pool, L, B, Hq, d, device=dev, dtype=sdt)
+    k_pool = torch.empty(pool, L, B, Hkv, d, device=dev, dtype=sdt)
+    v_pool = torch.empty_like(k_pool)
     for li, layer in enumerate(eng.layers):
-        Qp = torch.randn(B * Hq, ctx, d, device=dev, generator=gen).to(sdt)
-        Kp = torch.randn(B * Hkv, ctx, d, device=dev, generator=gen).to(sdt)
-        Vp = torch.randn(B * Hkv, ctx, d, device=dev, generator=gen).to(sdt)
+        if args.data != "random":
+            gen_heads = recency_biased_heads if args.data == "recency" else drift_heads
+            Qa, Ka, Va = gen_heads(B, Hq, Hkv, ctx + pool, d, gen, dev)
+            q_pool[:, li] = Qa[:, ctx:].reshape(B, Hq, pool, d).permute(2, 0, 1, 3).to(sdt)
+            k_pool[:, li] = Ka[:, ctx:].reshape(B, Hkv, pool, d).permute(2, 0, 1, 3).to(sdt)
+            v_pool[:, li] = Va[:, ctx:].reshape(B, Hkv, pool, d).permute(2, 0, 1, 3).to(sdt)
+            Qp, Kp, Vp = (x[:, :ctx].to(sdt).contiguous() for x in (Qa, Ka, Va))
+            del Qa, Ka, Va
+        else:
+            Qp = torch.randn(B * Hq, ctx, d, device=dev, generator=gen).to(sdt)
+            Kp = torch.randn(B * Hkv, ctx, d, device=dev, generator=gen).to(sdt)
+            Vp = torch.randn(B * Hkv, ctx, d, device=dev, generator=gen).to(sdt)
         ev0.record()
         res = prefill_factorize_device(Qp, Kp, r, dtype=w["dtype"], group=Hq // Hkv)
         ev1.record()
@@ -230,10 +340,10 @@ def run_ours(args, world, rank, local):
     setup_s = time.time() - t0
 
     # ---- per-step inputs: a pool of synthetic decode rows ------------------
-    pool = 8
-    q_pool = torch.randn(pool, L, B, Hq, d, device=dev, generator=gen).to(sdt)
-    k_pool = torch.randn(pool, L, B, Hkv, d, device=dev, generator=gen).to(sdt)
-    v_pool = torch.randn(pool, L, B, Hkv, d, device=dev, generator=gen).to(sdt)
+    if args.data == "random":
+        q_pool = torch.randn(pool, L, B, Hq, d, device=dev, generator=gen).to(sdt)
+        k_pool = torch.randn(pool, L, B, Hkv, d, device=dev, generator=gen).to(sdt)
+        v_pool = torch.randn(pool, L, B, Hkv, d, device=dev, generator=gen).to(sdt)
 
     def load_inputs(i):
         eng.q_buf[..., :d].copy_(q_pool[i % pool], non_blocking=True)
@@ -281,7 +391,8 @@ def run_ours(args, world, rank, local):
     time.sleep(0.3)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
-    miss0 = eng.counters()[0].sum().item()  # cumulative c_miss over layers (CacheStats)
+    cm0, ct0 = eng.counters()
+    miss0, tot0 = cm0.sum().item(), ct0.sum().item()  # cumulative CacheStats over layers and heads
     if world > 1:
         dist.barrier()
     start.record()
@@ -296,7 +407,9 @@ def run_ours(args, world, rank, local):
     ms = start.elapsed_time(stop)
     # miss transfers of the timed steps: with the host slow tier every miss is
     # one K row + one V row read from pinned host memory over PCIe (K5b)
-    misses = eng.counters()[0].sum().item() - miss0
+    cm1, ct1 = eng.counters()
+    misses = cm1.sum().item() - miss0
+    selected = ct1.sum().item() - tot0
     miss_bytes = misses * 2 * d * (2 if w["dtype"] == "bf16" else 4)
     eng.raise_status()
     t_now = int(eng.ctx[0].item())
@@ -382,25 +495,28 @@ def run_ours(args, world, rank, local):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     score_gbs = score_bytes / (score_ms / 1e3) / 1e9
+    traffic, traffic_src = _ncu_traffic(args.workload if args.policy == "hbm" else None, score_bytes)
     step_gbs = byt["total"] * L / (ms_per_step / 1e3) / 1e9
     return dict(
         metric="decode tokens/s at 128K ctx (LLaMA-3-8B shape); proxy-score HBM GB/s",
         value=round(tok_s, 3), unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
         ms_per_step=round(ms_per_step, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
-        dtype=w["dtype"], data="synthetic (random N(0,1) Q/K/V per layer; prompt factorised on GPU)",
-        config=dict(workload=w["desc"], ctx=w["ctx"], layers=L, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d,
-                    rank=r, top_k=k, lite=lite, batch_per_gpu=B, global_batch=total_seq,
-                    slow_tier=args.policy,
-                    parallelism=f"batch-sharded over {world} GPU(s), no collective inside the step; "
-                                f"NCCL all-gather of last-layer outputs per step" if world > 1 else "1 GPU",
-                    l2="no flush: each step streams %.1f GB (> 126 MB L2)" % (byt["total"] * L / 1e9)),
+        dtype=w["dtype"],
+        data={"random": "synthetic (random N(0,1) Q/K/V per layer; prompt factorised on GPU)",
+              "recency": "synthetic recency-biased low-rank Q/K (reference gen_recency_biased structure, r_true=64, "
+                         "decay 0.95, strength 2, scale sqrt(T)); decode rows continue the prompt; prompt factorised "
+                         "on GPU",
+              "drift": "synthetic AR(1)-correlated queries (rho 0.9) over a rank-64 key subspace with the reference's "
+                       "recency bias; decode rows continue the prompt; prompt factorised on GPU"}[args.data],
+        config=config_dict(args, world),
         roofline=dict(bound="hbm", kernel="score_kernel (proxy scores + radix histogram)",
                       achieved=round(score_gbs, 1), peak=hbm_peak, unit="GB/s",
-                      frac=round(score_gbs / hbm_peak, 4), traffic=_ncu_traffic(score_bytes),
+                      frac=round(score_gbs / hbm_peak, 4), traffic=traffic, traffic_source=traffic_src,
                       algorithmic_bytes_per_launch=score_bytes, avg_launch_ms=round(score_ms, 5),
                       step_frac_of_hbm=round(step_gbs / hbm_peak, 4), step_algorithmic_GBps=round(step_gbs, 1),
                       peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"),
         miss_transfers=dict(misses_per_step=round(misses / max(args.steps, 1), 1),
+                            miss_rate=round(misses / max(selected, 1), 4),
                             bytes_per_step=int(miss_bytes / max(args.steps, 1)),
                             host_tier_GBps=round(miss_bytes / (ms / 1e3) / 1e9, 2) if args.policy == "host" else None,
                             note="host policy: K5b zero-copy PCIe reads of the missed K/V rows; "
@@ -419,9 +535,8 @@ def run_ours(args, world, rank, local):
 # --------------------------------------------------------------------------
 # CPU arm: the oracle port of the reference (numpy fp64), bounded sample
 # --------------------------------------------------------------------------
-def _cpu_worker(argtuple):
-    ctx, d, r, k, lite, n_steps, seed = argtuple
-    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+def _cpu_session(ctx, d, r, k, lite, seed):
+    """One reference head session (oracle port) at `ctx` tokens of context."""
     from oracle import lrqk_oracle as O
 
     rng = np.random.default_rng(seed)
@@ -431,57 +546,132 @@ def _cpu_worker(argtuple):
     BQ = rng.standard_normal((r, d)) / math.sqrt(d)
     BK = rng.standard_normal((r, d)) / math.sqrt(d)
     st = O.seed_head(K, V, O.Factors(None, P, BQ, BK), k, lite)
-    # first step fills the resident set to its steady-state size
-    O.head_step(st, rng.standard_normal(d), rng.standard_normal(d), rng.standard_normal(d))
+    return st, rng
+
+
+def _cpu_worker(argtuple):
+    """warm + n timed head-steps of one session; returns seconds per step."""
+    ctx, d, r, k, lite, warm, n_steps, seed = argtuple
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import lrqk_oracle as O
+
+    st, rng = _cpu_session(ctx, d, r, k, lite, seed)
+    for _ in range(max(1, warm)):  # the first step fills the resident set to its steady-state size
+        O.head_step(st, rng.standard_normal(d), rng.standard_normal(d), rng.standard_normal(d))
     t0 = time.perf_counter()
     for _ in range(n_steps):
         O.head_step(st, rng.standard_normal(d), rng.standard_normal(d), rng.standard_normal(d))
     return (time.perf_counter() - t0) / n_steps
 
 
-def cpu_baseline(w, total_seq, budget_s=15.0, steps_override=None):
-    """Time the oracle port on P = cores processes, one head session each, and
-    extrapolate to the whole job (layers x heads x sequences; heads are
-    independent, SPEC.md:222)."""
+def _thread_pool_rate(w, cores, n_steps):
+    """The reference CLI's own fan-out: one session per thread on a
+    ThreadPoolExecutor (cli.py:126-137).  Head-steps per second."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import lrqk_oracle as O
+
+    sess = [_cpu_session(w["ctx"], w["d"], w["r"], w["k"], w["lite"], 100 + i) for i in range(cores)]
+    for st, rng in sess:
+        O.head_step(st, rng.standard_normal(w["d"]), rng.standard_normal(w["d"]), rng.standard_normal(w["d"]))
+
+    def run(i):
+        st, rng = sess[i]
+        for _ in range(n_steps):
+            O.head_step(st, rng.standard_normal(w["d"]), rng.standard_normal(w["d"]), rng.standard_normal(w["d"]))
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as pool:
+        list(pool.map(run, range(cores)))
+    return cores * n_steps / (time.perf_counter() - t0)
+
+
+def _cpu_prefill_s(w):
+    """Oracle prefill_run of one head at the workload's context (1 core)."""
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    from oracle import lrqk_oracle as O
+
+    rng = np.random.default_rng(7)
+    Q = rng.standard_normal((w["ctx"], w["d"]))
+    K = rng.standard_normal((w["ctx"], w["d"]))
+    t0 = time.perf_counter()
+    O.factorize(Q, K, rank=w["r"])
+    return time.perf_counter() - t0
+
+
+def _process_pool_rate(w, cores, warm, n_steps):
     import multiprocessing as mp
 
-    cores = os.cpu_count() or 1
-    ctx = w["ctx"]
-    # probe one step to size the sample
-    probe = _cpu_worker((ctx, w["d"], w["r"], w["k"], w["lite"], 1, 0))
-    n_steps = steps_override or max(2, min(500, int(budget_s / max(probe, 1e-3) / 2)))
+    # one BLAS thread per process: set before the spawned children import numpy
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
     with mp.get_context("spawn").Pool(cores) as pool:
         t0 = time.perf_counter()
-        per = pool.map(_cpu_worker, [(ctx, w["d"], w["r"], w["k"], w["lite"], n_steps, 1 + i) for i in range(cores)])
+        per = pool.map(_cpu_worker, [(w["ctx"], w["d"], w["r"], w["k"], w["lite"], warm, n_steps, 1 + i)
+                                     for i in range(cores)])
         wall = time.perf_counter() - t0
-    head_steps_per_s = cores / float(np.mean(per))
+    return cores / float(np.mean(per)), float(np.mean(per)), wall
+
+
+def cpu_baseline(w, total_seq, budget_s=15.0):
+    """Reference CPU path on this host's cores (reported next to our arm, not
+    the target): the oracle port of DecodeSession.decode_step, one head
+    session per process (processes = cores; the GIL makes the reference's
+    own thread fan-out nearly serial), extrapolated to the whole job
+    (layers x q-heads x sequences head sessions per token; heads are
+    independent).  Also: the thread-pool variant the reference
+    CLI uses, and the single-head prefill time."""
+    cores = os.cpu_count() or 1
+    probe = _cpu_worker((w["ctx"], w["d"], w["r"], w["k"], w["lite"], 1, 1, 0))
+    n_steps = max(2, min(500, int(budget_s / max(probe, 1e-3) / 2)))
+    rate, per, wall = _process_pool_rate(w, cores, 1, n_steps)
     sessions = w["layers"] * w["hq"] * total_seq
-    tok_s = head_steps_per_s / sessions * total_seq
+    tok_s = rate / sessions * total_seq
+    threads = min(cores, 8)  # the GIL serialises them anyway; 8 sessions bound the host memory
+    thr_steps = max(2, min(50, int(5.0 / max(probe * threads, 1e-3))))
+    thr_rate = _thread_pool_rate(w, threads, thr_steps)
+    pre_s = _cpu_prefill_s(w)
     return dict(value=round(tok_s, 5), unit="tokens/s", cores=cores, kind="port",
-                sample=f"{cores} processes x 1 head session ({ctx} ctx, k={w['k']}, r={w['r']}, fp64 numpy oracle) "
-                       f"x {n_steps} decode steps; {np.mean(per)*1e3:.1f} ms/head-step; extrapolated to "
-                       f"{sessions} head sessions per token (layers x q-heads x sequences)",
-                ms_per_head_step=round(float(np.mean(per)) * 1e3, 3), wall_s=round(wall, 1))
+                sample=f"{cores} processes x 1 head session ({w['ctx']} ctx, k={w['k']}, r={w['r']}, fp64 numpy "
+                       f"oracle) x {n_steps} timed decode steps after 1 warm step; {per * 1e3:.1f} ms/head-step; "
+                       f"extrapolated to {sessions} head sessions per token (layers x q-heads x sequences)",
+                ms_per_head_step=round(per * 1e3, 3), wall_s=round(wall, 1),
+                thread_pool=dict(value=round(thr_rate / sessions * total_seq, 5), unit="tokens/s", threads=threads,
+                                 head_steps_per_s=round(thr_rate, 2),
+                                 sample=f"{threads} threads x {thr_steps} head-steps (reference cli.py:126-137 fan-out)"),
+                prefill=dict(s_per_head=round(pre_s, 2), heads_per_token_batch=sessions,
+                             sample=f"oracle prefill_run, one head, {w['ctx']} x {w['d']}, r={w['r']}, 1 core"))
 
 
 def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU path timed on this host's cores.
+    Each of the K timed steps is one decode step of `cores` independent head
+    sessions (one per process) after W untimed ones; tokens/s is then
+    extrapolated to the whole job's head sessions (reported explicitly)."""
     w = workload(args)
     total_seq = args.batch_per_gpu * world
     if rank != 0:
         return None
-    # each "step" of this arm is one bounded parallel sample round
+    cores = os.cpu_count() or 1
     t0 = time.perf_counter()
-    cb = cpu_baseline(w, total_seq, budget_s=args.cpu_sample_s, steps_override=max(2, args.steps // 10))
+    rate, per, _ = _process_pool_rate(w, cores, max(1, args.warmup), args.steps)
     wall = time.perf_counter() - t0
-    ms_per_step = 1e3 * total_seq / cb["value"] if cb["value"] else None
+    sessions = w["layers"] * w["hq"] * total_seq
+    tok_s = rate / sessions * total_seq
+    cfg = config_dict(args, world)
     return dict(metric="decode tokens/s at 128K ctx (LLaMA-3-8B shape); proxy-score HBM GB/s",
-                value=cb["value"], unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-                ms_per_step=round(ms_per_step, 3) if ms_per_step else None, higher_is_better=True,
-                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=w["desc"], ctx=w["ctx"], layers=w["layers"], global_batch=total_seq,
-                            rank=w["r"], top_k=w["k"], lite=w["lite"]),
-                impl="reference", cpu_baseline=dict(cb, value=cb["value"]),
-                e2e=dict(value=cb["value"], unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                value=round(tok_s, 5), unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=round(1e3 * total_seq / tok_s, 3), higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f64", data="synthetic (random N(0,1) K/V/proxy rows per head session)",
+                config=cfg, impl="reference",
+                cpu_baseline=dict(value=round(tok_s, 5), unit="tokens/s", cores=cores, kind="port",
+                                  sample=f"{cores} processes x 1 head session, {args.warmup} warm + {args.steps} timed "
+                                         f"decode steps each ({w['ctx']} ctx, k={w['k']}, r={w['r']}, fp64 numpy "
+                                         f"oracle); {per * 1e3:.1f} ms/head-step"),
+                extrapolation=dict(head_sessions_per_token=sessions, timed_head_steps=cores * args.steps,
+                                   processes=cores, rule="tokens/s = head-steps/s / head sessions per token x sequences"),
+                e2e=dict(value=round(tok_s, 5), unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0,
+                         note="CPU path: inputs and outputs never leave host memory"),
                 wall_s=round(wall, 1))
 
 

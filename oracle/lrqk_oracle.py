@@ -384,12 +384,17 @@ def attend(q, K, V):
 
 class _Rows:
     """Append-only row store with amortised doubling, as the reference's
-    _RowStore (ref: cache.py:21-51), so the oracle's per-step cost matches
-    the reference's rather than an O(t) copy per append."""
+    _RowStore (ref: cache.py:21-51): capacity starts at 16 rows and doubles
+    when full, so after seeding n rows it is the smallest 16 * 2^j >= n and a
+    2^17-row prompt pays its regrowth copy on the first decode append, as in
+    the reference."""
 
-    def __init__(self, rows, extra=16):
+    def __init__(self, rows):
         rows = np.asarray(rows, dtype=np.float64)
-        self.buf = np.empty((max(16, rows.shape[0] + extra), rows.shape[1]))
+        cap = 16
+        while cap < rows.shape[0]:
+            cap *= 2
+        self.buf = np.empty((cap, rows.shape[1]))
         self.buf[: rows.shape[0]] = rows
         self.n = rows.shape[0]
 

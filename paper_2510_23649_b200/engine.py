@@ -278,14 +278,15 @@ class LayerState:
     # ---- decode ----------------------------------------------------------------
     def check_rows(self, q, k, v, out):
         """The C ABI reads q [B,Hq,ds], k/v [B,Hkv,ds] (storage dtype) and
-        writes out [B,Hq,ds] f32 as dense row-major device buffers."""
+        writes out [B,Hq,ds] f32 as dense row-major device buffers (any
+        contiguous view with that many elements)."""
         sh = self.shape
         for name, t, shp, dt in (("q", q, (sh.batch, sh.n_q_heads, sh.dim_stride), self.sdt),
                                  ("k", k, (sh.batch, sh.n_kv_heads, sh.dim_stride), self.sdt),
                                  ("v", v, (sh.batch, sh.n_kv_heads, sh.dim_stride), self.sdt),
                                  ("out", out, (sh.batch, sh.n_q_heads, sh.dim_stride), torch.float32)):
             same_dev = t.is_cuda and (self.device.index is None or t.device.index == self.device.index)
-            if tuple(t.shape) != shp or t.dtype != dt or not t.is_contiguous() or not same_dev:
+            if t.numel() != int(np.prod(shp)) or t.dtype != dt or not t.is_contiguous() or not same_dev:
                 raise ValueError(f"{name}: expected a contiguous {dt} tensor of shape {shp} on {self.device}, got "
                                  f"{t.dtype} {tuple(t.shape)} (contiguous={t.is_contiguous()}) on {t.device}")
 

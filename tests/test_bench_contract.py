@@ -35,10 +35,25 @@ def test_workload_overrides_are_named():
 
 
 def test_ncu_traffic_only_for_the_captured_shape():
+    """roofline.traffic comes from the committed ncu capture of the same
+    workload, scaled to this launch's algorithmic bytes when they are within
+    2 % (a few decode steps apart); otherwise it is null with a reason."""
     import json
-    rec = json.load(open(os.path.join(os.path.dirname(bench.__file__), "profiles", "roofline_traffic.json")))
+    rec = json.load(open(os.path.join(os.path.dirname(bench.__file__), "profiles", "roofline_traffic.json")))["c4"]
     alg = int(rec["algorithmic_bytes_per_launch"])
     assert alg % (32 * (32 * 2 + 4)) == 0  # B*Hq*(t+1)*(R*e + 4) at C4
-    got = bench._ncu_traffic(alg)
-    assert got == int(rec["dram_bytes_per_launch"]) and 0 < got <= alg * 1.05
-    assert bench._ncu_traffic(alg + 32 * 68) is None  # another context length
+    got, src = bench._ncu_traffic("c4", alg)
+    assert got == int(rec["dram_bytes_per_launch"]) and 0 < got <= alg * 1.05 and "ncu" in src
+    got2, _ = bench._ncu_traffic("c4", alg + 50 * 32 * 68)  # 50 tokens later: scaled
+    assert got2 == round(rec["dram_bytes_per_launch"] * (alg + 50 * 32 * 68) / alg)
+    assert bench._ncu_traffic("c4", alg // 2)[0] is None  # another context length
+    assert bench._ncu_traffic("c2", alg)[0] is None       # no capture for that workload
+
+
+def test_reference_arm_config_matches_ours():
+    a = bench.argparse.Namespace(workload="c4", ctx=None, layers=None, rank=None, topk=None, batch_per_gpu=1,
+                                 policy="hbm", data="random")
+    c = bench.config_dict(a, 1)
+    for key in ("workload", "ctx", "layers", "n_q_heads", "n_kv_heads", "head_dim", "rank", "top_k", "lite",
+                "global_batch", "slow_tier", "parallelism"):
+        assert key in c
