@@ -567,6 +567,9 @@ __device__ void count_hits_hbm(const lrqk_layer_t &L, int bh, int n, float *scra
     const int *idx = L.res_idx + (size_t)bh * L.s_cap;
     __syncthreads();
     const bool fresh = meta[M_BITS_FRESH] != 0;
+    // every thread has read the flag before thread 0 may clear it below
+    // (compute-sanitizer synccheck caught warps taking different branches)
+    __syncthreads();
     if (!fresh) {
         // all index loads of a thread in flight together, then the bit loads
         constexpr int UH = 8;
