@@ -279,6 +279,13 @@ typedef struct lrqk_prefill {
     int32_t *converged;     /* [n_heads]                                      */
     float *scratch;         /* lrqk_prefill_scratch_bytes()                   */
     uint32_t *status;
+    /* Optional separate init factors.  NULL: the init is read from A_Q/A_K
+     * (in/out, [n_heads, len, rank_stride]).  Non-NULL: read from here,
+     * [len, rank_stride] when init_shared (one draw for every head, as the
+     * reference's randn init, prefill.py:124-127), else
+     * [n_heads, len, rank_stride].                                        */
+    const float *A_Q0, *A_K0;
+    int32_t init_shared;
 } lrqk_prefill_t;
 
 size_t lrqk_prefill_scratch_bytes(const lrqk_prefill_t *P);

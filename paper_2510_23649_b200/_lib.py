@@ -51,7 +51,8 @@ class PrefillStruct(C.Structure):
                [(n, C.c_float) for n in ("lambda_q", "lambda_k", "tol")] + \
                [("want_objective", C.c_int32)] + \
                [(n, C.c_void_p) for n in ("Q", "K", "A_Q", "A_K", "B_Q", "B_K", "objective", "sweeps",
-                                          "converged", "scratch", "status")]
+                                          "converged", "scratch", "status", "A_Q0", "A_K0")] + \
+               [("init_shared", C.c_int32)]
 
 
 class LibraryUnavailable(RuntimeError):

@@ -1,894 +1,919 @@
-#include <cstdlib>
-// K1: prefill joint rank-r factorisation, batched over heads.
+// K1: the prefill joint rank-r factorisation, in Gram space on the tensor
+// cores.
 //
 // ref: prefill.py:142-230 (lagrangian_value, update_B, update_AK, update_AQ,
-//      _factor_delta, prefill_run).
+//      _factor_delta, prefill_run), linalg.py:63-93 (solve_spd).
 //
-// The reference sweep (B_Q, B_K, A_K, A_Q) is re-associated so that every
-// sweep streams each of K and Q exactly once:
+// Every product of the reference sweep is associated so that X (Q or K)
+// enters only through its d x d Gram GX = X^T X and, once, through the init
+// cross term C0 = X^T A0:
 //
-//   pass P1 (over K):  A_K' = K W_K,   W_K = (C_Q + lk B_K^T)(G_AQ + lk B_K B_K^T)^-1
-//                      and, fused,  G_AK' = A_K'^T A_K',  C_K' = K^T A_K'
-//   pass P2 (over Q):  A_Q' = Q W_Q,   W_Q = (C_K' + lq B_Q^T)(G_AK' + lq B_Q B_Q^T)^-1
-//                      and, fused,  G_AQ' = A_Q'^T A_Q',  C_Q' = Q^T A_Q'
+//   after the first A update, A_X = X W_X for a d x r matrix W_X, so
+//   C_X = X^T A_X = GX W_X,  G_AX = A_X^T A_X = W_X^T GX W_X,
+//   ||A_X' - A_X||^2 = tr(dW^T GX dW),
+//   ||X - A_X B_X||^2 = tr(GX) - 2<B_X^T, C_X> + <G_AX, B_X B_X^T>,
+//   ||Q K^T - A_Q A_K^T||^2 = <GQ, GK> - 2<C_Q, C_K> + <G_AQ, G_AK>
+//   (the reference's own Gram-trace expansion, prefill.py:150-153).
 //
-// where C_X = X^T A_X (d x r) and G_AX = A_X^T A_X (r x r).  update_B is then
-// B_X = G_AX^-1 C_X^T, computed from the fused reductions of the previous
-// pass without touching X again (prefill.py:161-163).  The objective uses the
-// same Gram-trace expansion as the reference (prefill.py:142-158) plus
-// ||X - A B||^2 = ||X||^2 - 2<B, C^T> + <G_A, B B^T>.
+// So the whole factorisation streams each prompt matrix exactly twice:
 //
-// Each pass kernel block owns a slab of rows of one head, keeps its C/G
-// partial sums in registers across 128-row chunks staged in shared memory,
-// and writes one partial; a per-head solve kernel reduces the partials and
-// does the r x r algebra (Gauss-Jordan inverse with the reference jitter
-// retry, linalg.py:80-91).
-#include "common.cuh"
-#include "mma_common.cuh"
+//   K1g  pf_gram_kernel      one TMA -> tcgen05 pass per head:
+//                            D1 = X^T X (128 x 128) and D2 = X^T Y (Y = the
+//                            bf16 hi|lo split of A0), fp32 accumulators in
+//                            TMEM, split over row slabs
+//   K1c  pf_combine_kernel   slab partials -> float64 GX, C0, G0 = A0^T A0
+//   K1s  pf_solve_kernel     one block per query head: every sweep of the
+//                            reference in float64 on d x r / r x r matrices
+//                            (Cholesky with the reference's jitter retry),
+//                            the objective trajectory and the convergence
+//                            test; writes B_Q, B_K and W_Q, W_K
+//   K1m  pf_mat_kernel       one TMA -> tcgen05 pass: A_Q = Q W_Q and
+//                            A_K = K W_K, one K tile serving all the query
+//                            heads of its GQA group (N = heads x 2r)
+//
+// Precision.  bf16 X is exact on the tensor core.  fp32 X is split into bf16
+// hi + lo (|X - hi - lo| <= 2^-17 |X|) and every product takes both parts;
+// fp32 factors (A0, W) are split the same way.  Accumulation is fp32 in
+// TMEM, slab sums and all the d-space algebra are float64.
+#include <cudaTypedefs.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "tc_common.cuh"
 
 namespace lrqk {
 
-constexpr int kPfThreads = 256;
-constexpr int kPfRows = 128;
+constexpr int kTile = 128;                 // rows per TMA tile
+constexpr int kBlkBytes = kTile * 128;     // one 64-column SW128 block of a tile
+constexpr int kMaxMapW = 128;              // widest TMA'd tensor (columns)
+constexpr int kGramThreads = 128;
+constexpr int kMatThreads = 192;           // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+constexpr int kSolveThreads = 256;
+constexpr int kMaxStages = 6;
+constexpr int kWorkMats = 10;              // float64 d x r work matrices per head (solver)
+constexpr size_t kSmemBudget = 200 * 1024;
 
-struct PfDims {
-    int H, group, l, d, ds, r, rs, NB;
-    size_t psz;        // floats per partial
-    size_t head_sz;    // floats of scratch per head
+enum PfMap { MQ = 0, MQL = 1, MK = 2, MKL = 3, MYQ = 4, MYK = 5, kNumMaps = 6 };
+
+struct PfMaps {
+    CUtensorMap m[kNumMaps];
 };
 
-LRQK_DEV size_t pf_part_off(const PfDims &D, int h, int nb) {
-    return (size_t)h * D.head_sz + (size_t)nb * D.psz;
+struct PfGeom {
+    int H, Hk, group, l, d, ds, r, rs;
+    int parts;   // 1: bf16 X, 2: fp32 X as bf16 hi + lo
+    int direct;  // bf16 X TMA'd in place
+    int XW, YW;  // TMA'd widths (64 or 128) of X and of Y = [A0 hi | A0 lo | 0]
+    int shared;  // one A0 for every head (the reference's randn draw)
+    int NY;      // Y tensors per side
+    int NQU, NKU, NU, S, PW, tiles;
+    int NMU, HPU, nsub, S2, Nmax;  // materialize units, heads per K unit, K sub-units per KV head, slabs, max N
+    size_t off_x[4], off_y[2], off_part, off_gq, off_cq, off_gk, off_ck, off_g0q, off_g0k, off_w, off_work, total;
+};
+
+// one Gram unit: D1 = X^T X, D2 = X^T [Y1 | Y2]
+struct GUnit {
+    int xm, xh, y1m, y1h, y2m, y2h;
+};
+
+__host__ __device__ inline int map_width(const PfGeom &G, int m) {
+    return m < 0 ? 0 : (m >= MYQ ? G.YW : G.XW);
 }
-// state block offsets (floats) inside one head's scratch
-struct PfState {
-    size_t CQ, CK, GQ, GK, W, BQp, BKp, misc;
-};
-__host__ __device__ inline PfState pf_state(const PfDims &D) {
-    PfState s;
-    size_t o = (size_t)D.NB * D.psz;
-    const size_t dr = (size_t)D.ds * D.rs, rr = (size_t)D.rs * D.rs;
-    s.CQ = o; o += dr;
-    s.CK = o; o += dr;
-    s.GQ = o; o += rr;
-    s.GK = o; o += rr;
-    s.W = o; o += dr;
-    s.BQp = o; o += dr;
-    s.BKp = o; o += dr;
-    s.misc = o;
+
+__host__ __device__ inline GUnit gram_unit(const PfGeom &G, int u) {
+    GUnit U{-1, 0, -1, 0, -1, 0};
+    const int nq = G.NQU * G.parts, nk = G.NKU * G.parts;
+    if (u < nq + nk) {
+        const bool kside = u >= nq;
+        const int v = kside ? u - nq : u;
+        const int i = v / G.parts, part = v % G.parts;
+        const int xh = kside ? (G.shared ? i : i / G.group) : i;
+        const int yh = G.shared ? 0 : i;
+        const int mx = kside ? MK : MQ, mxl = kside ? MKL : MQL, my = kside ? MYK : MYQ;
+        if (G.parts == 1) U = GUnit{mx, xh, my, yh, -1, 0};
+        else if (part == 0) U = GUnit{mx, xh, mxl, xh, my, yh};
+        else U = GUnit{mxl, xh, my, yh, -1, 0};
+    } else {
+        const int g = u - nq - nk;
+        U = g < G.NY ? GUnit{MYQ, g, -1, 0, -1, 0} : GUnit{MYK, g - G.NY, -1, 0, -1, 0};
+    }
+    return U;
+}
+
+// ---------------------------------------------------------------------------
+// K1g: D1 = X^T X, D2 = X^T Y over one slab of rows of one unit
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kGramThreads, 1)
+pf_gram_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, float *__restrict__ part) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int u = blockIdx.x / G.S, s = blockIdx.x % G.S;
+    const GUnit U = gram_unit(G, u);
+    const int xw = map_width(G, U.xm), w1 = map_width(G, U.y1m), w2 = map_width(G, U.y2m);
+    const int nxb = xw / 64, nyb = (w1 + w2) / 64, ny = w1 + w2;
+    const int stage_bytes = (2 + nyb) * kBlkBytes;
+    const int nst = min(kMaxStages, (int)(kSmemBudget / stage_bytes));
+    uint64_t *full = reinterpret_cast<uint64_t *>(sm + nst * stage_bytes);
+    uint64_t *empty = full + kMaxStages;
+    uint64_t *done = empty + kMaxStages;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(done + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = (int)((long long)G.tiles * s / G.S), t1 = (int)((long long)G.tiles * (s + 1) / G.S);
+
+    if (nxb == 1) {  // X narrower than the 128-row M: the upper block stays zero
+        for (int st = 0; st < nst; ++st)
+            for (int e = threadIdx.x; e < kBlkBytes / 16; e += blockDim.x)
+                reinterpret_cast<uint4 *>(sm + st * stage_bytes + kBlkBytes)[e] = make_uint4(0, 0, 0, 0);
+        tc::fence_proxy_async();
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tc::tma_prefetch(&maps.m[U.xm]);
+        if (U.y1m >= 0) tc::tma_prefetch(&maps.m[U.y1m]);
+        if (U.y2m >= 0) tc::tma_prefetch(&maps.m[U.y2m]);
+    }
+    if (warp == 2) tc::tmem_alloc(tslot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tm = *tslot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----------------------------------------------------
+        const uint64_t pol_x = l2_policy_evict_first(), pol_y = l2_policy_evict_last();
+        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+            const int st = i % nst;
+            mbar_wait(empty + st, ((i / nst) & 1) ^ 1);
+            uint8_t *base = sm + st * stage_bytes;
+            mbar_expect_tx(full + st, (nxb + nyb) * kBlkBytes);
+            for (int b = 0; b < nxb; ++b)
+                tc::tma_load_3d(base + b * kBlkBytes, &maps.m[U.xm], b * 64, t * kTile, U.xh, full + st, pol_x);
+            uint8_t *yb = base + 2 * kBlkBytes;
+            for (int b = 0; b < w1 / 64; ++b, yb += kBlkBytes)
+                tc::tma_load_3d(yb, &maps.m[U.y1m], b * 64, t * kTile, U.y1h, full + st,
+                                U.y1m >= MYQ ? pol_y : pol_x);
+            for (int b = 0; b < w2 / 64; ++b, yb += kBlkBytes)
+                tc::tma_load_3d(yb, &maps.m[U.y2m], b * 64, t * kTile, U.y2h, full + st, pol_y);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer: X^T (MN-major A) against X and Y (MN-major B) --------
+        const uint32_t id1 = tc::idesc_bf16(128, 128, true, true);
+        const uint32_t id2 = tc::idesc_bf16(128, ny > 0 ? ny : 16, true, true);
+        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+            const int st = i % nst;
+            mbar_wait(full + st, (i / nst) & 1);
+            tc::fence_after();
+            const uint32_t base = smem_u32(sm + st * stage_bytes);
+#pragma unroll
+            for (int k = 0; k < kTile / 16; ++k) {
+                const uint64_t ax = tc::desc_sw128(base + k * 2048, kBlkBytes, 1024);
+                const uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
+                tc::mma_bf16(tm, ax, ax, id1, acc);
+                if (ny) {
+                    const uint64_t by = tc::desc_sw128(base + 2 * kBlkBytes + k * 2048, kBlkBytes, 1024);
+                    tc::mma_bf16(tm + 128, ax, by, id2, acc);
+                }
+            }
+            tc::mma_commit(empty + st);
+        }
+        tc::mma_commit(done);
+    }
+    __syncwarp();
+    // ---- epilogue: every warp drains its 32 TMEM lanes (rows of D) ---------
+    mbar_wait(done, 0);
+    tc::fence_after();
+    const int row = warp * 32 + lane;
+    float *dst = part + ((size_t)blockIdx.x * kTile + row) * G.PW;
+    const uint32_t lane_addr = tm + ((uint32_t)(warp * 32) << 16);
+    for (int c = 0; c < 128 + ny; c += 32) {
+        float v[32];
+        tc::tmem_ld32(lane_addr + c, v);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4 *>(dst + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 2) tc::tmem_dealloc(tm, 512);
+}
+
+// ---------------------------------------------------------------------------
+// K1c: slab partials -> float64 GX (mirrored), C0, G0
+// ---------------------------------------------------------------------------
+LRQK_DEV double slab_sum(const PfGeom &G, const float *part, int u, int row, int col) {
+    double s = 0.0;
+    const float *p = part + ((size_t)u * G.S * kTile + row) * G.PW + col;
+    for (int k = 0; k < G.S; ++k) s += (double)p[(size_t)k * kTile * G.PW];  // fixed order
     return s;
 }
-enum PfMisc { PF_ACTIVE = 0, PF_XQ2 = 1, PF_XK2 = 2, PF_QK2 = 3, PF_DAK = 4, PF_DAQ = 5, PF_SWEEP = 6 };
-constexpr int kPfMisc = 16;
 
-// ---------------------------------------------------------------------------
-// pass kernel: optional A update (A_out = X W), then fused C, G reductions
-// ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(kPfThreads)
-pf_pass_kernel(const PfDims D, const T *X, int is_k, const float *A_in, float *A_out, int update,
-               int want_x2, float *scratch) {
-    extern __shared__ __align__(16) float sm[];
-    const int h = blockIdx.y, nb = blockIdx.x, tid = threadIdx.x;
-    const PfState st = pf_state(D);
-    float *hs = scratch + (size_t)h * D.head_sz;
-    if (hs[st.misc + PF_ACTIVE] == 0.f) return;
-    const int ds = D.ds, rs = D.rs;
-    const int ldx = ds + 4, lda = rs + 4;
-    float *sX = sm;                        // [kPfRows][ldx]
-    float *sA = sX + kPfRows * ldx;        // [kPfRows][lda]
-    float *sW = sA + kPfRows * lda;        // [ds][rs]
-    float *sRed = sW + ds * rs;            // reduction scratch
-    const int xh = is_k ? h / D.group : h;
-    const T *Xh = X + (size_t)xh * D.l * ds;
-    const float *Ain = A_in + (size_t)h * D.l * rs;
-    float *Aout = A_out + (size_t)h * D.l * rs;
-    if (update) {
-        const float *W = hs + st.W;
-        for (int e = tid; e < ds * rs; e += blockDim.x) sW[e] = W[e];
-    }
-    // slab of rows for this block
-    const int nchunks = (D.l + kPfRows - 1) / kPfRows;
-    const int c0 = (int)((long long)nchunks * nb / D.NB), c1 = (int)((long long)nchunks * (nb + 1) / D.NB);
-
-    // C tiles (4 k x 4 p) owned by this thread, up to 4
-    const int nCt = (ds / 4) * (rs / 4);
-    float cacc[4][16];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int e = 0; e < 16; ++e) cacc[a][e] = 0.f;
-    // G tiles (4 p x 4 q), row groups
-    const int nGt = (rs / 4) * (rs / 4);
-    const int ngr = max(1, (int)blockDim.x / nGt);
-    float gacc[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) gacc[e] = 0.f;
-    float diff = 0.f, x2 = 0.f;
-
-    for (int c = c0; c < c1; ++c) {
-        const int row0 = c * kPfRows;
-        const int nrow = min(kPfRows, D.l - row0);
-        __syncthreads();
-        // stage X chunk (fp32), zero rows beyond nrow
-        for (int e = tid; e < kPfRows * ds; e += blockDim.x) {
-            const int i = e / ds, k = e - i * ds;
-            float v = i < nrow ? to_float<T>(Xh[(size_t)(row0 + i) * ds + k]) : 0.f;
-            sX[i * ldx + k] = v;
-            x2 = fmaf(v, v, x2);
-        }
-        if (!update) {
-            for (int e = tid; e < kPfRows * rs; e += blockDim.x) {
-                const int i = e / rs, p = e - i * rs;
-                sA[i * lda + p] = i < nrow ? Ain[(size_t)(row0 + i) * rs + p] : 0.f;
+__global__ void pf_combine_kernel(const PfGeom G, const float *__restrict__ part, uint8_t *scr) {
+    const int RS = G.rs;
+    const long long nG = (long long)kTile * kTile, nC = (long long)kTile * RS, n0 = (long long)RS * RS;
+    const long long sQ = (long long)G.NQU * (nG + nC), sK = (long long)G.NKU * (nG + nC);
+    const long long total = sQ + sK + 2LL * G.NY * n0;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        if (e < sQ + sK) {
+            const bool kside = e >= sQ;
+            long long v = kside ? e - sQ : e;
+            const int nunits = kside ? G.NKU : G.NQU;
+            const int ubase = kside ? G.NQU * G.parts : 0;
+            double *gx = reinterpret_cast<double *>(scr + (kside ? G.off_gk : G.off_gq));
+            double *cx = reinterpret_cast<double *>(scr + (kside ? G.off_ck : G.off_cq));
+            if (v < nunits * nG) {
+                const int h = (int)(v / nG), ij = (int)(v % nG), i = ij / kTile, j = ij % kTile;
+                const int a = min(i, j), b = max(i, j);  // gram is exactly symmetric (linalg.py:53-54)
+                const int u = ubase + h * G.parts;
+                double s = slab_sum(G, part, u, a, b);
+                if (G.parts == 2)
+                    s += slab_sum(G, part, u, a, 128 + b) + slab_sum(G, part, u, b, 128 + a) +
+                         slab_sum(G, part, u + 1, a, b);
+                gx[(size_t)h * nG + ij] = s;
+            } else {
+                v -= nunits * nG;
+                const int h = (int)(v / nC), ip = (int)(v % nC), i = ip / RS, p = ip % RS;
+                const int u = ubase + h * G.parts;
+                double s;
+                if (G.parts == 1) s = slab_sum(G, part, u, i, 128 + p) + slab_sum(G, part, u, i, 128 + RS + p);
+                else
+                    s = slab_sum(G, part, u, i, 128 + G.XW + p) + slab_sum(G, part, u, i, 128 + G.XW + RS + p) +
+                        slab_sum(G, part, u + 1, i, 128 + p) + slab_sum(G, part, u + 1, i, 128 + RS + p);
+                cx[(size_t)h * nC + ip] = s;
             }
+        } else {
+            long long v = e - sQ - sK;
+            const int y = (int)(v / n0), pq = (int)(v % n0), p = pq / RS, q = pq % RS;
+            const int a = min(p, q), b = max(p, q);
+            const int u = (G.NQU + G.NKU) * G.parts + y;
+            const double s = slab_sum(G, part, u, a, b) + slab_sum(G, part, u, a, RS + b) +
+                             slab_sum(G, part, u, RS + a, b) + slab_sum(G, part, u, RS + a, RS + b);
+            const bool kside = y >= G.NY;
+            double *g0 = reinterpret_cast<double *>(scr + (kside ? G.off_g0k : G.off_g0q));
+            g0[(size_t)(kside ? y - G.NY : y) * n0 + pq] = s;
         }
-        __syncthreads();
-        if (update) {
-            // A_new = X W, 4 rows x 4 cols per tile
-            const int nAt = (kPfRows / 4) * (rs / 4);
-            for (int tI = tid; tI < nAt; tI += blockDim.x) {
-                const int i0 = (tI / (rs / 4)) * 4, p0 = (tI % (rs / 4)) * 4;
-                float acc[4][4] = {};
-                for (int k = 0; k < ds; k += 4) {
-                    float4 xr[4], wr[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) xr[u] = *reinterpret_cast<const float4 *>(sX + (i0 + u) * ldx + k);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) wr[u] = *reinterpret_cast<const float4 *>(sW + (k + u) * rs + p0);
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const float xs[4] = {xr[u].x, xr[u].y, xr[u].z, xr[u].w};
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            acc[u][0] = fmaf(xs[kk], wr[kk].x, acc[u][0]);
-                            acc[u][1] = fmaf(xs[kk], wr[kk].y, acc[u][1]);
-                            acc[u][2] = fmaf(xs[kk], wr[kk].z, acc[u][2]);
-                            acc[u][3] = fmaf(xs[kk], wr[kk].w, acc[u][3]);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = i0 + u;
-                    if (i < nrow) {
-                        const float4 old = *reinterpret_cast<const float4 *>(Ain + (size_t)(row0 + i) * rs + p0);
-                        const float o4[4] = {old.x, old.y, old.z, old.w};
-                        float n4[4];
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) {
-                            // padded rank columns stay exactly zero
-                            n4[v] = (p0 + v < D.r) ? acc[u][v] : 0.f;
-                            const float df = n4[v] - o4[v];
-                            diff = fmaf(df, df, diff);
-                        }
-                        *reinterpret_cast<float4 *>(Aout + (size_t)(row0 + i) * rs + p0) = make_float4(n4[0], n4[1], n4[2], n4[3]);
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) sA[i * lda + p0 + v] = n4[v];
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < 4; ++v) sA[i * lda + p0 + v] = 0.f;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        // C += X^T A  (4 k x 4 p tiles)
-        for (int a = 0; a < 4; ++a) {
-            const int tI = tid + a * blockDim.x;
-            if (tI >= nCt) break;
-            const int k0 = (tI / (rs / 4)) * 4, p0 = (tI % (rs / 4)) * 4;
-            for (int i = 0; i < nrow; ++i) {
-                const float4 xv = *reinterpret_cast<const float4 *>(sX + i * ldx + k0);
-                const float4 av = *reinterpret_cast<const float4 *>(sA + i * lda + p0);
-                const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, as[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) cacc[a][u * 4 + v] = fmaf(xs[u], as[v], cacc[a][u * 4 + v]);
-            }
-        }
-        // G += A^T A
-        if (tid < nGt * ngr) {
-            const int tI = tid % nGt, grp = tid / nGt;
-            const int p0 = (tI / (rs / 4)) * 4, q0 = (tI % (rs / 4)) * 4;
-            for (int i = grp; i < nrow; i += ngr) {
-                const float4 ap = *reinterpret_cast<const float4 *>(sA + i * lda + p0);
-                const float4 aq = *reinterpret_cast<const float4 *>(sA + i * lda + q0);
-                const float ps[4] = {ap.x, ap.y, ap.z, ap.w}, qs[4] = {aq.x, aq.y, aq.z, aq.w};
-#pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) gacc[u * 4 + v] = fmaf(ps[u], qs[v], gacc[u * 4 + v]);
-            }
-        }
-    }
-    // ---- write this block's partial ------------------------------------------
-    float *part = scratch + pf_part_off(D, h, nb);
-    for (int a = 0; a < 4; ++a) {
-        const int tI = tid + a * blockDim.x;
-        if (tI >= nCt) break;
-        const int k0 = (tI / (rs / 4)) * 4, p0 = (tI % (rs / 4)) * 4;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) part[(k0 + u) * rs + p0 + v] = cacc[a][u * 4 + v];
-    }
-    __syncthreads();
-    if (tid < nGt * ngr) {
-#pragma unroll
-        for (int e = 0; e < 16; ++e) sRed[tid * 16 + e] = gacc[e];
-    }
-    __syncthreads();
-    for (int e = tid; e < nGt * 16; e += blockDim.x) {
-        const int tI = e / 16, uv = e - tI * 16;
-        float s = 0.f;
-        for (int gI = 0; gI < ngr; ++gI) s += sRed[(gI * nGt + tI) * 16 + uv];
-        const int p0 = (tI / (rs / 4)) * 4, q0 = (tI % (rs / 4)) * 4;
-        part[ds * rs + (p0 + uv / 4) * rs + q0 + (uv & 3)] = s;
-    }
-    __syncthreads();
-    float v2[2] = {diff, x2};
-    for (int j = 0; j < 2; ++j) {
-        float s = warp_sum(v2[j]);
-        if ((tid & 31) == 0) sRed[j * 32 + (tid >> 5)] = s;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        float sd = 0.f, sx = 0.f;
-        for (int w = 0; w < (int)blockDim.x / 32; ++w) { sd += sRed[w]; sx += sRed[32 + w]; }
-        part[ds * rs + rs * rs] = sd;
-        part[ds * rs + rs * rs + 1] = want_x2 ? sx : 0.f;
     }
 }
 
 // ---------------------------------------------------------------------------
-// Tensor-core pass (bf16 X, d = 128, rank_stride RS in {16, 32, 64}): the
-// same three products as pf_pass_kernel on mma.sync m16n8k16 with fp32
-// accumulation.  X is exact in bf16; the fp32 operands W and A are split
-// into bf16 hi + lo parts (3xBF16: hi*hi + hi*lo + lo*hi), which keeps the
-// products to ~2^-16 relative, the accuracy class of the fp32 CUDA-core
-// pass.  Per 128-row tile, 8 warps:
-//   A_new = X W      warp w: rows [16w, 16w+16) x all RS columns
-//   C    += X^T A    warp w: d rows [16w, 16w+16) x all RS columns
-//   G    += A^T A    RS/16 x RS/8 tiles spread over the warps
-// The pass is memory-bound (X streamed once, A read/written once), so
-// mma.sync already reaches the HBM roofline.
+// K1s: the reference sweep in d-space, float64, one block per query head
 // ---------------------------------------------------------------------------
-constexpr int kPfD = 128;
+struct SolveSmem {
+    double *GAQ, *GAK, *L, *Li;  // r x r (stride r)
+    double *red;                 // 64
+    int *flag;
+};
 
-LRQK_DEV void ldsm_x4(uint32_t (&r)[4], const void *p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
-}
-LRQK_DEV void ldsm_x2(uint32_t (&r)[2], const void *p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
-                 : "=r"(r[0]), "=r"(r[1]) : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
-}
-LRQK_DEV void split_bf16(float v, __nv_bfloat16 &hi, __nv_bfloat16 &lo) {
-    hi = __float2bfloat16_rn(v);
-    lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-}
-
-template <int RS>
-__global__ void __launch_bounds__(kPfThreads)
-pf_pass_mma_kernel(const PfDims D, const __nv_bfloat16 *X, int is_k, const float *A_in, float *A_out, int update,
-                   int want_x2, float *scratch) {
-    constexpr int NT = RS / 8;                        // n tiles over the rank
-    constexpr int GT = (RS / 16) * (RS / 8);          // G tiles
-    constexpr int GPW = (GT + 7) / 8;                 // G tiles per warp
-    constexpr int LDX = kPfD * 2 + 16, LDA = RS * 2 + 16, LDW = kPfD * 2 + 16;  // bytes
-    extern __shared__ __align__(16) uint8_t pm[];
-    uint8_t *sXb = pm;                                // 2 x [128][LDX]  X tiles (bf16), double buffered
-    uint8_t *sAh = sXb + 2 * kPfRows * LDX;           // [128][LDA]  A tile hi
-    uint8_t *sAl = sAh + kPfRows * LDA;               // [128][LDA]  A tile lo
-    uint8_t *sWh = sAl + kPfRows * LDA;               // [RS][LDW]   W^T hi
-    uint8_t *sWl = sWh + RS * LDW;                    // [RS][LDW]   W^T lo
-    float *sRed = reinterpret_cast<float *>(sWl + RS * LDW);
-    const int h = blockIdx.y, nb = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const PfState st = pf_state(D);
-    float *hs = scratch + (size_t)h * D.head_sz;
-    if (hs[st.misc + PF_ACTIVE] == 0.f) return;
-    const int xh = is_k ? h / D.group : h;
-    const __nv_bfloat16 *Xh = X + (size_t)xh * D.l * kPfD;
-    const float *Ain = A_in + (size_t)h * D.l * RS;
-    float *Aout = A_out + (size_t)h * D.l * RS;
-    if (update) {  // W^T (RS x d), split
-        const float *W = hs + st.W;  // [d][RS]
-        for (int e = tid; e < kPfD * RS; e += blockDim.x) {
-            const int k = e / RS, p = e - k * RS;
-            __nv_bfloat16 hi, lo;
-            split_bf16(W[e], hi, lo);
-            reinterpret_cast<__nv_bfloat16 *>(sWh + p * LDW)[k] = hi;
-            reinterpret_cast<__nv_bfloat16 *>(sWl + p * LDW)[k] = lo;
-        }
-    }
-    const int nchunks = (D.l + kPfRows - 1) / kPfRows;
-    const int c0 = (int)((long long)nchunks * nb / D.NB), c1 = (int)((long long)nchunks * (nb + 1) / D.NB);
-    const int q = lane >> 3, i8 = lane & 7, fr = lane >> 2, fc = (lane & 3) * 2;
-    float cacc[NT][4], gacc[GPW][4];
-    static_assert(kPfD / 8 == 16, "X rows are 16 packs");
-#pragma unroll
-    for (int n = 0; n < NT; ++n)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) cacc[n][e] = 0.f;
-#pragma unroll
-    for (int g = 0; g < GPW; ++g)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) gacc[g][e] = 0.f;
-    float diff = 0.f, x2 = 0.f;
-    // X tiles stream through shared memory with cp.async, one tile ahead
-    auto issue_x = [&](int c) {
-        uint8_t *dst = sXb + (c & 1) * kPfRows * LDX;
-        const int row0 = c * kPfRows, nrow = min(kPfRows, D.l - row0);
-        for (int e = tid; e < kPfRows * (kPfD / 8); e += blockDim.x) {
-            const int i = e >> 4, pk = e & 15;
-            if (i < nrow) cp_async16(dst + i * LDX + pk * 16, Xh + (size_t)(row0 + i) * kPfD + pk * 8);
-            else *reinterpret_cast<uint4 *>(dst + i * LDX + pk * 16) = make_uint4(0, 0, 0, 0);
-        }
-        cp_async_commit();
-    };
-    if (c0 < c1) issue_x(c0);
-    for (int c = c0; c < c1; ++c) {
-        const int row0 = c * kPfRows;
-        const int nrow = min(kPfRows, D.l - row0);
-        uint8_t *sX = sXb + (c & 1) * kPfRows * LDX;
-        __syncthreads();  // the other buffer is free again
-        if (c + 1 < c1) { issue_x(c + 1); cp_async_wait<1>(); }
-        else cp_async_wait<0>();
-        // old A of this warp's rows (update: the convergence measure), early
-        float2 aold[NT][2];
-        if (update) {
-#pragma unroll
-            for (int n = 0; n < NT; ++n)
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    const int i = warp * 16 + fr + hf * 8;
-                    aold[n][hf] = i < nrow ? __ldcs(reinterpret_cast<const float2 *>(Ain + (size_t)(row0 + i) * RS + n * 8 + fc))
-                                           : make_float2(0.f, 0.f);
-                }
-        }
-        __syncthreads();
-        if (want_x2) {
-            for (int e = tid; e < kPfRows * (kPfD / 8); e += blockDim.x) {
-                float f[8];
-                unpack16<__nv_bfloat16>(*reinterpret_cast<const uint4 *>(sX + (e >> 4) * LDX + (e & 15) * 16), f);
-#pragma unroll
-                for (int u = 0; u < 8; ++u) x2 = fmaf(f[u], f[u], x2);
-            }
-        }
-        if (!update) {  // A tile from A_in, split
-            for (int e = tid; e < kPfRows * RS; e += blockDim.x) {
-                const int i = e / RS, p2 = e - i * RS;
-                const float v = i < nrow ? Ain[(size_t)(row0 + i) * RS + p2] : 0.f;
-                __nv_bfloat16 hi, lo;
-                split_bf16(v, hi, lo);
-                reinterpret_cast<__nv_bfloat16 *>(sAh + i * LDA)[p2] = hi;
-                reinterpret_cast<__nv_bfloat16 *>(sAl + i * LDA)[p2] = lo;
-            }
-        }
-        __syncthreads();
-        if (update) {
-            // ---- A_new = X W: warp rows [16w, 16w+16) -------------------------
-            float aacc[NT][4];
-#pragma unroll
-            for (int n = 0; n < NT; ++n)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) aacc[n][e] = 0.f;
-#pragma unroll
-            for (int ks = 0; ks < kPfD; ks += 16) {
-                uint32_t af[4];
-                ldsm_x4(af, sX + (warp * 16 + (lane & 15)) * LDX + (ks + (lane >> 4) * 8) * 2);
-#pragma unroll
-                for (int n = 0; n < NT; ++n) {
-                    uint32_t bh[2], bl[2];
-                    const uint8_t *wrow = (lane & 7) * LDW + (ks + ((lane >> 3) & 1) * 8) * 2 + (size_t)n * 8 * LDW + sWh;
-                    ldsm_x2(bh, wrow);
-                    ldsm_x2(bl, wrow + (sWl - sWh));
-                    mma_bf16_16816(aacc[n], af, bh);
-                    mma_bf16_16816(aacc[n], af, bl);
-                }
-            }
-            // fragment rows fr, fr + 8 of this warp's 16, columns n*8 + fc, +1
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-#pragma unroll
-                for (int hf = 0; hf < 2; ++hf) {
-                    const int i = warp * 16 + fr + hf * 8, p2 = n * 8 + fc;
-                    float v0 = p2 < D.r ? aacc[n][hf * 2] : 0.f, v1 = p2 + 1 < D.r ? aacc[n][hf * 2 + 1] : 0.f;
-                    if (i >= nrow) { v0 = 0.f; v1 = 0.f; }
-                    if (i < nrow) {
-                        const float2 old = aold[n][hf];
-                        diff = fmaf(v0 - old.x, v0 - old.x, diff);
-                        diff = fmaf(v1 - old.y, v1 - old.y, diff);
-                        *reinterpret_cast<float2 *>(Aout + (size_t)(row0 + i) * RS + p2) = make_float2(v0, v1);
-                    }
-                    __nv_bfloat16 h0, l0, h1, l1;
-                    split_bf16(v0, h0, l0);
-                    split_bf16(v1, h1, l1);
-                    __nv_bfloat162 hh, ll;
-                    hh.x = h0; hh.y = h1; ll.x = l0; ll.y = l1;
-                    *reinterpret_cast<__nv_bfloat162 *>(sAh + i * LDA + p2 * 2) = hh;
-                    *reinterpret_cast<__nv_bfloat162 *>(sAl + i * LDA + p2 * 2) = ll;
-                }
-            }
-            __syncthreads();
-        }
-        // ---- C += X^T A: warp d rows [16w, 16w+16) ---------------------------
-#pragma unroll
-        for (int ks = 0; ks < kPfRows; ks += 16) {
-            uint32_t af[4];
-            ldsm_x4_trans(af, sX + (ks + ((q & 2) ? 8 : 0) + i8) * LDX + (warp * 16 + ((q & 1) ? 8 : 0)) * 2);
-            const int k0 = ks + ((lane >> 3) & 1) * 8;
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-                uint32_t bh[2], bl[2];
-                ldsm_x2_trans(bh, sAh + (k0 + i8) * LDA + n * 16);
-                ldsm_x2_trans(bl, sAl + (k0 + i8) * LDA + n * 16);
-                mma_bf16_16816(cacc[n], af, bh);
-                mma_bf16_16816(cacc[n], af, bl);
-            }
-        }
-        // ---- G += A^T A (hi hi + hi lo + lo hi) -------------------------------
-#pragma unroll
-        for (int g = 0; g < GPW; ++g) {
-            const int gt = warp + 8 * g;
-            if (gt >= GT) break;
-            const int mt = gt / NT, n0 = (gt % NT) * 8;
-#pragma unroll
-            for (int ks = 0; ks < kPfRows; ks += 16) {
-                uint32_t ah[4], al[4];
-                const int m0 = mt * 16 + ((q & 1) ? 8 : 0), kk = ks + ((q & 2) ? 8 : 0);
-                ldsm_x4_trans(ah, sAh + (kk + i8) * LDA + m0 * 2);
-                ldsm_x4_trans(al, sAl + (kk + i8) * LDA + m0 * 2);
-                uint32_t bh[2], bl[2];
-                const int k0 = ks + ((lane >> 3) & 1) * 8;
-                ldsm_x2_trans(bh, sAh + (k0 + i8) * LDA + n0 * 2);
-                ldsm_x2_trans(bl, sAl + (k0 + i8) * LDA + n0 * 2);
-                mma_bf16_16816(gacc[g], ah, bh);
-                mma_bf16_16816(gacc[g], ah, bl);
-                mma_bf16_16816(gacc[g], al, bh);
-            }
-        }
-    }
-    // ---- this block's partial: C (d x RS) | G (RS x RS) | diff | x2 ---------
-    float *part = scratch + pf_part_off(D, h, nb);
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-        const int k = warp * 16 + fr, p2 = n * 8 + fc;
-        *reinterpret_cast<float2 *>(part + k * RS + p2) = make_float2(cacc[n][0], cacc[n][1]);
-        *reinterpret_cast<float2 *>(part + (k + 8) * RS + p2) = make_float2(cacc[n][2], cacc[n][3]);
-    }
-#pragma unroll
-    for (int g = 0; g < GPW; ++g) {
-        const int gt = warp + 8 * g;
-        if (gt >= GT) break;
-        const int mt = gt / NT, n0 = (gt % NT) * 8;
-        float *gp = part + kPfD * RS + (mt * 16 + fr) * RS + n0 + fc;
-        *reinterpret_cast<float2 *>(gp) = make_float2(gacc[g][0], gacc[g][1]);
-        *reinterpret_cast<float2 *>(gp + 8 * RS) = make_float2(gacc[g][2], gacc[g][3]);
-    }
-    float v2[2] = {diff, x2};
-    for (int j = 0; j < 2; ++j) {
-        const float sj = warp_sum(v2[j]);
-        if (lane == 0) sRed[j * 32 + warp] = sj;
-    }
+LRQK_DEV double block_sum_d(double v, double *red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     __syncthreads();
-    if (tid == 0) {
-        float sd = 0.f, sx = 0.f;
-        for (int w = 0; w < (int)blockDim.x / 32; ++w) { sd += sRed[w]; sx += sRed[32 + w]; }
-        part[kPfD * RS + RS * RS] = sd;
-        part[kPfD * RS + RS * RS + 1] = want_x2 ? sx : 0.f;
-    }
-}
-
-template <int RS>
-static size_t pf_mma_smem() {
-    return 2 * (size_t)kPfRows * (kPfD * 2 + 16) + 2 * (size_t)kPfRows * (RS * 2 + 16) +
-           2 * (size_t)RS * (kPfD * 2 + 16) + 64 * sizeof(float);
-}
-
-// d x d Gram of X (objective only): GX[i][j] = sum_l X[l][i] X[l][j]
-template <typename T>
-__global__ void pf_gram_dd_kernel(const PfDims D, const T *X, int n_x, float *out /* [n_x][ds][ds] */) {
-    const int xh = blockIdx.y;
-    const int i = blockIdx.x;  // row of the Gram
-    const T *Xh = X + (size_t)xh * D.l * D.ds;
-    for (int j = threadIdx.x; j < D.ds; j += blockDim.x) {
-        double acc = 0.0;
-        for (int l = 0; l < D.l; ++l)
-            acc += (double)to_float<T>(Xh[(size_t)l * D.ds + i]) * (double)to_float<T>(Xh[(size_t)l * D.ds + j]);
-        out[((size_t)xh * D.ds + i) * D.ds + j] = (float)acc;
-    }
-    (void)n_x;
-}
-
-// sum of GQ o GK over the d x d Grams, per query head
-__global__ void pf_qk2_kernel(const PfDims D, const float *gq, const float *gk, float *scratch) {
-    const int h = blockIdx.x;
-    const float *a = gq + (size_t)h * D.ds * D.ds;
-    const float *b = gk + (size_t)(h / D.group) * D.ds * D.ds;
-    __shared__ double s[32];
-    double acc = 0.0;
-    for (int e = threadIdx.x; e < D.ds * D.ds; e += blockDim.x) acc += (double)a[e] * (double)b[e];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < (int)blockDim.x / 32; ++w) t += s[w];
-        const PfState st = pf_state(D);
-        scratch[(size_t)h * D.head_sz + st.misc + PF_QK2] = (float)t;
-    }
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];  // fixed order
+    __syncthreads();
+    return t;
 }
 
-// ---------------------------------------------------------------------------
-// per-head r x r algebra
-// ---------------------------------------------------------------------------
-// Invert an SPD n x n (row stride ld) into Minv (stride ld) with the
-// reference's single jitter retry.  Returns 0 ok, 1 jittered, 2 failed.
-__device__ int spd_inverse(const float *M, int n, int ld, float *Minv) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+// M^-1 (r x r, stride r) into Li through Cholesky (L, lower) with the
+// reference's single jitter retry M + 1e-10 (tr(M)/r + 1) I
+// (linalg.py:80-91).  Returns 0 ok, 1 jittered, 2 failed, 3 non-finite M.
+__device__ int chol_inverse(const double *M, int r, double *L, double *Li, double *red) {
+    double bad = 0.0;
+    for (int e = threadIdx.x; e < r * r; e += blockDim.x) bad += isfinite(M[e]) ? 0.0 : 1.0;
+    if (block_sum_d(bad, red) != 0.0) return 3;
+    double tr = 0.0;
+    for (int i = threadIdx.x; i < r; i += blockDim.x) tr += M[i * r + i];
+    tr = block_sum_d(tr, red);
     __shared__ int s_fail;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        float jit = 0.f;
-        if (attempt) {
-            float tr = 0.f, dmax = 0.f;
-            for (int i = 0; i < n; ++i) { tr += M[i * ld + i]; dmax = fmaxf(dmax, fabsf(M[i * ld + i])); }
-            jit = fmaxf(1e-10f * (tr / n + 1.f), dmax * 1.2e-7f);
+        const double jit = attempt ? 1e-10 * (tr / r + 1.0) : 0.0;
+        for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+            const int i = e / r, j = e % r;
+            L[e] = i >= j ? M[e] + (i == j ? jit : 0.0) : 0.0;
         }
+        if (threadIdx.x == 0) s_fail = 0;
         __syncthreads();
-        for (int e = tid; e < n * n; e += nt) {
-            const int i = e / n, j = e - i * n;
-            Minv[i * ld + j] = M[i * ld + j] + (i == j ? jit : 0.f);
-        }
-        if (tid == 0) s_fail = 0;
-        for (int k = 0; k < n; ++k) {
+        for (int k = 0; k < r; ++k) {
+            const double pk = L[k * r + k];
+            if (!(pk > 0.0)) { if (threadIdx.x == 0) s_fail = 1; break; }  // uniform: all read pk
+            const double lkk = sqrt(pk);
             __syncthreads();
-            const float p = Minv[k * ld + k];
-            if (!(p > 0.f) || !isfinite(p)) { if (tid == 0) s_fail = 1; break; }
-            const float ip = 1.f / p;
-            float nv[24];
-            int cnt = 0;
-            for (int e = tid; e < n * n; e += nt) {
-                const int i = e / n, j = e - i * n;
-                const float a = Minv[i * ld + j];
-                float rr;
-                if (i == k && j == k) rr = ip;
-                else if (i == k) rr = a * ip;
-                else if (j == k) rr = -a * ip;
-                else rr = a - Minv[i * ld + k] * Minv[k * ld + j] * ip;
-                nv[cnt++] = rr;
+            if (threadIdx.x == 0) L[k * r + k] = lkk;
+            for (int i = k + 1 + threadIdx.x; i < r; i += blockDim.x) L[i * r + k] /= lkk;
+            __syncthreads();
+            const int m = r - k - 1;
+            for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+                const int i = k + 1 + e / m, j = k + 1 + e % m;
+                if (j <= i) L[i * r + j] -= L[i * r + k] * L[j * r + k];
             }
             __syncthreads();
-            cnt = 0;
-            for (int e = tid; e < n * n; e += nt) {
-                const int i = e / n, j = e - i * n;
-                Minv[i * ld + j] = nv[cnt++];
-            }
         }
         __syncthreads();
-        if (!s_fail) return attempt;
+        if (!s_fail) {
+            // Li = L^-1 (lower), one column per thread
+            for (int c = threadIdx.x; c < r; c += blockDim.x) {
+                for (int i = 0; i < r; ++i) {
+                    double v;
+                    if (i < c) v = 0.0;
+                    else if (i == c) v = 1.0 / L[c * r + c];
+                    else {
+                        double s = 0.0;
+                        for (int k = c; k < i; ++k) s += L[i * r + k] * Li[k * r + c];
+                        v = -s / L[i * r + i];
+                    }
+                    Li[i * r + c] = v;
+                }
+            }
+            __syncthreads();
+            // M^-1 = L^-T L^-1 into L
+            for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+                const int p = e / r, q = e % r;
+                double s = 0.0;
+                for (int k = max(p, q); k < r; ++k) s += Li[k * r + p] * Li[k * r + q];
+                L[e] = s;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < r * r; e += blockDim.x) Li[e] = L[e];
+            __syncthreads();
+            return attempt;
+        }
     }
     return 2;
 }
 
-// stage: 0 = after the init passes, 1 = after the K pass, 2 = after the Q pass
-__global__ void __launch_bounds__(kPfThreads)
-pf_solve_kernel(const PfDims D, lrqk_prefill_t P, int stage, int sweep) {
-    extern __shared__ __align__(16) float sm[];
+__global__ void __launch_bounds__(kSolveThreads)
+pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
+    extern __shared__ __align__(16) double sd[];
     const int h = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    const PfState st = pf_state(D);
-    float *hs = P.scratch + (size_t)h * D.head_sz;
-    float *misc = hs + st.misc;
-    const int ds = D.ds, rs = D.rs, r = D.r, d = D.d;
-    const float lq = P.lambda_q, lk = P.lambda_k;
-    if (misc[PF_ACTIVE] == 0.f) return;
-    const int ldm = rs + 1;
-    float *sM = sm;                 // [rs][ldm]
-    float *sMi = sM + rs * ldm;     // [rs][ldm]
-    float *sB = sMi + rs * ldm;     // [rs][ds]  current B (side being solved)
-    float *sRed = sB + rs * ds;     // 64
-    float *BQ = P.B_Q + (size_t)h * rs * ds;
-    float *BK = P.B_K + (size_t)h * rs * ds;
+    const int r = G.r, d = G.d, RS = G.rs, D = kTile;
+    const double lq = P.lambda_q, lk = P.lambda_k;
+    double *GAQ = sd, *GAK = GAQ + r * r, *Lm = GAK + r * r, *Li = Lm + r * r, *Mm = Li + r * r, *red = Mm + r * r;
+    const int ku = G.shared ? h / G.group : h;
+    const int yq = G.shared ? 0 : h;
+    const double *GQ = reinterpret_cast<const double *>(scr + G.off_gq) + (size_t)h * D * D;
+    const double *GK = reinterpret_cast<const double *>(scr + G.off_gk) + (size_t)ku * D * D;
+    const double *CQ0 = reinterpret_cast<const double *>(scr + G.off_cq) + (size_t)h * D * RS;
+    const double *CK0 = reinterpret_cast<const double *>(scr + G.off_ck) + (size_t)ku * D * RS;
+    const double *G0Q = reinterpret_cast<const double *>(scr + G.off_g0q) + (size_t)yq * RS * RS;
+    const double *G0K = reinterpret_cast<const double *>(scr + G.off_g0k) + (size_t)yq * RS * RS;
+    // float64 work, d x r (stride r) or r x d (stride d)
+    double *wk = reinterpret_cast<double *>(scr + G.off_work) + (size_t)h * kWorkMats * D * RS;
+    double *Cq = wk, *Ck = Cq + D * RS, *Wq = Ck + D * RS, *Wk = Wq + D * RS, *Wn = Wk + D * RS, *Dt = Wn + D * RS;
+    double *Bq = Dt + D * RS, *Bk = Bq + D * RS, *Boq = Bk + D * RS, *Bok = Boq + D * RS;
+    float *Wout = reinterpret_cast<float *>(scr + G.off_w);  // [2][H][128][RS] fp32 (Q then K)
+    float *obj = P.objective ? P.objective + (size_t)h * (P.max_iter + 1) : nullptr;
 
-    // reduce the pass partials into C (ds x rs), G (rs x rs), diff, x2
-    auto reduce_into = [&](float *C, float *G, float *diff, float *x2) {
-        for (int e = tid; e < ds * rs + rs * rs + 2; e += nt) {
-            float s = 0.f;
-            for (int nb = 0; nb < D.NB; ++nb) s += hs[(size_t)nb * D.psz + e];
-            if (e < ds * rs) C[e] = s;
-            else if (e < ds * rs + rs * rs) {
-                const int f = e - ds * rs;
-                const int p = f / rs, q = f - p * rs;
-                if (p <= q) { G[p * rs + q] = s; }
-            } else if (e == ds * rs + rs * rs) *diff = s;
-            else if (x2) *x2 = s;
+    // Gram-trace constants
+    double qk2 = 0.0, tq = 0.0, tk = 0.0;
+    for (int e = tid; e < d * d; e += nt) {
+        const int i = e / d, j = e % d;
+        qk2 += GQ[i * D + j] * GK[i * D + j];
+        if (i == j) { tq += GQ[i * D + i]; tk += GK[i * D + i]; }
+    }
+    qk2 = block_sum_d(qk2, red);
+    tq = block_sum_d(tq, red);
+    tk = block_sum_d(tk, red);
+    for (int e = tid; e < d * r; e += nt) {
+        const int i = e / r, p = e % r;
+        Cq[e] = CQ0[i * RS + p];
+        Ck[e] = CK0[i * RS + p];
+    }
+    for (int e = tid; e < r * r; e += nt) {
+        const int p = e / r, q = e % r;
+        GAQ[e] = G0Q[p * RS + q];
+        GAK[e] = G0K[p * RS + q];
+    }
+    for (int e = tid; e < r * d; e += nt) { Bq[e] = 0.0; Bk[e] = 0.0; }
+    double trg0q = 0.0, trg0k = 0.0;
+    for (int p = tid; p < r; p += nt) { trg0q += G0Q[p * RS + p]; trg0k += G0K[p * RS + p]; }
+    trg0q = block_sum_d(trg0q, red);
+    trg0k = block_sum_d(trg0k, red);
+    __syncthreads();
+
+    // lagrangian_value (prefill.py:142-158) from the Gram-space quantities
+    auto objective = [&]() -> double {
+        double cross = 0.0, approx = 0.0, rq = 0.0, rk = 0.0;
+        for (int e = tid; e < d * r; e += nt) {
+            const int i = e / r, p = e % r;
+            cross += Cq[e] * Ck[e];
+            rq -= 2.0 * Bq[p * d + i] * Cq[e];
+            rk -= 2.0 * Bk[p * d + i] * Ck[e];
         }
-        __syncthreads();
-        for (int e = tid; e < rs * rs; e += nt) {  // mirror upper -> lower (linalg.py:53-54)
-            const int p = e / rs, q = e - p * rs;
-            if (p > q) G[p * rs + q] = G[q * rs + p];
-        }
-        __syncthreads();
-    };
-    // B = G^-1 C^T  (update_B, prefill.py:161-163) into dst (rs x ds)
-    auto solve_B = [&](const float *G, const float *C, float *dst) -> bool {
-        for (int e = tid; e < r * r; e += nt) sM[(e / r) * ldm + e % r] = G[(e / r) * rs + e % r];
-        const int rc = spd_inverse(sM, r, ldm, sMi);
-        if (rc == 2) return false;
-        if (rc == 1 && tid == 0) set_status(P.status, LRQK_ST_JITTERED);
-        for (int e = tid; e < rs * ds; e += nt) {
-            const int p = e / ds, i = e - p * ds;
-            float acc = 0.f;
-            if (p < r && i < d)
-                for (int q = 0; q < r; ++q) acc = fmaf(sMi[p * ldm + q], C[i * rs + q], acc);
-            dst[e] = acc;
-        }
-        __syncthreads();
-        return true;
-    };
-    // W = (C + lam B^T) (G + lam B B^T)^-1  (update_AK / update_AQ)
-    auto solve_W = [&](const float *G, const float *C, const float *B, float lam, float *W) -> bool {
         for (int e = tid; e < r * r; e += nt) {
-            const int p = e / r, q = e - p * r;
-            float bb = 0.f;
-            for (int i = 0; i < d; ++i) bb = fmaf(B[p * ds + i], B[q * ds + i], bb);
-            sM[p * ldm + q] = G[p * rs + q] + lam * bb;
+            const int p = e / r, q = e % r;
+            approx += GAQ[e] * GAK[e];
+            double bbq = 0.0, bbk = 0.0;
+            for (int i = 0; i < d; ++i) { bbq += Bq[p * d + i] * Bq[q * d + i]; bbk += Bk[p * d + i] * Bk[q * d + i]; }
+            rq += GAQ[e] * bbq;
+            rk += GAK[e] * bbk;
         }
-        __syncthreads();
-        for (int e = tid; e < r * r; e += nt) {  // exact symmetry
-            const int p = e / r, q = e - p * r;
-            if (p > q) sM[p * ldm + q] = sM[q * ldm + p];
-        }
-        const int rc = spd_inverse(sM, r, ldm, sMi);
-        if (rc == 2) return false;
-        if (rc == 1 && tid == 0) set_status(P.status, LRQK_ST_JITTERED);
-        for (int e = tid; e < ds * rs; e += nt) {
-            const int i = e / rs, p = e - i * rs;
-            float acc = 0.f;
-            if (p < r && i < d)
-                for (int q = 0; q < r; ++q) acc = fmaf(C[i * rs + q] + lam * B[q * ds + i], sMi[q * ldm + p], acc);
-            W[e] = acc;
+        cross = block_sum_d(cross, red);
+        approx = block_sum_d(approx, red);
+        rq = block_sum_d(rq, red) + tq;
+        rk = block_sum_d(rk, red) + tk;
+        return 0.5 * fmax(qk2 - 2.0 * cross + approx, 0.0) + 0.5 * lq * rq + 0.5 * lk * rk;
+    };
+    auto fail = [&](uint32_t bit) {
+        if (tid == 0) set_status(P.status, bit);
+    };
+    // B = G_A^-1 C^T (update_B, prefill.py:161-163), r x d
+    auto update_B = [&](const double *GA, const double *Cx, double *B) -> bool {
+        const int rc = chol_inverse(GA, r, Lm, Li, red);
+        if (rc >= 2) { fail(rc == 3 ? LRQK_ST_NONFINITE : LRQK_ST_SOLVE_FAILED); return false; }
+        if (rc == 1) fail(LRQK_ST_JITTERED);
+        for (int e = tid; e < r * d; e += nt) {
+            const int p = e / d, i = e % d;
+            double s = 0.0;
+            for (int q = 0; q < r; ++q) s += Li[p * r + q] * Cx[i * r + q];
+            B[e] = s;
         }
         __syncthreads();
         return true;
     };
-    // objective (prefill.py:142-158) from the reduced quantities
-    auto objective = [&]() -> float {
-        const float *CQ = hs + st.CQ, *CK = hs + st.CK, *GQ = hs + st.GQ, *GK = hs + st.GK;
-        double acc[4] = {0, 0, 0, 0};  // cross, approx, q-resid-part, k-resid-part
-        for (int e = tid; e < ds * rs; e += nt) {
-            acc[0] += (double)CQ[e] * CK[e];
-            const int i = e / rs, p = e - i * rs;
-            acc[2] += -2.0 * (double)BQ[p * ds + i] * CQ[e];
-            acc[3] += -2.0 * (double)BK[p * ds + i] * CK[e];
+    // Wn = (Cx + lam B^T)(G_A + lam B B^T)^-1 (update_AK / update_AQ, prefill.py:166-181)
+    auto update_W = [&](const double *GA, const double *Cx, const double *B, double lam) -> bool {
+        for (int e = tid; e < r * r; e += nt) {
+            const int p = e / r, q = e % r;
+            double bb = 0.0;
+            for (int i = 0; i < d; ++i) bb += B[p * d + i] * B[q * d + i];
+            Mm[e] = GA[e] + lam * bb;
         }
-        for (int e = tid; e < rs * rs; e += nt) {
-            const int p = e / rs, q = e - p * rs;
-            acc[1] += (double)GQ[e] * GK[e];
-            double bbq = 0, bbk = 0;
-            for (int i = 0; i < ds; ++i) {
-                bbq += (double)BQ[p * ds + i] * BQ[q * ds + i];
-                bbk += (double)BK[p * ds + i] * BK[q * ds + i];
+        __syncthreads();
+        const int rc = chol_inverse(Mm, r, Lm, Li, red);
+        if (rc >= 2) { fail(rc == 3 ? LRQK_ST_NONFINITE : LRQK_ST_SOLVE_FAILED); return false; }
+        if (rc == 1) fail(LRQK_ST_JITTERED);
+        for (int e = tid; e < d * r; e += nt) {
+            const int i = e / r, p = e % r;
+            double s = 0.0;
+            for (int q = 0; q < r; ++q) s += (Cx[i * r + q] + lam * B[q * d + i]) * Li[q * r + p];
+            Wn[e] = s;
+        }
+        __syncthreads();
+        return true;
+    };
+    // out = GX X (d x r)
+    auto gram_times = [&](const double *GX, const double *X, double *out) {
+        for (int e = tid; e < d * r; e += nt) {
+            const int i = e / r, p = e % r;
+            double s = 0.0;
+            for (int j = 0; j < d; ++j) s += GX[i * D + j] * X[j * r + p];
+            out[e] = s;
+        }
+        __syncthreads();
+    };
+    // after Wn: new C, G_A, and ||A' - A||^2 (sweep 1: against the init A0)
+    auto advance = [&](const double *GX, double *W, double *Cx, double *GA, const double *C0, double trg0,
+                       bool first) -> double {
+        double diff = 0.0;
+        if (first) {
+            gram_times(GX, Wn, Cx);
+            for (int e = tid; e < d * r; e += nt) diff += Wn[e] * (Cx[e] - 2.0 * C0[(e / r) * RS + e % r]);
+            diff = block_sum_d(diff, red) + trg0;
+        } else {
+            for (int e = tid; e < d * r; e += nt) W[e] = Wn[e] - W[e];  // dW
+            __syncthreads();
+            gram_times(GX, W, Dt);
+            for (int e = tid; e < d * r; e += nt) { diff += W[e] * Dt[e]; Cx[e] += Dt[e]; }
+            diff = block_sum_d(diff, red);
+        }
+        for (int e = tid; e < d * r; e += nt) W[e] = Wn[e];
+        __syncthreads();
+        for (int e = tid; e < r * r; e += nt) {
+            const int p = e / r, q = e % r;
+            double s = 0.0, t = 0.0;
+            for (int i = 0; i < d; ++i) { s += W[i * r + p] * Cx[i * r + q]; t += W[i * r + q] * Cx[i * r + p]; }
+            GA[e] = 0.5 * (s + t);
+        }
+        __syncthreads();
+        return fmax(diff, 0.0);
+    };
+
+    if (obj) {
+        const double o = objective();
+        if (tid == 0) {
+            obj[0] = (float)o;
+            for (int i = 1; i <= P.max_iter; ++i) obj[i] = __int_as_float(0x7fc00000);
+        }
+    }
+    int sweeps = 0, conv = 0, ok = 1;
+    for (int s = 0; s < P.max_iter; ++s) {
+        // old B factors for the convergence measure (into Dt: r x d each)
+        double dbq = 0.0, dbk = 0.0;
+        for (int e = tid; e < r * d; e += nt) { Boq[e] = Bq[e]; Bok[e] = Bk[e]; }
+        __syncthreads();
+        if (!update_B(GAQ, Cq, Bq) || !update_B(GAK, Ck, Bk)) { ok = 0; break; }
+        for (int e = tid; e < r * d; e += nt) {
+            const double a = Bq[e] - Boq[e], b = Bk[e] - Bok[e];
+            dbq += a * a;
+            dbk += b * b;
+        }
+        dbq = block_sum_d(dbq, red);
+        dbk = block_sum_d(dbk, red);
+        if (!update_W(GAQ, Cq, Bk, lk)) { ok = 0; break; }
+        const double dak = advance(GK, Wk, Ck, GAK, CK0, trg0k, s == 0);
+        if (!update_W(GAK, Ck, Bq, lq)) { ok = 0; break; }
+        const double daq = advance(GQ, Wq, Cq, GAQ, CQ0, trg0q, s == 0);
+        ++sweeps;
+        // non-finite factors (prefill.py:216-218)
+        double bad = isfinite(dak) && isfinite(daq) && isfinite(dbq) && isfinite(dbk) ? 0.0 : 1.0;
+        for (int e = tid; e < d * r; e += nt) bad += (isfinite(Wq[e]) && isfinite(Wk[e])) ? 0.0 : 1.0;
+        if (block_sum_d(bad, red) != 0.0) { fail(LRQK_ST_NONFINITE); ok = 0; break; }
+        if (obj) {
+            const double o = objective();
+            if (tid == 0) obj[s + 1] = (float)o;
+        }
+        // _factor_delta (prefill.py:184-194): mean over the four factors
+        const double lr = (double)G.l * r, rd = (double)r * d;
+        const double delta = (daq / lr + dak / lr + dbq / rd + dbk / rd) / 4.0;
+        if (delta <= (double)P.tol) { conv = 1; break; }
+    }
+    if (tid == 0) { P.sweeps[h] = sweeps; P.converged[h] = conv; }
+    // outputs: B (fp32, [RS][ds] zero-padded) and W for the materialize pass
+    float *BQo = P.B_Q + (size_t)h * RS * G.ds, *BKo = P.B_K + (size_t)h * RS * G.ds;
+    for (int e = tid; e < RS * G.ds; e += nt) {
+        const int p = e / G.ds, i = e % G.ds;
+        const bool in = ok && p < r && i < d;
+        BQo[e] = in ? (float)Bq[p * d + i] : 0.f;
+        BKo[e] = in ? (float)Bk[p * d + i] : 0.f;
+    }
+    float *WQo = Wout + (size_t)h * D * RS, *WKo = Wout + ((size_t)G.H + h) * D * RS;
+    for (int e = tid; e < D * RS; e += nt) {
+        const int i = e / RS, p = e % RS;
+        const bool in = ok && sweeps > 0 && p < r && i < d;
+        WQo[e] = in ? (float)Wq[i * r + p] : 0.f;
+        WKo[e] = in ? (float)Wk[i * r + p] : 0.f;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1m: A = X W for the query heads of one unit (TMA -> tcgen05 -> TMEM ->
+// fp32 rows), double-buffered accumulators
+// ---------------------------------------------------------------------------
+__host__ __device__ inline void mat_unit(const PfGeom &G, int u, int &kside, int &xh, int &h0, int &nh) {
+    if (u < G.H) { kside = 0; xh = u; h0 = u; nh = 1; return; }
+    const int v = u - G.H, g = v / G.nsub, sb = v % G.nsub;
+    kside = 1;
+    xh = g;
+    h0 = g * G.group + sb * G.HPU;
+    nh = min(G.HPU, G.group - sb * G.HPU);
+}
+
+__global__ void __launch_bounds__(kMatThreads, 1)
+pf_mat_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, const float *__restrict__ W, float *A_Q, float *A_K) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int u = blockIdx.x / G.S2, s = blockIdx.x % G.S2;
+    int kside, xh, h0, nh;
+    mat_unit(G, u, kside, xh, h0, nh);
+    const int RS = G.rs, N = nh * 2 * RS;  // accumulator columns: per head [hi-part | lo-part]
+    const int nxb = G.XW / 64, npart = G.parts;
+    const int stage_bytes = npart * 2 * kBlkBytes;
+    const int wbytes = 2 * G.Nmax * 128;  // W^T split, K-major SW128: [2 d-blocks][N rows][128 B]
+    const int nst = min(kMaxStages, (int)((kSmemBudget - wbytes) / stage_bytes));
+    uint8_t *sW = sm + nst * stage_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(sW + wbytes);
+    uint64_t *empty = full + kMaxStages;
+    uint64_t *tfull = empty + kMaxStages;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = (int)((long long)G.tiles * s / G.S2), t1 = (int)((long long)G.tiles * (s + 1) / G.S2);
+    const uint32_t ncols = N <= 16 ? 32 : (N <= 32 ? 64 : (N <= 64 ? 128 : (N <= 128 ? 256 : 512)));
+    const int mx = kside ? MK : MQ, mxl = kside ? MKL : MQL;
+
+    // stage W^T (rows n = head j, column c of [hi | lo]; K = d) with the swizzle
+    const float *Wsrc = W + ((size_t)(kside ? G.H : 0) + h0) * kTile * RS;
+    for (int e = threadIdx.x; e < N * (kTile / 8); e += blockDim.x) {
+        const int n = e / (kTile / 8), ch = e % (kTile / 8);  // 8 d-values per 16-B chunk
+        const int j = n / (2 * RS), c = n % (2 * RS), p = c % RS, lo = c >= RS;
+        uint32_t pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            __nv_bfloat16 v2[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const float w = Wsrc[((size_t)j * kTile + ch * 8 + q * 2 + t) * RS + p];
+                const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+                v2[t] = lo ? __float2bfloat16_rn(w - __bfloat162float(hi)) : hi;
             }
-            acc[2] += (double)GQ[e] * bbq;
-            acc[3] += (double)GK[e] * bbk;
+            pk[q] = (uint32_t)__bfloat16_as_ushort(v2[0]) | ((uint32_t)__bfloat16_as_ushort(v2[1]) << 16);
         }
-        __shared__ double sacc[4][32];
-        for (int j = 0; j < 4; ++j) {
-            double v = acc[j];
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if ((tid & 31) == 0) sacc[j][tid >> 5] = v;
-        }
-        __syncthreads();
-        double tot[4] = {0, 0, 0, 0};
-        for (int j = 0; j < 4; ++j)
-            for (int w = 0; w < nt / 32; ++w) tot[j] += sacc[j][w];
-        __syncthreads();
-        const double fit = fmax((double)misc[PF_QK2] - 2.0 * tot[0] + tot[1], 0.0);
-        const double rq = fmax((double)misc[PF_XQ2] + tot[2], 0.0);
-        const double rk = fmax((double)misc[PF_XK2] + tot[3], 0.0);
-        return (float)(0.5 * fit + 0.5 * lq * rq + 0.5 * lk * rk);
-    };
-    auto fail = [&]() {
-        if (tid == 0) { set_status(P.status, LRQK_ST_SOLVE_FAILED); misc[PF_ACTIVE] = 0.f; }
-    };
+        const int kb = ch / 8, c16 = ch % 8;
+        *reinterpret_cast<uint4 *>(sW + kb * N * 128 + n * 128 + ((c16 ^ (n & 7)) * 16)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    }
+    if (nxb == 1)  // X narrower than 128 columns: its upper K block is zero
+        for (int st = 0; st < nst; ++st)
+            for (int pp = 0; pp < npart; ++pp)
+                for (int e = threadIdx.x; e < kBlkBytes / 16; e += blockDim.x)
+                    reinterpret_cast<uint4 *>(sm + st * stage_bytes + (pp * 2 + 1) * kBlkBytes)[e] = make_uint4(0, 0, 0, 0);
+    tc::fence_proxy_async();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nst; ++i) { mbar_init(full + i, 1); mbar_init(empty + i, 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(tfull + i, 1); mbar_init(tempty + i, 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tc::tma_prefetch(&maps.m[mx]);
+        if (npart == 2) tc::tma_prefetch(&maps.m[mxl]);
+    }
+    if (warp == 1) tc::tmem_alloc(tslot, ncols);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tm = *tslot;
 
-    if (stage == 0) {
-        // partials of the two init passes were written to the Q slot (CQ/GQ)
-        // and K slot by the host sequencing: Q pass -> reduce now into CQ/GQ
-        // is done by the caller splitting stage 0 into 0a/0b (see below).
-        return;
-    }
-    if (stage == 3 || stage == 4) {  // 3: reduce init Q pass, 4: reduce init K pass + first B/W
-        float dummy;
-        if (stage == 3) {
-            reduce_into(hs + st.CQ, hs + st.GQ, &dummy, misc + PF_XQ2);
-            return;
+    if (warp == 0 && lane == 0) {
+        const uint64_t pol = l2_policy_evict_first();
+        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+            const int st = i % nst;
+            mbar_wait(empty + st, ((i / nst) & 1) ^ 1);
+            uint8_t *base = sm + st * stage_bytes;
+            mbar_expect_tx(full + st, npart * nxb * kBlkBytes);
+            for (int pp = 0; pp < npart; ++pp)
+                for (int b = 0; b < nxb; ++b)
+                    tc::tma_load_3d(base + (pp * 2 + b) * kBlkBytes, &maps.m[pp ? mxl : mx], b * 64, t * kTile, xh,
+                                    full + st, pol);
         }
-        reduce_into(hs + st.CK, hs + st.GK, &dummy, misc + PF_XK2);
-        if (P.want_objective && tid == 0) misc[PF_SWEEP] = 0.f;
-        // B factors start at zero (prefill.py:137-139) for the initial objective
-        for (int e = tid; e < rs * ds; e += nt) { BQ[e] = 0.f; BK[e] = 0.f; }
-        __syncthreads();
-        if (P.want_objective) {
-            const float obj = objective();
-            if (tid == 0) P.objective[(size_t)h * (P.max_iter + 1)] = obj;
+    } else if (warp == 1 && lane == 0) {
+        const uint32_t id = tc::idesc_bf16(128, N, false, false);
+        const uint32_t wb = smem_u32(sW);
+        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+            const int st = i % nst, ab = i & 1;
+            mbar_wait(tempty + ab, ((i >> 1) & 1) ^ 1);
+            mbar_wait(full + st, (i / nst) & 1);
+            tc::fence_after();
+            const uint32_t base = smem_u32(sm + st * stage_bytes);
+            for (int pp = 0; pp < npart; ++pp)
+#pragma unroll
+                for (int k = 0; k < kTile / 16; ++k) {
+                    const uint32_t koff = (k >> 2) * kBlkBytes + (k & 3) * 32;
+                    const uint64_t ad = tc::desc_sw128(base + pp * 2 * kBlkBytes + koff, 16, 1024);
+                    const uint64_t bd = tc::desc_sw128(wb + (k >> 2) * N * 128 + (k & 3) * 32, 16, 1024);
+                    tc::mma_bf16(tm + ab * (ncols / 2), ad, bd, id, (pp > 0 || k > 0) ? 1u : 0u);
+                }
+            tc::mma_commit(empty + st);
+            tc::mma_commit(tfull + ab);
         }
-        // first sweep: B_Q, B_K from the init factors, then W_K
-        if (!solve_B(hs + st.GQ, hs + st.CQ, BQ)) return fail();
-        if (!solve_B(hs + st.GK, hs + st.CK, BK)) return fail();
-        for (int e = tid; e < rs * ds; e += nt) { hs[st.BQp + e] = 0.f; hs[st.BKp + e] = 0.f; }
-        __syncthreads();
-        if (!solve_W(hs + st.GQ, hs + st.CQ, BK, lk, hs + st.W)) return fail();
-        return;
+    } else if (warp >= 2) {
+        // ---- epilogue: rows of this warp's TMEM lane quarter -----------------
+        const int q4 = warp & 3, row = q4 * 32 + lane;
+        float *Aout = kside ? A_K : A_Q;
+        for (int t = t0, i = 0; t < t1; ++t, ++i) {
+            const int ab = i & 1;
+            mbar_wait(tfull + ab, (i >> 1) & 1);
+            tc::fence_after();
+            const uint32_t ta = tm + ab * (ncols / 2) + ((uint32_t)(q4 * 32) << 16);
+            const int grow = t * kTile + row;
+            for (int j = 0; j < nh; ++j) {
+                float *dst = Aout + ((size_t)(h0 + j) * G.l + grow) * RS;
+                if (RS >= 32) {
+                    for (int c0 = 0; c0 < RS; c0 += 32) {
+                        float hi[32], lo[32];
+                        tc::tmem_ld32(ta + j * 2 * RS + c0, hi);
+                        tc::tmem_ld32(ta + j * 2 * RS + RS + c0, lo);
+                        if (grow < G.l)
+#pragma unroll
+                            for (int p = 0; p < 32; p += 4)
+                                *reinterpret_cast<float4 *>(dst + c0 + p) =
+                                    make_float4(hi[p] + lo[p], hi[p + 1] + lo[p + 1], hi[p + 2] + lo[p + 2], hi[p + 3] + lo[p + 3]);
+                    }
+                } else if (RS == 16) {  // one head = [hi 16 | lo 16]
+                    float v[32];
+                    tc::tmem_ld32(ta + j * 32, v);
+                    if (grow < G.l)
+#pragma unroll
+                        for (int p = 0; p < 16; p += 4)
+                            *reinterpret_cast<float4 *>(dst + p) =
+                                make_float4(v[p] + v[16 + p], v[p + 1] + v[17 + p], v[p + 2] + v[18 + p], v[p + 3] + v[19 + p]);
+                } else {  // RS == 8: one head = [hi 8 | lo 8]
+                    float v[16];
+                    tc::tmem_ld16(ta + j * 16, v);
+                    if (grow < G.l)
+#pragma unroll
+                        for (int p = 0; p < 8; p += 4)
+                            *reinterpret_cast<float4 *>(dst + p) =
+                                make_float4(v[p] + v[8 + p], v[p + 1] + v[9 + p], v[p + 2] + v[10 + p], v[p + 3] + v[11 + p]);
+                }
+            }
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + ab);
+        }
     }
-    if (stage == 1) {
-        // after the K pass: new C_K, G_AK; W_Q for the Q pass
-        reduce_into(hs + st.CK, hs + st.GK, misc + PF_DAK, nullptr);
-        if (!solve_W(hs + st.GK, hs + st.CK, BQ, lq, hs + st.W)) return fail();
-        return;
-    }
-    // stage 2: after the Q pass -> objective, convergence, next sweep's B and W_K
-    reduce_into(hs + st.CQ, hs + st.GQ, misc + PF_DAQ, nullptr);
-    // non-finite factors (prefill.py:216-218)
-    __shared__ int s_bad;
-    if (tid == 0) s_bad = 0;
+    tc::fence_before();
     __syncthreads();
-    for (int e = tid; e < ds * rs; e += nt)
-        if (!isfinite(hs[st.CQ + e]) || !isfinite(hs[st.CK + e])) s_bad = 1;
-    if (tid == 0 && !(isfinite(misc[PF_DAQ]) && isfinite(misc[PF_DAK]))) s_bad = 1;
-    __syncthreads();
-    if (s_bad) {
-        if (tid == 0) { set_status(P.status, LRQK_ST_NONFINITE); misc[PF_ACTIVE] = 0.f; }
-        return;
-    }
-    if (P.want_objective) {
-        const float obj = objective();
-        if (tid == 0) P.objective[(size_t)h * (P.max_iter + 1) + sweep + 1] = obj;
-    }
-    // _factor_delta (prefill.py:184-194)
-    __shared__ float s_db[2];
-    if (tid < 64) {
-        const int side = tid >> 5, lane = tid & 31;
-        const float *Bn = side ? BK : BQ;
-        const float *Bo = hs + (side ? st.BKp : st.BQp);
-        float acc = 0.f;
-        for (int e = lane; e < rs * ds; e += 32) { const float df = Bn[e] - Bo[e]; acc = fmaf(df, df, acc); }
-        acc = warp_sum(acc);
-        if (lane == 0) s_db[side] = acc;
-    }
-    __syncthreads();
-    const double lr = (double)D.l * r, rd = (double)r * d;
-    const double delta = ((double)misc[PF_DAQ] / lr + (double)misc[PF_DAK] / lr + (double)s_db[0] / rd +
-                          (double)s_db[1] / rd) / 4.0;
-    const bool conv = delta <= (double)P.tol;
-    const bool last = conv || (sweep + 1 >= P.max_iter);
-    if (tid == 0) {
-        P.sweeps[h] = sweep + 1;
-        P.converged[h] = conv ? 1 : 0;
-    }
-    __syncthreads();
-    if (last) {
-        if (tid == 0) misc[PF_ACTIVE] = 0.f;
-        return;
-    }
-    // next sweep: B from the new A's (start of sweep s+1), keep the old B's
-    for (int e = tid; e < rs * ds; e += nt) { hs[st.BQp + e] = BQ[e]; hs[st.BKp + e] = BK[e]; }
-    __syncthreads();
-    if (!solve_B(hs + st.GQ, hs + st.CQ, BQ)) return fail();
-    if (!solve_B(hs + st.GK, hs + st.CK, BK)) return fail();
-    if (!solve_W(hs + st.GQ, hs + st.CQ, BK, lk, hs + st.W)) return fail();
+    if (warp == 1) tc::tmem_dealloc(tm, ncols);
 }
 
-__global__ void pf_init_kernel(const PfDims D, lrqk_prefill_t P) {
-    const int h = blockIdx.x * blockDim.x + threadIdx.x;
-    if (h >= D.H) return;
-    const PfState st = pf_state(D);
-    float *misc = P.scratch + (size_t)h * D.head_sz + st.misc;
-    for (int i = 0; i < kPfMisc; ++i) misc[i] = 0.f;
-    misc[PF_ACTIVE] = 1.f;
-    P.sweeps[h] = 0;
-    P.converged[h] = 0;
-    if (P.objective)
-        for (int i = 0; i <= P.max_iter; ++i) P.objective[(size_t)h * (P.max_iter + 1) + i] = __int_as_float(0x7fc00000);
+// ---------------------------------------------------------------------------
+// bf16 operand preparation: X (fp32 split hi/lo, or bf16 widened to 64
+// columns) and Y = [A0 hi | A0 lo | 0] (width YW)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void pf_split_kernel(const T *__restrict__ X, int rows, int cols, int ld, int ow,
+                                __nv_bfloat16 *__restrict__ hi, __nv_bfloat16 *__restrict__ lo) {
+    const long long n = (long long)rows * ow;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const long long rI = e / ow;
+        const int c = (int)(e % ow);
+        const float v = c < cols ? to_float<T>(X[rI * ld + c]) : 0.f;
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        hi[e] = h;
+        if (lo) lo[e] = __float2bfloat16_rn(v - __bfloat162float(h));
+    }
 }
 
-static PfDims pf_dims(const lrqk_prefill_t &P, int nsm) {
-    PfDims D;
-    D.H = P.n_heads;
-    D.group = P.group > 0 ? P.group : 1;
-    D.l = P.len;
-    D.d = P.head_dim;
-    D.ds = P.dim_stride;
-    D.r = P.rank;
-    D.rs = P.rank_stride;
-    const int nchunks = (P.len + kPfRows - 1) / kPfRows;
-    int nb = (2 * nsm + D.H - 1) / D.H;  // about two waves over all heads
-    nb = nb < 1 ? 1 : nb;
-    D.NB = nb < nchunks ? nb : nchunks;
-    if (D.NB < 1) D.NB = 1;
-    D.psz = (size_t)D.ds * D.rs + (size_t)D.rs * D.rs + 2;
-    D.head_sz = (size_t)D.NB * D.psz + 5 * (size_t)D.ds * D.rs + 2 * (size_t)D.rs * D.rs + kPfMisc;
-    D.head_sz = (D.head_sz + 3) & ~(size_t)3;
-    return D;
+__global__ void pf_ysplit_kernel(const float *__restrict__ A, int rows, int r, int RS, int YW, __nv_bfloat16 *__restrict__ Y) {
+    const long long n = (long long)rows * YW;
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const long long rI = e / YW;
+        const int c = (int)(e % YW);
+        float v = 0.f;
+        if (c < 2 * RS && c % RS < r) {
+            const float a = A[rI * RS + c % RS];
+            const __nv_bfloat16 h = __float2bfloat16_rn(a);
+            v = c < RS ? __bfloat162float(h) : a - __bfloat162float(h);
+        }
+        Y[e] = __float2bfloat16_rn(v);
+    }
 }
 
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
 extern int num_sms();
 
-static bool pf_mma_enabled() {
-    static const bool on = [] { const char *e = getenv("LRQK_PREFILL_MMA"); return !(e && e[0] == '0'); }();
-    return on;
+static int pick_slabs(int units, int tiles, int nsm) {
+    // the smallest slab count whose last wave of one-block-per-SM is >= 85 % full
+    int best = 1;
+    double best_eff = -1.0;
+    for (int w = 1; w <= 16; ++w) {
+        int s = (w * nsm + units - 1) / units;
+        s = std::max(1, std::min(s, tiles));
+        const long long blocks = (long long)units * s;
+        const long long waves = (blocks + nsm - 1) / nsm;
+        const double eff = (double)blocks / (double)(waves * nsm);
+        if (eff > best_eff + 1e-9) { best_eff = eff; best = s; }
+        if (eff >= 0.85 || s == tiles) break;
+    }
+    return best;
+}
+
+static size_t al(size_t x) { return (x + 1023) & ~(size_t)1023; }
+
+static bool pf_geom(const lrqk_prefill_t &P, PfGeom &G) {
+    G.H = P.n_heads;
+    G.group = P.group > 0 ? P.group : 1;
+    G.Hk = G.H / G.group;
+    G.l = P.len;
+    G.d = P.head_dim;
+    G.ds = P.dim_stride;
+    G.r = P.rank;
+    G.rs = P.rank_stride;
+    if (G.ds > 128 || G.ds < 8 || G.ds % 8 || G.rs > 64 || G.rs < 8 || (G.rs & (G.rs - 1)) || G.r > G.d || G.r > G.rs || G.d > G.ds)
+        return false;
+    G.parts = P.dtype == LRQK_BF16 ? 1 : 2;
+    G.direct = P.dtype == LRQK_BF16 && (G.ds == 64 || G.ds == 128);
+    G.XW = G.ds > 64 ? 128 : 64;
+    G.YW = 2 * G.rs > 64 ? 128 : 64;
+    G.shared = P.A_Q0 && P.init_shared ? 1 : 0;
+    G.NY = G.shared ? 1 : G.H;
+    G.NQU = G.H;
+    G.NKU = G.shared ? G.Hk : G.H;
+    G.NU = (G.NQU + G.NKU) * G.parts + 2 * G.NY;
+    G.tiles = (G.l + kTile - 1) / kTile;
+    const int nsm = num_sms();
+    G.S = pick_slabs(G.NU, G.tiles, nsm);
+    G.PW = 128 + (G.parts == 2 ? G.XW + G.YW : G.YW);
+    G.HPU = std::max(1, std::min(G.group, 256 / (2 * G.rs)));
+    G.nsub = (G.group + G.HPU - 1) / G.HPU;
+    G.NMU = G.H + G.Hk * G.nsub;
+    G.Nmax = std::max(2 * G.rs, G.HPU * 2 * G.rs);
+    G.S2 = pick_slabs(G.NMU, G.tiles, nsm);
+    size_t o = 0;
+    const size_t xq = (size_t)G.H * G.l * G.XW * 2, xk = (size_t)G.Hk * G.l * G.XW * 2;
+    const bool own_x = !G.direct;
+    for (int i = 0; i < 4; ++i) G.off_x[i] = 0;
+    if (own_x) {
+        G.off_x[0] = o; o = al(o + xq);
+        G.off_x[2] = o; o = al(o + xk);
+        if (G.parts == 2) {
+            G.off_x[1] = o; o = al(o + xq);
+            G.off_x[3] = o; o = al(o + xk);
+        }
+    }
+    const size_t ysz = (size_t)G.NY * G.l * G.YW * 2;
+    G.off_y[0] = o; o = al(o + ysz);
+    G.off_y[1] = o; o = al(o + ysz);
+    G.off_part = o; o = al(o + (size_t)G.NU * G.S * kTile * G.PW * 4);
+    G.off_gq = o; o = al(o + (size_t)G.NQU * kTile * kTile * 8);
+    G.off_cq = o; o = al(o + (size_t)G.NQU * kTile * G.rs * 8);
+    G.off_gk = o; o = al(o + (size_t)G.NKU * kTile * kTile * 8);
+    G.off_ck = o; o = al(o + (size_t)G.NKU * kTile * G.rs * 8);
+    G.off_g0q = o; o = al(o + (size_t)G.NY * G.rs * G.rs * 8);
+    G.off_g0k = o; o = al(o + (size_t)G.NY * G.rs * G.rs * 8);
+    G.off_w = o; o = al(o + (size_t)2 * G.H * kTile * G.rs * 4);
+    G.off_work = o; o = al(o + (size_t)G.H * kWorkMats * kTile * G.rs * 8);
+    G.total = o + 1024;
+    return true;
 }
 
 size_t prefill_scratch_floats(const lrqk_prefill_t &P) {
-    PfDims D = pf_dims(P, num_sms());
-    return (size_t)D.H * D.head_sz + (P.want_objective ? (size_t)(D.H + D.H / D.group) * D.ds * D.ds : 0);
+    PfGeom G;
+    if (!pf_geom(P, G)) return 0;
+    return (G.total + 3) / 4;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// [heads][rows][width] bf16, boxes of 64 columns x 128 rows, SW128
+static bool make_map(CUtensorMap *m, const void *base, int heads, int rows, int width) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)width, (cuuint64_t)rows, (cuuint64_t)heads};
+    const cuuint64_t strides[2] = {(cuuint64_t)width * 2, (cuuint64_t)rows * width * 2};
+    const cuuint32_t box[3] = {64, (cuuint32_t)kTile, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
-    if (P.rank_stride % 4 || P.dim_stride % 4 || P.rank > P.head_dim || P.rank_stride > 64 || P.dim_stride > 256)
-        return LRQK_EUNSUPPORTED;
-    const PfDims D = pf_dims(P, num_sms());
-    pf_init_kernel<<<(D.H + 127) / 128, 128, 0, st>>>(D, P);
-    const size_t pass_smem = ((size_t)kPfRows * (D.ds + 4) + (size_t)kPfRows * (D.rs + 4) + (size_t)D.ds * D.rs +
-                              (size_t)kPfThreads * 16 + 64) * sizeof(float);
-    const size_t solve_smem = (2 * (size_t)D.rs * (D.rs + 1) + (size_t)D.rs * D.ds + 64) * sizeof(float);
-    dim3 pgrid(D.NB, D.H);
-    const bool bf = P.dtype == LRQK_BF16;
-    const bool mma = bf && D.ds == kPfD && (D.rs == 16 || D.rs == 32 || D.rs == 64) && pf_mma_enabled();
-    auto pass = [&](const void *X, int is_k, float *A, int update, int want_x2) {
-        if (mma) {
-            const __nv_bfloat16 *Xb = reinterpret_cast<const __nv_bfloat16 *>(X);
-#define LRQK_PF_MMA(RSV)                                                                             \
-    do {                                                                                             \
-        auto fn = pf_pass_mma_kernel<RSV>;                                                           \
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pf_mma_smem<RSV>()); \
-        fn<<<pgrid, kPfThreads, pf_mma_smem<RSV>(), st>>>(D, Xb, is_k, A, A, update, want_x2, P.scratch); \
-    } while (0)
-            if (D.rs == 16) LRQK_PF_MMA(16);
-            else if (D.rs == 32) LRQK_PF_MMA(32);
-            else LRQK_PF_MMA(64);
-#undef LRQK_PF_MMA
-        } else if (bf) {
-            auto fn = pf_pass_kernel<__nv_bfloat16>;
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem);
-            fn<<<pgrid, kPfThreads, pass_smem, st>>>(D, reinterpret_cast<const __nv_bfloat16 *>(X), is_k, A, A,
-                                                    update, want_x2, P.scratch);
-        } else {
-            auto fn = pf_pass_kernel<float>;
-            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem);
-            fn<<<pgrid, kPfThreads, pass_smem, st>>>(D, reinterpret_cast<const float *>(X), is_k, A, A, update,
-                                                    want_x2, P.scratch);
-        }
-    };
-    cudaFuncSetAttribute(pf_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)solve_smem);
-    if (P.want_objective) {
-        float *gbase = P.scratch + (size_t)D.H * D.head_sz;
-        float *gq = gbase, *gk = gbase + (size_t)D.H * D.ds * D.ds;
-        const int nk = D.H / D.group;
-        if (bf) {
-            pf_gram_dd_kernel<__nv_bfloat16><<<dim3(D.ds, D.H), 128, 0, st>>>(D, reinterpret_cast<const __nv_bfloat16 *>(P.Q), D.H, gq);
-            pf_gram_dd_kernel<__nv_bfloat16><<<dim3(D.ds, nk), 128, 0, st>>>(D, reinterpret_cast<const __nv_bfloat16 *>(P.K), nk, gk);
-        } else {
-            pf_gram_dd_kernel<float><<<dim3(D.ds, D.H), 128, 0, st>>>(D, reinterpret_cast<const float *>(P.Q), D.H, gq);
-            pf_gram_dd_kernel<float><<<dim3(D.ds, nk), 128, 0, st>>>(D, reinterpret_cast<const float *>(P.K), nk, gk);
-        }
-        pf_qk2_kernel<<<D.H, 256, 0, st>>>(D, gq, gk, P.scratch);
+    PfGeom G;
+    if (!pf_geom(P, G)) return LRQK_EUNSUPPORTED;
+    uint8_t *scr = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(P.scratch) + 1023) & ~(uintptr_t)1023);
+    // ---- operands ----------------------------------------------------------
+    const int Hk = G.Hk;
+    const void *xq = P.Q, *xk = P.K, *xql = nullptr, *xkl = nullptr;
+    if (!G.direct) {
+        auto split = [&](const void *X, int heads, uint8_t *hi, uint8_t *lo) {
+            const long long n = (long long)heads * G.l * G.XW;
+            const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+            if (P.dtype == LRQK_BF16)
+                pf_split_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16 *>(X),
+                                                                      heads * G.l, G.d, G.ds, G.XW,
+                                                                      reinterpret_cast<__nv_bfloat16 *>(hi), nullptr);
+            else
+                pf_split_kernel<float><<<grid, 256, 0, st>>>(reinterpret_cast<const float *>(X), heads * G.l, G.d,
+                                                              G.ds, G.XW, reinterpret_cast<__nv_bfloat16 *>(hi),
+                                                              reinterpret_cast<__nv_bfloat16 *>(lo));
+        };
+        split(P.Q, G.H, scr + G.off_x[0], G.parts == 2 ? scr + G.off_x[1] : nullptr);
+        split(P.K, Hk, scr + G.off_x[2], G.parts == 2 ? scr + G.off_x[3] : nullptr);
+        xq = scr + G.off_x[0];
+        xk = scr + G.off_x[2];
+        xql = G.parts == 2 ? scr + G.off_x[1] : nullptr;
+        xkl = G.parts == 2 ? scr + G.off_x[3] : nullptr;
     }
-    // init passes: reductions of the initial A's
-    pass(P.Q, 0, P.A_Q, 0, 1);
-    pf_solve_kernel<<<D.H, kPfThreads, solve_smem, st>>>(D, P, 3, 0);
-    pass(P.K, 1, P.A_K, 0, 1);
-    pf_solve_kernel<<<D.H, kPfThreads, solve_smem, st>>>(D, P, 4, 0);
-    for (int s = 0; s < P.max_iter; ++s) {
-        pass(P.K, 1, P.A_K, 1, 0);
-        pf_solve_kernel<<<D.H, kPfThreads, solve_smem, st>>>(D, P, 1, s);
-        pass(P.Q, 0, P.A_Q, 1, 0);
-        pf_solve_kernel<<<D.H, kPfThreads, solve_smem, st>>>(D, P, 2, s);
+    const float *a0q = P.A_Q0 ? P.A_Q0 : P.A_Q, *a0k = P.A_K0 ? P.A_K0 : P.A_K;
+    {
+        const long long n = (long long)G.NY * G.l * G.YW;
+        const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+        pf_ysplit_kernel<<<grid, 256, 0, st>>>(a0q, G.NY * G.l, G.r, G.rs, G.YW,
+                                               reinterpret_cast<__nv_bfloat16 *>(scr + G.off_y[0]));
+        pf_ysplit_kernel<<<grid, 256, 0, st>>>(a0k, G.NY * G.l, G.r, G.rs, G.YW,
+                                               reinterpret_cast<__nv_bfloat16 *>(scr + G.off_y[1]));
     }
+    PfMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    bool ok = make_map(&maps.m[MQ], xq, G.H, G.l, G.XW) && make_map(&maps.m[MK], xk, Hk, G.l, G.XW) &&
+              make_map(&maps.m[MYQ], scr + G.off_y[0], G.NY, G.l, G.YW) &&
+              make_map(&maps.m[MYK], scr + G.off_y[1], G.NY, G.l, G.YW);
+    if (G.parts == 2)
+        ok = ok && make_map(&maps.m[MQL], xql, G.H, G.l, G.XW) && make_map(&maps.m[MKL], xkl, Hk, G.l, G.XW);
+    if (!ok) return LRQK_ECUDA;
+    // ---- K1g -----------------------------------------------------------------
+    const size_t gsm = kSmemBudget + 3072;
+    cudaFuncSetAttribute(pf_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+    float *part = reinterpret_cast<float *>(scr + G.off_part);
+    pf_gram_kernel<<<G.NU * G.S, kGramThreads, gsm, st>>>(maps, G, part);
+    // ---- K1c -----------------------------------------------------------------
+    {
+        const long long tot = (long long)(G.NQU + G.NKU) * kTile * (kTile + G.rs) + 2LL * G.NY * G.rs * G.rs;
+        const int grid = (int)std::min<long long>((tot + 255) / 256, 148LL * 8);
+        pf_combine_kernel<<<grid, 256, 0, st>>>(G, part, scr);
+    }
+    // ---- K1s -----------------------------------------------------------------
+    const size_t ssm = (5 * (size_t)G.r * G.r + 64) * sizeof(double);
+    cudaFuncSetAttribute(pf_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    pf_solve_kernel<<<G.H, kSolveThreads, ssm, st>>>(G, P, scr);
+    // ---- K1m -----------------------------------------------------------------
+    const size_t msm = kSmemBudget + 3072;
+    cudaFuncSetAttribute(pf_mat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+    pf_mat_kernel<<<G.NMU * G.S2, kMatThreads, msm, st>>>(maps, G, reinterpret_cast<const float *>(scr + G.off_w),
+                                                          P.A_Q, P.A_K);
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 

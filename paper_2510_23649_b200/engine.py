@@ -345,18 +345,25 @@ def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter
     group = group or (H // K.shape[0])
     ds, rs = pow2_at_least(d), pow2_at_least(rank)
     sdt = torch_dtype(dtype)
-    Qp = pad_last(Q.to(sdt), ds).contiguous()
-    Kp = pad_last(K.to(sdt), ds).contiguous()
+    Qp = Q if (Q.dtype == sdt and d == ds and Q.is_contiguous()) else pad_last(Q.to(sdt), ds).contiguous()
+    Kp = K if (K.dtype == sdt and d == ds and K.is_contiguous()) else pad_last(K.to(sdt), ds).contiguous()
     if A_Q0 is None or A_K0 is None:
         aq, ak = randn_init(l, rank, seed)
         A_Q0, A_K0 = aq, ak
+
     def prep(A):
+        # the init stays as given: one [l, r] draw shared by every head (the
+        # reference's randn init) or per-head [H, l, r]; no per-head copies
         A = torch.as_tensor(np.array(A, dtype=np.float32) if isinstance(A, np.ndarray) else A,
                             dtype=torch.float32, device=dev)
-        if A.dim() == 2:
-            A = A.unsqueeze(0).expand(H, l, A.shape[-1])
-        return pad_last(A, rs).contiguous().clone()
-    A_Q, A_K = prep(A_Q0), prep(A_K0)
+        return pad_last(A, rs).contiguous()
+    A0q, A0k = prep(A_Q0), prep(A_K0)
+    shared = A0q.dim() == 2 and A0k.dim() == 2
+    if not shared:
+        A0q = A0q.expand(H, l, rs).contiguous() if A0q.dim() == 2 else A0q
+        A0k = A0k.expand(H, l, rs).contiguous() if A0k.dim() == 2 else A0k
+    A_Q = torch.empty(H, l, rs, dtype=torch.float32, device=dev)
+    A_K = torch.empty(H, l, rs, dtype=torch.float32, device=dev)
     B_Q = torch.zeros(H, rs, ds, dtype=torch.float32, device=dev)
     B_K = torch.zeros(H, rs, ds, dtype=torch.float32, device=dev)
     obj = torch.full((H, max_iter + 1), float("nan"), dtype=torch.float32, device=dev)
@@ -372,7 +379,10 @@ def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter
     P.A_Q, P.A_K, P.B_Q, P.B_K = A_Q.data_ptr(), A_K.data_ptr(), B_Q.data_ptr(), B_K.data_ptr()
     P.objective, P.sweeps, P.converged = obj.data_ptr(), sweeps.data_ptr(), conv.data_ptr()
     P.status = status.data_ptr()
+    P.A_Q0, P.A_K0, P.init_shared = A0q.data_ptr(), A0k.data_ptr(), int(shared)
     nbytes = lib.lrqk_prefill_scratch_bytes(C.byref(P))
+    if nbytes == 0:
+        raise ValueError(f"prefill: unsupported shape (head_dim {d} -> {ds}, rank {rank} -> {rs})")
     scratch = torch.empty(max(16, nbytes // 4 + 16), dtype=torch.float32, device=dev)
     P.scratch = scratch.data_ptr()
     _lib.check(lib.lrqk_prefill_factorize(C.byref(P), _lib.stream_ptr()), "lrqk_prefill_factorize")
