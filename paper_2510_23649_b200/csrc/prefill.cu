@@ -49,10 +49,9 @@ constexpr int kBlkBytes = kTile * 128;     // one 64-column SW128 block of a til
 constexpr int kMaxMapW = 128;              // widest TMA'd tensor (columns)
 constexpr int kGramThreads = 128;
 constexpr int kMatThreads = 192;           // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
-constexpr int kSolveThreads = 256;
+constexpr int kSolveThreads = 1024;
 constexpr int kMaxStages = 6;
 constexpr int kWorkMats = 10;              // float64 d x r work matrices per head (solver)
-constexpr size_t kSmemBudget = 200 * 1024;
 
 enum PfMap { MQ = 0, MQL = 1, MK = 2, MKL = 3, MYQ = 4, MYK = 5, kNumMaps = 6 };
 
@@ -68,7 +67,7 @@ struct PfGeom {
     int shared;  // one A0 for every head (the reference's randn draw)
     int NY;      // Y tensors per side
     int NQU, NKU, NU, S, PW, tiles;
-    int NMU, HPU, nsub, S2, Nmax;  // materialize units, heads per K unit, K sub-units per KV head, slabs, max N
+    int NMU, HPU, nsub, Nmax;  // materialize units, heads per K unit, K sub-units per KV head, max N
     size_t off_x[4], off_y[2], off_part, off_gq, off_cq, off_gk, off_ck, off_g0q, off_g0k, off_w, off_work, total;
 };
 
@@ -105,7 +104,7 @@ __host__ __device__ inline GUnit gram_unit(const PfGeom &G, int u) {
 // K1g: D1 = X^T X, D2 = X^T Y over one slab of rows of one unit
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kGramThreads, 1)
-pf_gram_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, float *__restrict__ part) {
+pf_gram_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, float *__restrict__ part, int budget) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int u = blockIdx.x / G.S, s = blockIdx.x % G.S;
@@ -113,7 +112,8 @@ pf_gram_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, float *__res
     const int xw = map_width(G, U.xm), w1 = map_width(G, U.y1m), w2 = map_width(G, U.y2m);
     const int nxb = xw / 64, nyb = (w1 + w2) / 64, ny = w1 + w2;
     const int stage_bytes = (2 + nyb) * kBlkBytes;
-    const int nst = min(kMaxStages, (int)(kSmemBudget / stage_bytes));
+    const int nst = min(kMaxStages, budget / stage_bytes);
+    const uint32_t ncols = 128 + ny <= 256 ? 256 : 512;  // D1 | D2 (two CTAs per SM fit at 256)
     uint64_t *full = reinterpret_cast<uint64_t *>(sm + nst * stage_bytes);
     uint64_t *empty = full + kMaxStages;
     uint64_t *done = empty + kMaxStages;
@@ -135,7 +135,7 @@ pf_gram_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, float *__res
         if (U.y1m >= 0) tc::tma_prefetch(&maps.m[U.y1m]);
         if (U.y2m >= 0) tc::tma_prefetch(&maps.m[U.y2m]);
     }
-    if (warp == 2) tc::tmem_alloc(tslot, 512);
+    if (warp == 2) tc::tmem_alloc(tslot, ncols);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -196,7 +196,7 @@ pf_gram_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, float *__res
     }
     tc::fence_before();
     __syncthreads();
-    if (warp == 2) tc::tmem_dealloc(tm, 512);
+    if (warp == 2) tc::tmem_dealloc(tm, ncols);
 }
 
 // ---------------------------------------------------------------------------
@@ -227,9 +227,11 @@ __global__ void pf_combine_kernel(const PfGeom G, const float *__restrict__ part
                 const int a = min(i, j), b = max(i, j);  // gram is exactly symmetric (linalg.py:53-54)
                 const int u = ubase + h * G.parts;
                 double s = slab_sum(G, part, u, a, b);
-                if (G.parts == 2)
-                    s += slab_sum(G, part, u, a, 128 + b) + slab_sum(G, part, u, b, 128 + a) +
-                         slab_sum(G, part, u + 1, a, b);
+                if (G.parts == 2) {
+                    // hi^T lo occupies D2 columns [0, XW) only; X is zero past XW
+                    if (b < G.XW) s += slab_sum(G, part, u, a, 128 + b) + slab_sum(G, part, u, b, 128 + a);
+                    s += slab_sum(G, part, u + 1, a, b);
+                }
                 gx[(size_t)h * nG + ij] = s;
             } else {
                 v -= nunits * nG;
@@ -259,83 +261,122 @@ __global__ void pf_combine_kernel(const PfGeom G, const float *__restrict__ part
 // ---------------------------------------------------------------------------
 // K1s: the reference sweep in d-space, float64, one block per query head
 // ---------------------------------------------------------------------------
-struct SolveSmem {
-    double *GAQ, *GAK, *L, *Li;  // r x r (stride r)
-    double *red;                 // 64
-    int *flag;
-};
-
-LRQK_DEV double block_sum_d(double v, double *red) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+// Block-wide product out(i, j) = sum_k a(i, k) b(k, j) with compile-time
+// shapes: 2 x 2 register tiles; when there are fewer tiles than threads, KS
+// adjacent lanes split the k range and combine with shuffles (fixed order).
+template <int M, int N, int K, class FA, class FB, class FO>
+LRQK_DEV void tile_mm(FA a, FB b, FO o) {
+    static_assert(M % 2 == 0 && N % 2 == 0, "even shapes");
+    constexpr int TN = N / 2, NTILE = (M / 2) * TN;
+    constexpr int KS = NTILE >= kSolveThreads ? 1 : (NTILE * 2 >= kSolveThreads ? 2 : (NTILE * 4 >= kSolveThreads ? 4 : 8));
+    constexpr int TOTAL = NTILE * KS;
+    static_assert(TOTAL % 32 == 0, "whole warps");
+#pragma unroll 1
+    for (int t = threadIdx.x; t < TOTAL; t += kSolveThreads) {
+        const int tile = t / KS, sl = t % KS;
+        const int i0 = (tile / TN) * 2, j0 = (tile % TN) * 2;
+        double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
+#pragma unroll 8
+        for (int k = sl; k < K; k += KS) {
+            const double x0 = a(i0, k), x1 = a(i0 + 1, k), y0 = b(k, j0), y1 = b(k, j0 + 1);
+            a00 = fma(x0, y0, a00);
+            a01 = fma(x0, y1, a01);
+            a10 = fma(x1, y0, a10);
+            a11 = fma(x1, y1, a11);
+        }
+#pragma unroll
+        for (int off = 1; off < KS; off <<= 1) {
+            a00 += __shfl_xor_sync(0xffffffffu, a00, off);
+            a01 += __shfl_xor_sync(0xffffffffu, a01, off);
+            a10 += __shfl_xor_sync(0xffffffffu, a10, off);
+            a11 += __shfl_xor_sync(0xffffffffu, a11, off);
+        }
+        if (sl == 0) {
+            o(i0, j0, a00);
+            o(i0, j0 + 1, a01);
+            o(i0 + 1, j0, a10);
+            o(i0 + 1, j0 + 1, a11);
+        }
+    }
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];  // fixed order
-    __syncthreads();
-    return t;
 }
 
-// M^-1 (r x r, stride r) into Li through Cholesky (L, lower) with the
-// reference's single jitter retry M + 1e-10 (tr(M)/r + 1) I
-// (linalg.py:80-91).  Returns 0 ok, 1 jittered, 2 failed, 3 non-finite M.
-__device__ int chol_inverse(const double *M, int r, double *L, double *Li, double *red) {
-    double bad = 0.0;
-    for (int e = threadIdx.x; e < r * r; e += blockDim.x) bad += isfinite(M[e]) ? 0.0 : 1.0;
-    if (block_sum_d(bad, red) != 0.0) return 3;
-    double tr = 0.0;
-    for (int i = threadIdx.x; i < r; i += blockDim.x) tr += M[i * r + i];
-    tr = block_sum_d(tr, red);
-    __shared__ int s_fail;
+// block sum of NV values at once (fixed order: deterministic)
+template <int NV>
+LRQK_DEV void block_sums(double (&v)[NV], double *red) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+    constexpr int nw = kSolveThreads / 32;
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) red[j * 32 + (threadIdx.x >> 5)] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < nw; ++w) t += red[j * 32 + w];
+        v[j] = t;
+    }
+    __syncthreads();
+}
+
+// In-place inverse of the SPD matrix M (R x R, rank r, identity-padded past r)
+// by Gauss-Jordan without pivoting, one barrier per pivot.  On an SPD matrix
+// every pivot is positive exactly when the reference's Cholesky succeeds (the
+// pivots are the squared Cholesky diagonal), so a non-positive pivot is the
+// LinAlgError of linalg.py:81 and triggers the same single retry with
+// M + 1e-10 (tr(M)/r + 1) I (linalg.py:84-91).
+// Returns 0 ok, 1 jittered, 2 failed, 3 non-finite M.
+template <int R>
+__device__ int spd_inverse_f64(double *M, int r, double *W, double *rc, double *red) {
+    double s2[2] = {0.0, 0.0};
+    for (int e = threadIdx.x; e < R * R; e += kSolveThreads) {
+        const int i = e / R, j = e % R;
+        s2[0] += isfinite(M[e]) ? 0.0 : 1.0;
+        if (i == j && i < r) s2[1] += M[e];
+    }
+    block_sums<2>(s2, red);
+    if (s2[0] != 0.0) return 3;
+    const double tr = s2[1];
     for (int attempt = 0; attempt < 2; ++attempt) {
         const double jit = attempt ? 1e-10 * (tr / r + 1.0) : 0.0;
-        for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-            const int i = e / r, j = e % r;
-            L[e] = i >= j ? M[e] + (i == j ? jit : 0.0) : 0.0;
-        }
-        if (threadIdx.x == 0) s_fail = 0;
-        __syncthreads();
-        for (int k = 0; k < r; ++k) {
-            const double pk = L[k * r + k];
-            if (!(pk > 0.0)) { if (threadIdx.x == 0) s_fail = 1; break; }  // uniform: all read pk
-            const double lkk = sqrt(pk);
-            __syncthreads();
-            if (threadIdx.x == 0) L[k * r + k] = lkk;
-            for (int i = k + 1 + threadIdx.x; i < r; i += blockDim.x) L[i * r + k] /= lkk;
-            __syncthreads();
-            const int m = r - k - 1;
-            for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-                const int i = k + 1 + e / m, j = k + 1 + e % m;
-                if (j <= i) L[i * r + j] -= L[i * r + k] * L[j * r + k];
-            }
-            __syncthreads();
+        __syncthreads();  // a failed attempt's last pivot reads are done before rc is refilled
+        for (int e = threadIdx.x; e < R * R; e += kSolveThreads) {
+            const int i = e / R, j = e % R;
+            const double v = (i < r && j < r) ? M[e] + (i == j ? jit : 0.0) : (i == j ? 1.0 : 0.0);
+            W[e] = v;
+            if (i == 0) rc[j] = v;  // pivot row / column of step 0
+            if (j == 0) rc[64 + i] = v;
         }
         __syncthreads();
-        if (!s_fail) {
-            // Li = L^-1 (lower), one column per thread
-            for (int c = threadIdx.x; c < r; c += blockDim.x) {
-                for (int i = 0; i < r; ++i) {
-                    double v;
-                    if (i < c) v = 0.0;
-                    else if (i == c) v = 1.0 / L[c * r + c];
-                    else {
-                        double s = 0.0;
-                        for (int k = c; k < i; ++k) s += L[i * r + k] * Li[k * r + c];
-                        v = -s / L[i * r + i];
-                    }
-                    Li[i * r + c] = v;
-                }
+        bool ok = true;
+#pragma unroll 1
+        for (int k = 0; k < R; ++k) {
+            // the pivot row / column of step k were written by their owners
+            // during step k - 1; the next step's go to the other buffer
+            const double *row = rc + (k & 1) * 128, *col = row + 64;
+            double *nrow = rc + ((k + 1) & 1) * 128, *ncol = nrow + 64;
+            const double p = row[k];
+            if (!(p > 0.0)) { ok = false; break; }  // block-uniform
+            const double ip = 1.0 / p;
+            for (int e = threadIdx.x; e < R * R; e += kSolveThreads) {
+                const int i = e / R, j = e % R;
+                const double a = W[e];
+                const double f = col[i] * ip;
+                const double v = i == k ? (j == k ? ip : a * ip) : (j == k ? -f : fma(-f, row[j], a));
+                W[e] = v;
+                if (i == k + 1) nrow[j] = v;
+                if (j == k + 1) ncol[i] = v;
             }
             __syncthreads();
-            // M^-1 = L^-T L^-1 into L
-            for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
-                const int p = e / r, q = e % r;
-                double s = 0.0;
-                for (int k = max(p, q); k < r; ++k) s += Li[k * r + p] * Li[k * r + q];
-                L[e] = s;
+        }
+        if (ok) {
+            for (int e = threadIdx.x; e < R * R; e += kSolveThreads) {  // exact symmetry
+                const int i = e / R, j = e % R;
+                M[e] = i <= j ? W[e] : W[j * R + i];
             }
-            __syncthreads();
-            for (int e = threadIdx.x; e < r * r; e += blockDim.x) Li[e] = L[e];
             __syncthreads();
             return attempt;
         }
@@ -343,151 +384,117 @@ __device__ int chol_inverse(const double *M, int r, double *L, double *Li, doubl
     return 2;
 }
 
+// Padded shapes: D = 128 rows of d (zero past d), R = rank_stride columns of
+// r (zero past r); the inverses see the identity past r, so every padded
+// entry stays exactly zero and the true blocks are the reference's algebra.
+template <int R>
 __global__ void __launch_bounds__(kSolveThreads)
 pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
+    constexpr int D = kTile;
     extern __shared__ __align__(16) double sd[];
-    const int h = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
-    const int r = G.r, d = G.d, RS = G.rs, D = kTile;
+    const int h = blockIdx.x, tid = threadIdx.x, nt = kSolveThreads;
+    const int r = G.r, d = G.d;
     const double lq = P.lambda_q, lk = P.lambda_k;
-    double *GAQ = sd, *GAK = GAQ + r * r, *Lm = GAK + r * r, *Li = Lm + r * r, *Mm = Li + r * r, *red = Mm + r * r;
+    double *GAQ = sd, *GAK = GAQ + R * R, *Mm = GAK + R * R, *Wg = Mm + R * R, *BBq = Wg + R * R, *BBk = BBq + R * R;
+    double *rc = BBk + R * R, *red = rc + 256;
     const int ku = G.shared ? h / G.group : h;
     const int yq = G.shared ? 0 : h;
-    const double *GQ = reinterpret_cast<const double *>(scr + G.off_gq) + (size_t)h * D * D;
-    const double *GK = reinterpret_cast<const double *>(scr + G.off_gk) + (size_t)ku * D * D;
-    const double *CQ0 = reinterpret_cast<const double *>(scr + G.off_cq) + (size_t)h * D * RS;
-    const double *CK0 = reinterpret_cast<const double *>(scr + G.off_ck) + (size_t)ku * D * RS;
-    const double *G0Q = reinterpret_cast<const double *>(scr + G.off_g0q) + (size_t)yq * RS * RS;
-    const double *G0K = reinterpret_cast<const double *>(scr + G.off_g0k) + (size_t)yq * RS * RS;
-    // float64 work, d x r (stride r) or r x d (stride d)
-    double *wk = reinterpret_cast<double *>(scr + G.off_work) + (size_t)h * kWorkMats * D * RS;
-    double *Cq = wk, *Ck = Cq + D * RS, *Wq = Ck + D * RS, *Wk = Wq + D * RS, *Wn = Wk + D * RS, *Dt = Wn + D * RS;
-    double *Bq = Dt + D * RS, *Bk = Bq + D * RS, *Boq = Bk + D * RS, *Bok = Boq + D * RS;
+    const double *__restrict__ GQ = reinterpret_cast<const double *>(scr + G.off_gq) + (size_t)h * D * D;
+    const double *__restrict__ GK = reinterpret_cast<const double *>(scr + G.off_gk) + (size_t)ku * D * D;
+    const double *__restrict__ CQ0 = reinterpret_cast<const double *>(scr + G.off_cq) + (size_t)h * D * R;
+    const double *__restrict__ CK0 = reinterpret_cast<const double *>(scr + G.off_ck) + (size_t)ku * D * R;
+    const double *__restrict__ G0Q = reinterpret_cast<const double *>(scr + G.off_g0q) + (size_t)yq * R * R;
+    const double *__restrict__ G0K = reinterpret_cast<const double *>(scr + G.off_g0k) + (size_t)yq * R * R;
+    // float64 work: C, W are D x R; B are R x D
+    double *wk = reinterpret_cast<double *>(scr + G.off_work) + (size_t)h * kWorkMats * D * R;
+    double *Cq = wk, *Ck = Cq + D * R, *Wq = Ck + D * R, *Wk = Wq + D * R, *Wn = Wk + D * R, *Dt = Wn + D * R;
+    double *Bq = Dt + D * R, *Bk = Bq + D * R, *Boq = Bk + D * R, *Bok = Boq + D * R;
     float *Wout = reinterpret_cast<float *>(scr + G.off_w);  // [2][H][128][RS] fp32 (Q then K)
     float *obj = P.objective ? P.objective + (size_t)h * (P.max_iter + 1) : nullptr;
 
-    // Gram-trace constants
-    double qk2 = 0.0, tq = 0.0, tk = 0.0;
-    for (int e = tid; e < d * d; e += nt) {
-        const int i = e / d, j = e % d;
-        qk2 += GQ[i * D + j] * GK[i * D + j];
-        if (i == j) { tq += GQ[i * D + i]; tk += GK[i * D + i]; }
+    // Gram-trace constants <GQ, GK>, tr GQ, tr GK, tr G0Q, tr G0K
+    double c5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int e = tid; e < D * D; e += nt) {
+        c5[0] += GQ[e] * GK[e];
+        if (e / D == e % D) { c5[1] += GQ[e]; c5[2] += GK[e]; }
     }
-    qk2 = block_sum_d(qk2, red);
-    tq = block_sum_d(tq, red);
-    tk = block_sum_d(tk, red);
-    for (int e = tid; e < d * r; e += nt) {
-        const int i = e / r, p = e % r;
-        Cq[e] = CQ0[i * RS + p];
-        Ck[e] = CK0[i * RS + p];
-    }
-    for (int e = tid; e < r * r; e += nt) {
-        const int p = e / r, q = e % r;
-        GAQ[e] = G0Q[p * RS + q];
-        GAK[e] = G0K[p * RS + q];
-    }
-    for (int e = tid; e < r * d; e += nt) { Bq[e] = 0.0; Bk[e] = 0.0; }
-    double trg0q = 0.0, trg0k = 0.0;
-    for (int p = tid; p < r; p += nt) { trg0q += G0Q[p * RS + p]; trg0k += G0K[p * RS + p]; }
-    trg0q = block_sum_d(trg0q, red);
-    trg0k = block_sum_d(trg0k, red);
+    for (int p = tid; p < R; p += nt) { c5[3] += G0Q[p * R + p]; c5[4] += G0K[p * R + p]; }
+    block_sums<5>(c5, red);
+    const double qk2 = c5[0], tq = c5[1], tk = c5[2], trg0q = c5[3], trg0k = c5[4];
+    for (int e = tid; e < D * R; e += nt) { Cq[e] = CQ0[e]; Ck[e] = CK0[e]; Bq[e] = 0.0; Bk[e] = 0.0; }
+    for (int e = tid; e < R * R; e += nt) { GAQ[e] = G0Q[e]; GAK[e] = G0K[e]; BBq[e] = 0.0; BBk[e] = 0.0; }
     __syncthreads();
 
-    // lagrangian_value (prefill.py:142-158) from the Gram-space quantities
+    // lagrangian_value (prefill.py:142-158) from the Gram-space quantities;
+    // BBq = B_Q B_Q^T and BBk = B_K B_K^T are current whenever it runs
     auto objective = [&]() -> double {
-        double cross = 0.0, approx = 0.0, rq = 0.0, rk = 0.0;
-        for (int e = tid; e < d * r; e += nt) {
-            const int i = e / r, p = e % r;
-            cross += Cq[e] * Ck[e];
-            rq -= 2.0 * Bq[p * d + i] * Cq[e];
-            rk -= 2.0 * Bk[p * d + i] * Ck[e];
+        double v4[4] = {0.0, 0.0, 0.0, 0.0};  // cross, approx, q-resid, k-resid
+        for (int e = tid; e < D * R; e += nt) {
+            const int i = e / R, p = e % R;
+            v4[0] += Cq[e] * Ck[e];
+            v4[2] -= 2.0 * Bq[p * D + i] * Cq[e];
+            v4[3] -= 2.0 * Bk[p * D + i] * Ck[e];
         }
-        for (int e = tid; e < r * r; e += nt) {
-            const int p = e / r, q = e % r;
-            approx += GAQ[e] * GAK[e];
-            double bbq = 0.0, bbk = 0.0;
-            for (int i = 0; i < d; ++i) { bbq += Bq[p * d + i] * Bq[q * d + i]; bbk += Bk[p * d + i] * Bk[q * d + i]; }
-            rq += GAQ[e] * bbq;
-            rk += GAK[e] * bbk;
+        for (int e = tid; e < R * R; e += nt) {
+            v4[1] += GAQ[e] * GAK[e];
+            v4[2] += GAQ[e] * BBq[e];
+            v4[3] += GAK[e] * BBk[e];
         }
-        cross = block_sum_d(cross, red);
-        approx = block_sum_d(approx, red);
-        rq = block_sum_d(rq, red) + tq;
-        rk = block_sum_d(rk, red) + tk;
-        return 0.5 * fmax(qk2 - 2.0 * cross + approx, 0.0) + 0.5 * lq * rq + 0.5 * lk * rk;
+        block_sums<4>(v4, red);
+        return 0.5 * fmax(qk2 - 2.0 * v4[0] + v4[1], 0.0) + 0.5 * lq * (v4[2] + tq) + 0.5 * lk * (v4[3] + tk);
     };
     auto fail = [&](uint32_t bit) {
         if (tid == 0) set_status(P.status, bit);
     };
-    // B = G_A^-1 C^T (update_B, prefill.py:161-163), r x d
-    auto update_B = [&](const double *GA, const double *Cx, double *B) -> bool {
-        const int rc = chol_inverse(GA, r, Lm, Li, red);
-        if (rc >= 2) { fail(rc == 3 ? LRQK_ST_NONFINITE : LRQK_ST_SOLVE_FAILED); return false; }
-        if (rc == 1) fail(LRQK_ST_JITTERED);
-        for (int e = tid; e < r * d; e += nt) {
-            const int p = e / d, i = e % d;
-            double s = 0.0;
-            for (int q = 0; q < r; ++q) s += Li[p * r + q] * Cx[i * r + q];
-            B[e] = s;
-        }
+    auto inverse = [&](double *Mx) -> bool {
+        const int rc2 = spd_inverse_f64<R>(Mx, r, Wg, rc, red);
+        if (rc2 >= 2) { fail(rc2 == 3 ? LRQK_ST_NONFINITE : LRQK_ST_SOLVE_FAILED); return false; }
+        if (rc2 == 1) fail(LRQK_ST_JITTERED);
+        return true;
+    };
+    // B = G_A^-1 C^T (update_B, prefill.py:161-163), then B B^T
+    auto update_B = [&](const double *GA, const double *Cx, double *B, double *BB) -> bool {
+        for (int e = tid; e < R * R; e += nt) Mm[e] = GA[e];
         __syncthreads();
+        if (!inverse(Mm)) return false;
+        tile_mm<R, D, R>([&](int p, int q) { return Mm[p * R + q]; }, [&](int q, int i) { return Cx[i * R + q]; },
+                         [&](int p, int i, double v) { B[p * D + i] = v; });
+        tile_mm<R, R, D>([&](int p, int i) { return B[p * D + i]; }, [&](int i, int q) { return B[q * D + i]; },
+                         [&](int p, int q, double v) { BB[p * R + q] = v; });
         return true;
     };
     // Wn = (Cx + lam B^T)(G_A + lam B B^T)^-1 (update_AK / update_AQ, prefill.py:166-181)
-    auto update_W = [&](const double *GA, const double *Cx, const double *B, double lam) -> bool {
-        for (int e = tid; e < r * r; e += nt) {
-            const int p = e / r, q = e % r;
-            double bb = 0.0;
-            for (int i = 0; i < d; ++i) bb += B[p * d + i] * B[q * d + i];
-            Mm[e] = GA[e] + lam * bb;
-        }
+    auto update_W = [&](const double *GA, const double *Cx, const double *B, const double *BB, double lam) -> bool {
+        for (int e = tid; e < R * R; e += nt) Mm[e] = GA[e] + lam * BB[e];
         __syncthreads();
-        const int rc = chol_inverse(Mm, r, Lm, Li, red);
-        if (rc >= 2) { fail(rc == 3 ? LRQK_ST_NONFINITE : LRQK_ST_SOLVE_FAILED); return false; }
-        if (rc == 1) fail(LRQK_ST_JITTERED);
-        for (int e = tid; e < d * r; e += nt) {
-            const int i = e / r, p = e % r;
-            double s = 0.0;
-            for (int q = 0; q < r; ++q) s += (Cx[i * r + q] + lam * B[q * d + i]) * Li[q * r + p];
-            Wn[e] = s;
-        }
-        __syncthreads();
+        if (!inverse(Mm)) return false;
+        tile_mm<D, R, R>([&](int i, int q) { return Cx[i * R + q] + lam * B[q * D + i]; },
+                         [&](int q, int p) { return Mm[q * R + p]; }, [&](int i, int p, double v) { Wn[i * R + p] = v; });
         return true;
     };
-    // out = GX X (d x r)
-    auto gram_times = [&](const double *GX, const double *X, double *out) {
-        for (int e = tid; e < d * r; e += nt) {
-            const int i = e / r, p = e % r;
-            double s = 0.0;
-            for (int j = 0; j < d; ++j) s += GX[i * D + j] * X[j * r + p];
-            out[e] = s;
-        }
-        __syncthreads();
-    };
-    // after Wn: new C, G_A, and ||A' - A||^2 (sweep 1: against the init A0)
-    auto advance = [&](const double *GX, double *W, double *Cx, double *GA, const double *C0, double trg0,
-                       bool first) -> double {
-        double diff = 0.0;
+    // after Wn: new C = GX W, G_A = W^T C, and ||A' - A||^2 (sweep 1: against A0)
+    auto advance = [&](const double *__restrict__ GX, double *W, double *Cx, double *GA, const double *C0,
+                       double trg0, bool first) -> double {
+        double dv[1] = {0.0};
         if (first) {
-            gram_times(GX, Wn, Cx);
-            for (int e = tid; e < d * r; e += nt) diff += Wn[e] * (Cx[e] - 2.0 * C0[(e / r) * RS + e % r]);
-            diff = block_sum_d(diff, red) + trg0;
+            tile_mm<D, R, D>([&](int i, int j) { return GX[i * D + j]; }, [&](int j, int p) { return Wn[j * R + p]; },
+                             [&](int i, int p, double v) { Cx[i * R + p] = v; });
+            for (int e = tid; e < D * R; e += nt) { dv[0] += Wn[e] * (Cx[e] - 2.0 * C0[e]); W[e] = Wn[e]; }
+            block_sums<1>(dv, red);
+            dv[0] += trg0;
         } else {
-            for (int e = tid; e < d * r; e += nt) W[e] = Wn[e] - W[e];  // dW
+            for (int e = tid; e < D * R; e += nt) W[e] = Wn[e] - W[e];  // dW
             __syncthreads();
-            gram_times(GX, W, Dt);
-            for (int e = tid; e < d * r; e += nt) { diff += W[e] * Dt[e]; Cx[e] += Dt[e]; }
-            diff = block_sum_d(diff, red);
+            tile_mm<D, R, D>([&](int i, int j) { return GX[i * D + j]; }, [&](int j, int p) { return W[j * R + p]; },
+                             [&](int i, int p, double v) { Dt[i * R + p] = v; });
+            for (int e = tid; e < D * R; e += nt) { dv[0] += W[e] * Dt[e]; Cx[e] += Dt[e]; W[e] = Wn[e]; }
+            block_sums<1>(dv, red);
         }
-        for (int e = tid; e < d * r; e += nt) W[e] = Wn[e];
+        tile_mm<R, R, D>([&](int p, int i) { return W[i * R + p]; }, [&](int i, int q) { return Cx[i * R + q]; },
+                         [&](int p, int q, double v) { Mm[p * R + q] = v; });
+        for (int e = tid; e < R * R; e += nt) GA[e] = 0.5 * (Mm[e] + Mm[(e % R) * R + e / R]);
         __syncthreads();
-        for (int e = tid; e < r * r; e += nt) {
-            const int p = e / r, q = e % r;
-            double s = 0.0, t = 0.0;
-            for (int i = 0; i < d; ++i) { s += W[i * r + p] * Cx[i * r + q]; t += W[i * r + q] * Cx[i * r + p]; }
-            GA[e] = 0.5 * (s + t);
-        }
-        __syncthreads();
-        return fmax(diff, 0.0);
+        return fmax(dv[0], 0.0);
     };
 
     if (obj) {
@@ -499,51 +506,50 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
     }
     int sweeps = 0, conv = 0, ok = 1;
     for (int s = 0; s < P.max_iter; ++s) {
-        // old B factors for the convergence measure (into Dt: r x d each)
-        double dbq = 0.0, dbk = 0.0;
-        for (int e = tid; e < r * d; e += nt) { Boq[e] = Bq[e]; Bok[e] = Bk[e]; }
+        for (int e = tid; e < R * D; e += nt) { Boq[e] = Bq[e]; Bok[e] = Bk[e]; }
         __syncthreads();
-        if (!update_B(GAQ, Cq, Bq) || !update_B(GAK, Ck, Bk)) { ok = 0; break; }
-        for (int e = tid; e < r * d; e += nt) {
-            const double a = Bq[e] - Boq[e], b = Bk[e] - Bok[e];
-            dbq += a * a;
-            dbk += b * b;
-        }
-        dbq = block_sum_d(dbq, red);
-        dbk = block_sum_d(dbk, red);
-        if (!update_W(GAQ, Cq, Bk, lk)) { ok = 0; break; }
+        if (!update_B(GAQ, Cq, Bq, BBq) || !update_B(GAK, Ck, Bk, BBk)) { ok = 0; break; }
+        if (!update_W(GAQ, Cq, Bk, BBk, lk)) { ok = 0; break; }
         const double dak = advance(GK, Wk, Ck, GAK, CK0, trg0k, s == 0);
-        if (!update_W(GAK, Ck, Bq, lq)) { ok = 0; break; }
+        if (!update_W(GAK, Ck, Bq, BBq, lq)) { ok = 0; break; }
         const double daq = advance(GQ, Wq, Cq, GAQ, CQ0, trg0q, s == 0);
         ++sweeps;
+        double v3[3] = {0.0, 0.0, 0.0};  // ||dB_Q||^2, ||dB_K||^2, non-finite count
+        for (int e = tid; e < R * D; e += nt) {
+            const double a = Bq[e] - Boq[e], b = Bk[e] - Bok[e];
+            v3[0] += a * a;
+            v3[1] += b * b;
+            v3[2] += (isfinite(Wq[e]) && isfinite(Wk[e])) ? 0.0 : 1.0;
+        }
+        block_sums<3>(v3, red);
         // non-finite factors (prefill.py:216-218)
-        double bad = isfinite(dak) && isfinite(daq) && isfinite(dbq) && isfinite(dbk) ? 0.0 : 1.0;
-        for (int e = tid; e < d * r; e += nt) bad += (isfinite(Wq[e]) && isfinite(Wk[e])) ? 0.0 : 1.0;
-        if (block_sum_d(bad, red) != 0.0) { fail(LRQK_ST_NONFINITE); ok = 0; break; }
+        if (v3[2] != 0.0 || !isfinite(dak) || !isfinite(daq) || !isfinite(v3[0]) || !isfinite(v3[1])) {
+            fail(LRQK_ST_NONFINITE);
+            ok = 0;
+            break;
+        }
         if (obj) {
             const double o = objective();
             if (tid == 0) obj[s + 1] = (float)o;
         }
         // _factor_delta (prefill.py:184-194): mean over the four factors
         const double lr = (double)G.l * r, rd = (double)r * d;
-        const double delta = (daq / lr + dak / lr + dbq / rd + dbk / rd) / 4.0;
+        const double delta = (daq / lr + dak / lr + v3[0] / rd + v3[1] / rd) / 4.0;
         if (delta <= (double)P.tol) { conv = 1; break; }
     }
     if (tid == 0) { P.sweeps[h] = sweeps; P.converged[h] = conv; }
-    // outputs: B (fp32, [RS][ds] zero-padded) and W for the materialize pass
-    float *BQo = P.B_Q + (size_t)h * RS * G.ds, *BKo = P.B_K + (size_t)h * RS * G.ds;
-    for (int e = tid; e < RS * G.ds; e += nt) {
+    // outputs: B (fp32, [RS][ds]) and W for the materialize pass
+    float *BQo = P.B_Q + (size_t)h * R * G.ds, *BKo = P.B_K + (size_t)h * R * G.ds;
+    for (int e = tid; e < R * G.ds; e += nt) {
         const int p = e / G.ds, i = e % G.ds;
-        const bool in = ok && p < r && i < d;
-        BQo[e] = in ? (float)Bq[p * d + i] : 0.f;
-        BKo[e] = in ? (float)Bk[p * d + i] : 0.f;
+        BQo[e] = ok ? (float)Bq[p * D + i] : 0.f;
+        BKo[e] = ok ? (float)Bk[p * D + i] : 0.f;
     }
-    float *WQo = Wout + (size_t)h * D * RS, *WKo = Wout + ((size_t)G.H + h) * D * RS;
-    for (int e = tid; e < D * RS; e += nt) {
-        const int i = e / RS, p = e % RS;
-        const bool in = ok && sweeps > 0 && p < r && i < d;
-        WQo[e] = in ? (float)Wq[i * r + p] : 0.f;
-        WKo[e] = in ? (float)Wk[i * r + p] : 0.f;
+    float *WQo = Wout + (size_t)h * D * R, *WKo = Wout + ((size_t)G.H + h) * D * R;
+    for (int e = tid; e < D * R; e += nt) {
+        const bool in = ok && sweeps > 0;
+        WQo[e] = in ? (float)Wq[e] : 0.f;
+        WKo[e] = in ? (float)Wk[e] : 0.f;
     }
 }
 
@@ -561,17 +567,18 @@ __host__ __device__ inline void mat_unit(const PfGeom &G, int u, int &kside, int
 }
 
 __global__ void __launch_bounds__(kMatThreads, 1)
-pf_mat_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, const float *__restrict__ W, float *A_Q, float *A_K) {
+pf_mat_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, const float *__restrict__ W, float *A_Q, float *A_K,
+              int u0, int S2, int budget) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-    const int u = blockIdx.x / G.S2, s = blockIdx.x % G.S2;
+    const int u = u0 + blockIdx.x / S2, s = blockIdx.x % S2;
     int kside, xh, h0, nh;
     mat_unit(G, u, kside, xh, h0, nh);
     const int RS = G.rs, N = nh * 2 * RS;  // accumulator columns: per head [hi-part | lo-part]
     const int nxb = G.XW / 64, npart = G.parts;
     const int stage_bytes = npart * 2 * kBlkBytes;
-    const int wbytes = 2 * G.Nmax * 128;  // W^T split, K-major SW128: [2 d-blocks][N rows][128 B]
-    const int nst = min(kMaxStages, (int)((kSmemBudget - wbytes) / stage_bytes));
+    const int wbytes = 2 * (kside ? G.Nmax : 2 * RS) * 128;  // W^T split, K-major SW128: [2 d-blocks][N rows][128 B]
+    const int nst = min(kMaxStages, (budget - wbytes) / stage_bytes);
     uint8_t *sW = sm + nst * stage_bytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(sW + wbytes);
     uint64_t *empty = full + kMaxStages;
@@ -579,7 +586,7 @@ pf_mat_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, const float *
     uint64_t *tempty = tfull + 2;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t0 = (int)((long long)G.tiles * s / G.S2), t1 = (int)((long long)G.tiles * (s + 1) / G.S2);
+    const int t0 = (int)((long long)G.tiles * s / S2), t1 = (int)((long long)G.tiles * (s + 1) / S2);
     const uint32_t ncols = N <= 16 ? 32 : (N <= 32 ? 64 : (N <= 64 ? 128 : (N <= 128 ? 256 : 512)));
     const int mx = kside ? MK : MQ, mxl = kside ? MKL : MQL;
 
@@ -725,17 +732,30 @@ __global__ void pf_split_kernel(const T *__restrict__ X, int rows, int cols, int
 }
 
 __global__ void pf_ysplit_kernel(const float *__restrict__ A, int rows, int r, int RS, int YW, __nv_bfloat16 *__restrict__ Y) {
-    const long long n = (long long)rows * YW;
+    // Y = [A hi | A lo | 0]: one thread per row and 8-column chunk
+    const int cpr = YW / 8;
+    const long long n = (long long)rows * cpr;
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        const long long rI = e / YW;
-        const int c = (int)(e % YW);
-        float v = 0.f;
-        if (c < 2 * RS && c % RS < r) {
-            const float a = A[rI * RS + c % RS];
-            const __nv_bfloat16 h = __float2bfloat16_rn(a);
-            v = c < RS ? __bfloat162float(h) : a - __bfloat162float(h);
+        const long long rI = e / cpr;
+        const int c0 = (int)(e - rI * cpr) * 8;
+        uint32_t pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint16_t h2[2];
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                const int c = c0 + 2 * q + t;
+                float v = 0.f;
+                if (c < 2 * RS && c % RS < r) {
+                    const float a = A[rI * RS + c % RS];
+                    const __nv_bfloat16 hi = __float2bfloat16_rn(a);
+                    v = c < RS ? __bfloat162float(hi) : a - __bfloat162float(hi);
+                }
+                h2[t] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+            }
+            pk[q] = (uint32_t)h2[0] | ((uint32_t)h2[1] << 16);
         }
-        Y[e] = __float2bfloat16_rn(v);
+        *reinterpret_cast<uint4 *>(Y + rI * YW + c0) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
 }
 
@@ -744,7 +764,7 @@ __global__ void pf_ysplit_kernel(const float *__restrict__ A, int rows, int r, i
 // ---------------------------------------------------------------------------
 extern int num_sms();
 
-static int pick_slabs(int units, int tiles, int nsm) {
+static int pick_slabs(int units, int tiles, int nsm) {  // nsm: resident block slots
     // the smallest slab count whose last wave of one-block-per-SM is >= 85 % full
     int best = 1;
     double best_eff = -1.0;
@@ -784,13 +804,12 @@ static bool pf_geom(const lrqk_prefill_t &P, PfGeom &G) {
     G.NU = (G.NQU + G.NKU) * G.parts + 2 * G.NY;
     G.tiles = (G.l + kTile - 1) / kTile;
     const int nsm = num_sms();
-    G.S = pick_slabs(G.NU, G.tiles, nsm);
+    G.S = pick_slabs(G.NU, G.tiles, nsm * (G.parts == 1 ? 2 : 1));
     G.PW = 128 + (G.parts == 2 ? G.XW + G.YW : G.YW);
     G.HPU = std::max(1, std::min(G.group, 256 / (2 * G.rs)));
     G.nsub = (G.group + G.HPU - 1) / G.HPU;
     G.NMU = G.H + G.Hk * G.nsub;
     G.Nmax = std::max(2 * G.rs, G.HPU * 2 * G.rs);
-    G.S2 = pick_slabs(G.NMU, G.tiles, nsm);
     size_t o = 0;
     const size_t xq = (size_t)G.H * G.l * G.XW * 2, xk = (size_t)G.Hk * G.l * G.XW * 2;
     const bool own_x = !G.direct;
@@ -879,7 +898,7 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
     }
     const float *a0q = P.A_Q0 ? P.A_Q0 : P.A_Q, *a0k = P.A_K0 ? P.A_K0 : P.A_K;
     {
-        const long long n = (long long)G.NY * G.l * G.YW;
+        const long long n = (long long)G.NY * G.l * (G.YW / 8);
         const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
         pf_ysplit_kernel<<<grid, 256, 0, st>>>(a0q, G.NY * G.l, G.r, G.rs, G.YW,
                                                reinterpret_cast<__nv_bfloat16 *>(scr + G.off_y[0]));
@@ -895,10 +914,12 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
         ok = ok && make_map(&maps.m[MQL], xql, G.H, G.l, G.XW) && make_map(&maps.m[MKL], xkl, Hk, G.l, G.XW);
     if (!ok) return LRQK_ECUDA;
     // ---- K1g -----------------------------------------------------------------
-    const size_t gsm = kSmemBudget + 3072;
-    cudaFuncSetAttribute(pf_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+    // bf16: two CTAs per SM (TMEM 256 columns, 2 stages of X|Y each); fp32: one
+    const int gbudget = G.parts == 1 ? 96 * 1024 : 200 * 1024;
+    const size_t gsm = gbudget + 2048;
+    cudaFuncSetAttribute(pf_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 2048);
     float *part = reinterpret_cast<float *>(scr + G.off_part);
-    pf_gram_kernel<<<G.NU * G.S, kGramThreads, gsm, st>>>(maps, G, part);
+    pf_gram_kernel<<<G.NU * G.S, kGramThreads, gsm, st>>>(maps, G, part, gbudget);
     // ---- K1c -----------------------------------------------------------------
     {
         const long long tot = (long long)(G.NQU + G.NKU) * kTile * (kTile + G.rs) + 2LL * G.NY * G.rs * G.rs;
@@ -906,14 +927,33 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
         pf_combine_kernel<<<grid, 256, 0, st>>>(G, part, scr);
     }
     // ---- K1s -----------------------------------------------------------------
-    const size_t ssm = (5 * (size_t)G.r * G.r + 64) * sizeof(double);
-    cudaFuncSetAttribute(pf_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-    pf_solve_kernel<<<G.H, kSolveThreads, ssm, st>>>(G, P, scr);
+    const size_t ssm = (6 * (size_t)G.rs * G.rs + 256 + 5 * 32) * sizeof(double);
+#define LRQK_PF_SOLVE(RV)                                                                               \
+    do {                                                                                                \
+        cudaFuncSetAttribute(pf_solve_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm); \
+        pf_solve_kernel<RV><<<G.H, kSolveThreads, ssm, st>>>(G, P, scr);                                \
+    } while (0)
+    if (G.rs == 8) LRQK_PF_SOLVE(8);
+    else if (G.rs == 16) LRQK_PF_SOLVE(16);
+    else if (G.rs == 32) LRQK_PF_SOLVE(32);
+    else LRQK_PF_SOLVE(64);
+#undef LRQK_PF_SOLVE
     // ---- K1m -----------------------------------------------------------------
-    const size_t msm = kSmemBudget + 3072;
-    cudaFuncSetAttribute(pf_mat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
-    pf_mat_kernel<<<G.NMU * G.S2, kMatThreads, msm, st>>>(maps, G, reinterpret_cast<const float *>(scr + G.off_w),
-                                                          P.A_Q, P.A_K);
+    // query heads: two CTAs per SM for bf16 (N = 2r, W^T 16 KB, 2 stages);
+    // K heads: one CTA per SM, one K tile for up to 256 / 2r heads of its group
+    cudaFuncSetAttribute(pf_mat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 2048);
+    const float *Wsp = reinterpret_cast<const float *>(scr + G.off_w);
+    const int nsm = num_sms();
+    {
+        const int budget = G.parts == 1 ? 96 * 1024 : 200 * 1024;
+        const int S2 = pick_slabs(G.H, G.tiles, nsm * (G.parts == 1 ? 2 : 1));
+        pf_mat_kernel<<<G.H * S2, kMatThreads, budget + 2048, st>>>(maps, G, Wsp, P.A_Q, P.A_K, 0, S2, budget);
+    }
+    {
+        const int nk = G.Hk * G.nsub, S2 = pick_slabs(nk, G.tiles, nsm);
+        pf_mat_kernel<<<nk * S2, kMatThreads, 200 * 1024 + 2048, st>>>(maps, G, Wsp, P.A_Q, P.A_K, G.H, S2,
+                                                                       200 * 1024);
+    }
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
 
