@@ -10,7 +10,7 @@ LIB := $(PKG)/liblrqk_b200.so
 # (tools/step_timeline.py loads it through LRQK_LIB_PATH)
 TOBJ := $(patsubst $(PKG)/csrc/%.cu,build/trace/%.o,$(SRC))
 TLIB := $(PKG)/liblrqk_b200_trace.so
-HDRS := $(PKG)/csrc/common.cuh $(PKG)/csrc/select_common.cuh $(PKG)/csrc/mma_common.cuh include/lrqk_b200.h
+HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/lrqk_b200.h
 
 all: $(LIB)
 

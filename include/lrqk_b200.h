@@ -60,6 +60,7 @@ extern "C" {
 #define LRQK_ST_CAPACITY 8u      /* store capacity t_max exhausted          */
 #define LRQK_ST_JITTERED 16u     /* informational: a jittered solve ran     */
 #define LRQK_ST_FALLBACK 32u     /* informational: direct-solve fallback ran */
+#define LRQK_ST_BARRIER 64u      /* a per-head barrier of lrqk_score_attend timed out (never expected) */
 
 typedef struct lrqk_layer {
     /* ---- shapes / configuration ---- */
@@ -174,6 +175,16 @@ int lrqk_select(const lrqk_layer_t *L, void *stream);
  * after it.  ref: cache.py:149-171, attention.py:23-34. */
 int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
+/* lrqk_score + lrqk_select_attend + the partial merge as ONE kernel (HBM
+ * policy, dim_stride 128): each head's blocks meet at per-head barriers, so
+ * a head selects and attends as soon as its own parts have streamed.  Heads
+ * off the hint-window path this step are left to lrqk_select /
+ * lrqk_attention as after lrqk_score.  Returns LRQK_EUNSUPPORTED (nothing
+ * launched) for layouts it does not cover or when its grid cannot be
+ * co-resident; run lrqk_score + lrqk_select_attend then.
+ * ref: cache.py:141-171, linalg.py:96-110, attention.py:23-34. */
+int lrqk_score_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
+
 /* Host policy: copy this step's missed K/V rows from the pinned host slow
  * tier into their slots (zero-copy PCIe reads).  ref: cache.py:193-194. */
 int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);
@@ -182,8 +193,8 @@ int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);
  * ref: attention.py:23-34, session.py:101-102. */
 int lrqk_attention(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
-/* One whole decode step of one layer (compress, score, select_attend,
- * select, gather, attention, compress_prepare -- the reference's order,
+/* One whole decode step of one layer (compress, score_attend -- or score +
+ * select_attend --, select, gather, attention, compress_prepare -- the reference's order,
  * session.py:90-104); advance!=0 also bumps ctx_len. */
 int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const void *v,
                      float *out, int advance, void *stream);

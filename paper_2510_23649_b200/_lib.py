@@ -22,6 +22,7 @@ ST_INDEX_RANGE = 4
 ST_CAPACITY = 8
 ST_JITTERED = 16
 ST_FALLBACK = 32
+ST_BARRIER = 64
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 
@@ -81,6 +82,7 @@ SIGNATURES = {
     "lrqk_attention": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_compress_prepare_layers": (C.c_int, [_P, C.POINTER(LayerStruct), C.c_int32, _P]),
     "lrqk_select_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
+    "lrqk_score_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_workspace_size": (C.c_size_t, [C.POINTER(LayerStruct)]),
     "lrqk_score_append": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_cache_update": (C.c_int, [C.POINTER(LayerStruct), _P]),

@@ -3,6 +3,7 @@
 // K5b: host-policy miss gather from the pinned host slow tier (cache.py:193-194)
 // plus prompt seeding (cache.py:114-124) and small utilities.
 #include "common.cuh"
+#include "attend_common.cuh"
 
 namespace lrqk {
 
@@ -53,49 +54,11 @@ __device__ void fold_yg_slots(const lrqk_layer_t &L, int bh, int yg_slots, int b
 // Output of a head whose selection ran in select_attend_kernel: its
 // parts + 1 partials (max, sum, acc[d]; log2 domain) merged by one block.
 __device__ void merge_select_attend_partials(const lrqk_layer_t &L, int bh, float *out) {
-    __shared__ float s_w[64], s_den, s_mx;
+    __shared__ float s_w[64], s_red[2];
     const int d = L.dim_stride;
     const int np = L.sel_meta[(size_t)bh * kMetaInts + M_ATT_PARTS];
     const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, np - 1) * (size_t)(d + 2);
-    if (threadIdx.x < 32) {
-        float mx = -INFINITY;
-        for (int p = threadIdx.x; p < np; p += 32) mx = fmaxf(mx, __ldcg(parts + (size_t)p * (d + 2)));
-        mx = warp_max(mx);
-        float den = 0.f;
-        for (int p = threadIdx.x; p < np; p += 32) {
-            const float pm = __ldcg(parts + (size_t)p * (d + 2));
-            const float w = pm == -INFINITY ? 0.f : exp2f(pm - mx);
-            if (p < 64) s_w[p] = w;
-            den = fmaf(__ldcg(parts + (size_t)p * (d + 2) + 1), w, den);
-        }
-        den = warp_sum(den);
-        if (threadIdx.x == 0) { s_den = den; s_mx = mx; }
-    }
-    __syncthreads();
-    const float inv = 1.f / s_den;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-        float o = 0.f;
-        for (int p0 = 0; p0 < np; p0 += 8) {  // 8 partials' loads in flight, summed in order
-            float v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (p0 + u < np) v[u] = __ldcg(parts + (size_t)(p0 + u) * (d + 2) + 2 + i);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int p = p0 + u;
-                if (p >= np) break;
-                float w;
-                if (p < 64) {
-                    w = s_w[p];
-                } else {
-                    const float pm = __ldcg(parts + (size_t)p * (d + 2));
-                    w = pm == -INFINITY ? 0.f : exp2f(pm - s_mx);
-                }
-                o = fmaf(v[u], w, o);
-            }
-        }
-        out[(size_t)bh * d + i] = o * inv;
-    }
+    merge_partials(parts, np, d, out + (size_t)bh * d, s_w, s_red);
     trace(39);
 }
 
@@ -119,10 +82,15 @@ attention_kernel(const AttnArgs a) {
     trace(30);
     pdl_wait();
     pdl_trigger();
-    if (L.sel_meta[(size_t)bh * kMetaInts + M_MODE] == 5) {
+    const int mode = L.sel_meta[(size_t)bh * kMetaInts + M_MODE];
+    if (mode == 5) {
         // select_attend_kernel left parts + 1 softmax partials: merge them
         if (split == 0) merge_select_attend_partials(L, bh, a.out);
         else if (a.yg_slots > 0) fold_yg_slots(L, bh, a.yg_slots, split - 1, gridDim.x - 1);
+        return;
+    }
+    if (mode == 6) {  // score_attend_kernel wrote the output: only fold its Y|G slots
+        if (a.yg_slots > 0) fold_yg_slots(L, bh, a.yg_slots, split, gridDim.x);
         return;
     }
     const int S = L.res_cnt[bh];

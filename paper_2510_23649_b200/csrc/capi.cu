@@ -21,6 +21,7 @@ int select_sure_rows(const lrqk_layer_t &L);
 int score_part_rows(const lrqk_layer_t &L);
 int attn_scratch_slots(const lrqk_layer_t &L);
 int launch_select_attend(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st);
+int launch_score_attend(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st);
 int launch_seed(const lrqk_layer_t &L, int prompt_len, cudaStream_t st);
 int launch_advance(int32_t *ctx_len, int n, cudaStream_t st);
 int launch_proxy_scores(const void *store, int dtype, const float *qh, float *out, int n_heads, int n_rows, int R,
@@ -228,6 +229,24 @@ int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *s
     return check(launch_select_attend(*L, q, out, (cudaStream_t)stream));
 }
 
+// LRQK_FUSED=0 turns the fused score/select/attend kernel off (A/B runs)
+static bool fused_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("LRQK_FUSED");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on != 0;
+}
+
+int lrqk_score_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream) {
+    int rc = validate(L);
+    if (rc) return rc;
+    if (!q || !out) return LRQK_EINVAL;
+    if (!fused_enabled()) return LRQK_EUNSUPPORTED;
+    return check(launch_score_attend(*L, q, out, (cudaStream_t)stream));
+}
+
 int lrqk_attention(const lrqk_layer_t *L, const void *q, float *out, void *stream) {
     int rc = validate(L);
     if (rc) return rc;
@@ -241,8 +260,13 @@ int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const 
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     if ((rc = check(launch_compress(*L, q, k, v, 1, st)))) return rc;
-    if ((rc = check(launch_score(*L, nullptr, st)))) return rc;
-    if ((rc = check(launch_select_attend(*L, q, out, st)))) return rc;
+    rc = fused_enabled() ? launch_score_attend(*L, q, out, st) : LRQK_EUNSUPPORTED;
+    if (rc == LRQK_EUNSUPPORTED) {
+        if ((rc = check(launch_score(*L, nullptr, st)))) return rc;
+        if ((rc = check(launch_select_attend(*L, q, out, st)))) return rc;
+    } else if ((rc = check(rc))) {
+        return rc;
+    }
     if ((rc = check(launch_select(*L, st)))) return rc;
     if ((rc = check(launch_gather(*L, st)))) return rc;
     if ((rc = check(launch_attention(*L, q, out, st)))) return rc;

@@ -48,6 +48,7 @@ enum Meta : int {
     M_ATT_PARTS = 43,  // softmax partials select_attend left for attention_kernel to merge (parts + 1)
     M_KC = 44,         // this step's candidate bound (key) of cmask; 0xFFFFFFFF: no mask
     M_YG_FOLD = 45,    // attention_kernel already summed the M_YG slots into slot 0
+    M_HINT_QN = 46,    // persistent: |q_hat| (f32 bits) of the step that set M_HINT
 };
 constexpr int kPrevCrit = 8;
 
@@ -304,6 +305,15 @@ LRQK_DEV uint64_t l2_policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+// L2 prefetches that survive an evict-first stream: a bulk range with a cache
+// policy, and one line with evict-last priority
+LRQK_DEV void bulk_prefetch_l2_hint(const void *p, uint32_t bytes, uint64_t policy) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(policy)
+                 : "memory");
+}
+LRQK_DEV void prefetch_l2_last(const void *p) {
+    asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 LRQK_DEV void st_hint_u32(uint32_t *p, uint32_t v, uint64_t policy) {
     asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(policy) : "memory");

@@ -42,7 +42,7 @@ __host__ __device__ inline int mma_stage_bytes(int R, int d) { return kMmaRows *
 // bf16 rows of rank_stride R; K tile: [kMmaRows][ldk bytes] bf16 rows of d.
 // Eight warps: warp w owns Y columns [w*8*NTW, (w+1)*8*NTW) and G tiles
 // w, w+8, ...  MT = R/16 m tiles, NTW = d/64 n tiles per warp.
-template <int MT, int NTW>
+template <int MT, int NTW, int KR = kMmaRows>
 LRQK_DEV void mma_reduce_tile(const uint8_t *kb_s, int ldk, const uint8_t *ab_s, int lda, int R,
                               float (&yacc)[MT][NTW][4], float (&gacc)[4][4]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -51,7 +51,7 @@ LRQK_DEV void mma_reduce_tile(const uint8_t *kb_s, int ldk, const uint8_t *ab_s,
     constexpr int GT = (RR / 16) * (RR / 8);
     (void)R;
 #pragma unroll
-    for (int ks = 0; ks < kMmaRows; ks += 16) {
+    for (int ks = 0; ks < KR; ks += 16) {
         uint32_t af[MT][4];
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {

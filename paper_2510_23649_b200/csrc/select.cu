@@ -25,20 +25,18 @@
 //                  block falls back to an exact radix select over all keys.
 #include "common.cuh"
 #include "select_common.cuh"
+#include "score_common.cuh"
 
 namespace lrqk {
 
 constexpr int kScoreThreads = 256;
 constexpr int kSelThreads = 512;
-constexpr int kSampleRows = 16384;  // histogram rows per head before sampling kicks in
 // Direct selection (mode 5, HBM policy): the score kernel also keeps each
 // part's window histogram (fcand, reinterpreted as [parts][kHistBins + 1]
 // uint32: bins, then the count above the window), so its last block knows
 // how many certain winners every part holds -> each select block writes its
 // winners straight to their final positions in res_idx.
 
-// extra sel_meta fields (common.cuh holds the first ones)
-enum MetaExt : int { M_B_HI = 8, M_B_LO = 9, M_STRIDE = 10, M_S2 = 11 };
 
 // fine (level-2) bin of a key inside the candidate band [b_lo, b_hi]
 LRQK_DEV int fine_bin(uint32_t key, int b_lo, int s2) {
@@ -46,48 +44,6 @@ LRQK_DEV int fine_bin(uint32_t key, int b_lo, int s2) {
 }
 
 
-
-LRQK_DEV int sample_stride(int n_rows) {  // in 32-row tiles
-    const int tiles = (n_rows + 31) >> 5;
-    const int want = kSampleRows >> 5;
-    return tiles <= want ? 1 : (tiles + want - 1) / want;
-}
-
-struct ScoreArgs {
-    lrqk_layer_t L;
-    const float *ext_scores;  // standalone path: precomputed float scores [BH, t+1]
-    int parts;                // work items per head
-};
-
-// Find D in [0, nbins) with  above(D) < m <= above(D) + hist[D], scanning bins
-// from the top (whole block).  s_out[0] = D (or -1 if total < m), s_out[1] = above.
-__device__ void find_crossing(const int *hist, int nbins, int m, int *s_scan, int *s_out) {
-    const int nt = blockDim.x;
-    const int per = (nbins + nt - 1) / nt;
-    const int hi = nbins - 1 - threadIdx.x * per;
-    if (threadIdx.x == 0) { s_out[0] = -1; s_out[1] = 0; }
-    int local = 0;
-    for (int i = 0; i < per; ++i) {
-        const int bin = hi - i;
-        if (bin >= 0) local += hist[bin];
-    }
-    int total;
-    const int above = block_exclusive_scan(local, s_scan, &total);
-    if (above < m && m <= above + local) {
-        int acc = above;
-        for (int i = 0; i < per; ++i) {
-            const int bin = hi - i;
-            if (bin < 0) break;
-            if (acc + hist[bin] >= m) {
-                s_out[0] = bin;
-                s_out[1] = acc;
-                break;
-            }
-            acc += hist[bin];
-        }
-    }
-    __syncthreads();
-}
 
 // ---------------------------------------------------------------------------
 // K3: score kernel.  NPK = 16-byte packs per proxy row (rank_stride*e/16).
@@ -229,23 +185,11 @@ score_kernel(const ScoreArgs a) {
 // per stage straight out of shared memory (lane = row).  Every byte of the
 // proxy store is read exactly once, with no register staging.
 // ---------------------------------------------------------------------------
-constexpr int kCW = 8;  // consumer warps
-
-template <int NPK> struct ScoreStages {
-    static constexpr int kTileBytes = NPK * 512;
-    static constexpr int kStageBytes = kCW * kTileBytes;
-    // 64 KB: two score blocks stay co-resident with a compress block (68 KB)
-    static constexpr int kStages = (64 * 1024 / kStageBytes) < 2 ? 2 : ((64 * 1024 / kStageBytes) > 6 ? 6 : 64 * 1024 / kStageBytes);
-    static constexpr int kSmem = kStages * kStageBytes + 2 * kStages * 8;
-};
-
 template <typename T, int NPK>
 __global__ void __launch_bounds__(32 * (kCW + 1))
 score_tma_kernel(const ScoreArgs a) {
     using SS = ScoreStages<NPK>;
     const lrqk_layer_t &L = a.L;
-    constexpr int N = Pack<T>::N;
-    constexpr int R = NPK * N;
     extern __shared__ __align__(128) uint8_t tsm[];
     uint64_t *full = reinterpret_cast<uint64_t *>(tsm + SS::kStages * SS::kStageBytes);
     uint64_t *empty = full + SS::kStages;
@@ -268,18 +212,10 @@ score_tma_kernel(const ScoreArgs a) {
     const int tpp = (tiles + P - 1) / P;
     const int tile0 = min(tiles, part * tpp), tile1 = min(tiles, tile0 + tpp);
     const int stride = sample_stride(lite_start);
-    const int n_stage_iters = (tile1 - tile0 + kCW - 1) / kCW;
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     // hint window (persistent meta written by the previous step's select)
     const bool win = meta[M_HINT_OK] != 0;
-    uint32_t klo = 0, kc = 0xFFFFFFFFu;
-    if (win) {
-        const uint32_t hk = (uint32_t)meta[M_HINT];
-        klo = hk > kWinKeys / 2 ? hk - kWinKeys / 2 : 0u;
-        if (klo > 0xFFFFFFFFu - (kWinKeys - 1)) klo = 0xFFFFFFFFu - (kWinKeys - 1);
-        kc = max(klo, hk > kCandBelow ? hk - kCandBelow : 0u);
-    }
-    uint32_t *cmask = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5);
+    uint32_t klo = 0, kc = 0xFFFFFFFFu;  // set after pdl_wait (the hint scales with this step's q_hat)
     for (int i = tid; i < kHistBins; i += blockDim.x) { s_hist[i] = 0; s_win[i] = 0; }
     if (tid == 0) {
         s_above = 0;
@@ -290,203 +226,20 @@ score_tma_kernel(const ScoreArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    int it0 = 0;  // stages in flight before the wait (producer lane)
+    if (warp == kCW && lane == 0) it0 = score_prefetch_stages<T, NPK>(L, bh, tile0, tile1, t, tsm, full);
     pdl_wait();  // q_hat, the appended proxy row and ctx_len come from compress
     pdl_trigger();
-    const uint8_t *src = reinterpret_cast<const uint8_t *>(reinterpret_cast<const T *>(L.proxy) +
-                                                           (size_t)bh * L.t_max * R);
-    uint32_t *keys = L.keys + (size_t)bh * L.t_max;
-    const uint64_t pol_stream = l2_policy_evict_first(), pol_keys = l2_policy_evict_last();
-    if (warp == kCW) {
-        // ---------------- producer ----------------
-        if (lane == 0) {
-            for (int it = 0; it < n_stage_iters; ++it) {
-                const int s2 = it % SS::kStages;
-                if (it >= SS::kStages) mbar_wait(empty + s2, ((it / SS::kStages) - 1) & 1);
-                const int nt = min(kCW, tile1 - tile0 - it * kCW);
-                const uint32_t bytes = (uint32_t)nt * SS::kTileBytes;
-                mbar_expect_tx(full + s2, bytes);
-                // the proxy store is streamed once per step: evict it first, so the
-                // keys (read again by the selection) stay in L2
-                bulk_g2s_hint(tsm + s2 * SS::kStageBytes, src + (size_t)(tile0 + it * kCW) * SS::kTileBytes, bytes,
-                              full + s2, pol_stream);
-            }
-        }
-    } else {
-        // ---------------- consumers ----------------
-        float qv[R];
-        const float *qh = L.q_hat + (size_t)bh * L.rank_stride;
-#pragma unroll
-        for (int e = 0; e < R; ++e) qv[e] = qh[e];
-        int above = 0;
-        for (int it = 0; it < n_stage_iters; ++it) {
-            const int s2 = it % SS::kStages;
-            mbar_wait(full + s2, (it / SS::kStages) & 1);
-            const int tile = tile0 + it * kCW + warp;
-            if (tile < tile1) {
-                const uint4 *p4 = reinterpret_cast<const uint4 *>(tsm + s2 * SS::kStageBytes + warp * SS::kTileBytes) + lane;
-                float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-                for (int pk = 0; pk < NPK; ++pk) {
-                    float f[N];
-                    unpack16<T>(p4[pk * 32], f);
-#pragma unroll
-                    for (int e = 0; e < N; e += 2) {
-                        s0 = fmaf(f[e], qv[pk * N + e], s0);
-                        s1 = fmaf(f[e + 1], qv[pk * N + e + 1], s1);
-                    }
-                }
-                const int row = tile * 32 + lane;
-                const uint32_t key = score_key(s0 + s1);
-                if (row < n) st_hint_u32(keys + row, key, pol_keys);
-                {   // candidate bit per row (the fused selection's shortlist)
-                    const uint32_t cm = __ballot_sync(0xffffffffu, win && row < lite_start && key >= kc);
-                    if (lane == 0) st_hint_u32(cmask + tile, cm, pol_keys);
-                }
-                if (row < lite_start) {
-                    // the sampled coarse histogram only serves the no-hint path
-                    if (!win && (tile % stride) == 0) atomicAdd(&s_hist[key >> (32 - kHistBits)], 1);
-                    if (win && key >= klo) {
-                        const uint32_t dk = key - klo;
-                        if (dk < kWinKeys) atomicAdd(&s_win[dk >> kWinShift], 1);
-                        else ++above;
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(empty + s2);
-        }
-        above = __reduce_add_sync(0xffffffffu, above);
-        if (lane == 0 && above) atomicAdd(&s_above, above);
-    }
+    if (win) hint_window(scaled_hint(meta, qhat_norm(L, bh)), klo, kc);
+    score_stream<T, NPK>(L, bh, tile0, tile1, n, lite_start, stride, win, klo, kc, tsm, full, empty, s_hist, s_win,
+                         &s_above, it0);
     trace(41);
     __syncthreads();
-    uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;
-    uint32_t *gwin = ghist + 2 * kHistBins;
-    for (int i = tid; i < kHistBins; i += blockDim.x) {
-        if (s_hist[i]) atomicAdd(ghist + i, (uint32_t)s_hist[i]);
-        if (s_win[i]) atomicAdd(gwin + i, (uint32_t)s_win[i]);
-    }
-    if (tid == 0 && s_above) atomicAdd(meta + M_ABOVE, s_above);
-    if (win) {
-        // this part's suffix counts (mode 5): ph[i] = rows of the part with a
-        // key in window bin >= i or above the window; ph[kHistBins] = above
-        uint32_t *ph = reinterpret_cast<uint32_t *>(L.fcand) + ((size_t)bh * P + part) * kPartHist;
-        constexpr int CB = kHistBins / 256;  // bins per thread (threads 0..255)
-        int loc = 0;
-        if (tid < 256)
-#pragma unroll
-            for (int j = 0; j < CB; ++j) loc += s_win[tid * CB + j];
-        int tot;
-        const int ex = block_exclusive_scan(loc, s_scan, &tot);
-        if (tid < 256) {
-            int suf = s_above + tot - ex;  // rows in bins >= tid*CB, plus above
-#pragma unroll
-            for (int j = 0; j < CB; ++j) {
-                ph[tid * CB + j] = (uint32_t)suf;
-                suf -= s_win[tid * CB + j];
-            }
-        }
-        if (tid == 0) ph[kHistBins] = (uint32_t)s_above;
-    }
+    score_flush(L, bh, P, part, win, s_hist, s_win, s_above, s_scan);
     int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
     if (!last_arrival(cnt, P, &s_flag)) return;
     trace(42);
-    // ---- last block of this head: candidate bins ----------------------------
-    const int k_eff = min(L.k_budget, lite_start);
-    if (lite_start == 0 || k_eff >= lite_start) {
-        if (tid == 0) {
-            meta[M_MODE] = 1; meta[M_K_EFF] = k_eff; meta[M_LITE] = lite_start;
-            meta[M_SURE] = 0; meta[M_CAND] = 0; meta[M_ABOVE] = 0;
-        }
-        return;
-    }
-    if (win) {
-        // mode 3 if the k-th largest key falls inside the hint window: the
-        // window histogram is exact, so bin D and the count above it are exact
-        const int above_win = __ldcg(meta + M_ABOVE);
-        for (int i = tid; i < kHistBins; i += blockDim.x) s_win[i] = (int)__ldcg(gwin + i);
-        __syncthreads();
-        int D = -1;
-        if (above_win < k_eff) {
-            find_crossing(s_win, kHistBins, k_eff - above_win, s_scan, s_out);
-            D = s_out[0];
-        }
-        if (D >= 0) {
-            const int nabove = above_win + s_out[1];
-            int mode = 3;
-            if (L.policy == LRQK_SLOW_HBM) {
-                // mode 5: certain winners per part -> exclusive offsets (fcnt)
-                mode = 5;
-                const uint32_t *ph0 = reinterpret_cast<const uint32_t *>(L.fcand) + (size_t)bh * P * kPartHist;
-                const int c = tid < P ? (int)__ldcg(ph0 + (size_t)tid * kPartHist + D + 1) : 0;
-                int tot;
-                const int off = block_exclusive_scan(c, s_scan, &tot);
-                if (tid < P) L.fcnt[(size_t)bh * P + tid] = off;
-                // inconsistent counts, or a threshold bin too large to sort: scan path
-                if (tot != nabove || s_win[D] > kFCrit) mode = 3;
-            }
-            if (tid == 0) {
-                meta[M_KLO] = (int)klo;
-                meta[M_KC] = (int)kc;
-                meta[M_FBIN] = D;
-                meta[M_NABOVE] = nabove;
-                meta[M_SPARTS] = P;
-                meta[M_K_EFF] = k_eff;
-                meta[M_LITE] = lite_start;
-                meta[M_SURE] = 0;
-                meta[M_CAND] = 0;
-                meta[M_ABOVE] = 0;
-                meta[M_MODE] = mode;
-            }
-            trace(43);
-            return;
-        }
-        __syncthreads();
-    }
-    if (win) {  // the hint window missed and no coarse histogram was taken: exact path
-        if (tid == 0) {
-            meta[M_B_HI] = kHistBins - 1;
-            meta[M_B_LO] = 0;
-            meta[M_STRIDE] = 1;
-            meta[M_S2] = 0;
-            meta[M_K_EFF] = k_eff;
-            meta[M_LITE] = lite_start;
-            meta[M_SURE] = 0;
-            meta[M_CAND] = 0;
-            meta[M_ABOVE] = 0;
-            meta[M_MODE] = 0;
-        }
-        return;
-    }
-    for (int i = tid; i < kHistBins; i += blockDim.x) s_hist[i] = (int)__ldcg(ghist + i);
-    __syncthreads();
-    int b_hi, b_lo;
-    if (stride == 1) {
-        find_crossing(s_hist, kHistBins, k_eff, s_scan, s_out);
-        b_hi = b_lo = s_out[0];
-    } else {
-        const int m_hi = max(1, (int)(0.8f * k_eff / stride));
-        find_crossing(s_hist, kHistBins, m_hi, s_scan, s_out);
-        b_hi = s_out[0] < 0 ? kHistBins - 1 : s_out[0];
-        const int m_lo = (int)ceilf(1.25f * k_eff / stride) + 8;
-        find_crossing(s_hist, kHistBins, m_lo, s_scan, s_out);
-        b_lo = s_out[0] < 0 ? 0 : s_out[0];
-    }
-    if (tid == 0) {
-        meta[M_B_HI] = b_hi;
-        meta[M_B_LO] = b_lo;
-        meta[M_STRIDE] = stride;
-        int s2 = 0;
-        while (s2 < 32 - kHistBits && ((b_hi - b_lo + 1) << (s2 + 1)) <= kHistBins) ++s2;
-        meta[M_S2] = s2;
-        meta[M_K_EFF] = k_eff;
-        meta[M_LITE] = lite_start;
-        meta[M_SURE] = 0;
-        meta[M_CAND] = 0;
-        meta[M_ABOVE] = 0;
-        meta[M_MODE] = 0;
-    }
-    trace(43);
+    score_last_block(L, bh, P, win, klo, kc, lite_start, stride, s_hist, s_win, s_scan, s_out);
 }
 
 // Radix select over unique composites (exact fallback): returns thr such that
@@ -577,7 +330,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
         if (t >= L.t_max) continue;
         int *meta = L.sel_meta + (size_t)bh * kMetaInts;
         const int mode0 = meta[M_MODE];
-        if (mode0 == 5) continue;  // select_attend_kernel handles this head
+        if (mode0 >= 5) continue;  // select_attend_kernel / score_attend_kernel handled this head
         const int lite_start = meta[M_LITE];
         const int k_eff = meta[M_K_EFF];
         const uint32_t *keys = L.keys + (size_t)bh * L.t_max;
@@ -1033,6 +786,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
             meta[M_HITS] = 0;
             meta[M_HINT] = (int)s_hint_key;
             meta[M_HINT_OK] = s_hint_ok;
+            meta[M_HINT_QN] = __float_as_int(qhat_norm(L, bh));
             meta[M_STAT + min(max(mode0, 0), 5)] += 1;
             if (exact_fb) meta[M_STAT + 6] += 1;
         }

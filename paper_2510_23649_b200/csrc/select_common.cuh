@@ -31,6 +31,35 @@ LRQK_DEV uint64_t make_comp(uint32_t key, int idx) {
 }
 LRQK_DEV int comp_index(uint64_t c) { return (int)(kIdxMax - (uint32_t)(c & kIdxMax)); }
 
+// |q_hat| of head bh this step (the hint's scale reference)
+LRQK_DEV float qhat_norm(const lrqk_layer_t &L, int bh) {
+    if (L.q_hat == nullptr) return 0.f;  // standalone selection (lrqk_select_scores): no q_hat
+    const float *qh = L.q_hat + (size_t)bh * L.rank_stride;
+    float a = 0.f;
+    for (int e = 0; e < L.rank_stride; ++e) a = fmaf(qh[e], qh[e], a);
+    return sqrtf(a);
+}
+
+// This step's threshold hint: the previous step's k-th largest score, scaled
+// by |q_hat_t| / |q_hat_{t-1}| (every proxy score is linear in q_hat, so a
+// change of its norm moves all scores, and the threshold, by that factor),
+// as a key.  The hint window is centred on it; without a stored norm the
+// previous key is used as is.
+LRQK_DEV uint32_t scaled_hint(const int *meta, float qn_now) {
+    const uint32_t hk = (uint32_t)meta[M_HINT];
+    const float qn0 = __int_as_float(meta[M_HINT_QN]);
+    if (!(qn0 > 0.f) || !(qn_now > 0.f) || !isfinite(qn0) || !isfinite(qn_now)) return hk;
+    const float sc = key_score(hk) * (qn_now / qn0);
+    return isfinite(sc) ? score_key(sc) : hk;
+}
+
+// klo (hint window start) and kc (candidate bound) around the hint key
+LRQK_DEV void hint_window(uint32_t hk, uint32_t &klo, uint32_t &kc) {
+    klo = hk > kWinKeys / 2 ? hk - kWinKeys / 2 : 0u;
+    if (klo > 0xFFFFFFFFu - (kWinKeys - 1)) klo = 0xFFFFFFFFu - (kWinKeys - 1);
+    kc = max(klo, hk > kCandBelow ? hk - kCandBelow : 0u);
+}
+
 LRQK_DEV int n_words_of(int rows) { return (rows + 31) >> 5; }
 
 // Bitonic sort of a[0, M) in shared memory (M a power of two), whole block.

@@ -235,6 +235,8 @@ class LayerState:
             raise IndexError("selection references a token outside the store")
         if st & _lib.ST_CAPACITY:
             raise RuntimeError("LRQK store capacity (t_max) exhausted")
+        if st & _lib.ST_BARRIER:
+            raise RuntimeError("a per-head barrier of the fused score/select/attend kernel timed out")
         return st
 
     # ---- step atomicity (the reference raises before mutating a session) ------
@@ -431,6 +433,7 @@ class Engine:
                                    device=self.device)
         self.graph = None
         self.kernels_per_step = None
+        self.fused = None  # the fused score/select/attend kernel ran (set by decode_step)
         # the layers' descriptors, on the host and on the device, for the
         # batched compress_prepare launch
         self._host_layers = (_lib.LayerStruct * n_layers)(*[l.struct for l in self.layers])
@@ -442,10 +445,11 @@ class Engine:
         return self.ctx_len[: 4 * self.shape.batch].view(torch.int32)
 
     def launches_per_step(self):
-        """Kernels one decode step launches: per layer compress, score,
-        [select_attend], select, [gather], attention; then the batched
-        compress_prepare (two kernels for bf16) and the ctx advance."""
-        per = 5
+        """Kernels one decode step launches: per layer compress,
+        score_attend (or score + select_attend), select, [gather], attention;
+        then the batched compress_prepare (two kernels for bf16) and the ctx
+        advance."""
+        per = 4 if self.fused else 5
         prep = 2 if self.shape.dtype == "bf16" else self.n_layers
         return self.n_layers * per + prep + 1
 
@@ -466,8 +470,13 @@ class Engine:
             lp = layer.ptr
             _lib.check(lib.lrqk_decode_compress(lp, q[i].data_ptr(), k[i].data_ptr(), v[i].data_ptr(), 1, sp),
                        "lrqk_decode_compress")
-            _lib.check(lib.lrqk_score(lp, sp), "lrqk_score")
-            _lib.check(lib.lrqk_select_attend(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_select_attend")
+            rc = lib.lrqk_score_attend(lp, q[i].data_ptr(), out[i].data_ptr(), sp)
+            self.fused = rc == _lib.OK
+            if rc == _lib.EUNSUPPORTED:  # layouts the fused kernel does not cover
+                _lib.check(lib.lrqk_score(lp, sp), "lrqk_score")
+                _lib.check(lib.lrqk_select_attend(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_select_attend")
+            else:
+                _lib.check(rc, "lrqk_score_attend")
             _lib.check(lib.lrqk_select(lp, sp), "lrqk_select")
             _lib.check(lib.lrqk_gather_misses(lp, sp), "lrqk_gather_misses")
             _lib.check(lib.lrqk_attention(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_attention")

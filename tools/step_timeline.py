@@ -17,6 +17,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--ctx", type=int, default=131072)
 p.add_argument("--layers", type=int, default=1)
 p.add_argument("--batch", type=int, default=1)
+p.add_argument("--fused-names", action="store_true", help="label the score_attend kernel's tags")
 a = p.parse_args()
 dev = torch.device("cuda")
 B, Hq, Hkv, d, r, l = a.batch, 32, 8, 128, 32, a.ctx
@@ -61,6 +62,11 @@ names = {0: "compress start", 1: "compress staged", 4: "compress B-update done",
          53: "sel_attend last-block", 54: "sel_attend end", 55: "sa crit sorted", 56: "sa part scanned", 44: "sa classified", 45: "sa crit flushed", 46: "sa cmask read", 47: "sa cands listed", 48: "sa keys classified", 49: "sa scanned",
          57: "sa part YG written", 58: "sa own partial", 59: "sa parts max", 60: "sa merged", 20: "select start", 30: "attention start", 10: "prepare start", 13: "finish YG summed", 7: "finish kernel start", 39: "attention merged (mode 5)", 8: "reduce kernel start", 9: "reduce kernel end", 35: "finish hits counted", 36: "finish B staged", 37: "finish B updated", 38: "finish grams",
          11: "prepare reduce done", 14: "prepare finish start", 16: "prepare end", 17: "prep idx staged", 18: "prep first chunk in", 19: "prep mma done", 61: "prep R gram", 62: "prep R GJ", 63: "prep pre-sync"}
+if a.fused_names:
+    names.update({41: "sa stream done", 42: "sa B1 passed", 46: "sa gwin loaded", 47: "sa D found", 48: "sa offsets",
+                  49: "sa cands listed", 55: "sa keys classified", 58: "sa winners scanned", 44: "sa classified",
+                  45: "sa B2 passed", 56: "sa lists ready", 59: "sa chunk 0 in", 60: "sa chunk 3 in", 52: "sa attended",
+                  57: "sa partial written", 53: "sa last block", 54: "sa end"})
 for tag in sorted(set(tags), key=lambda x: np.median(rec[tags == x, 1])):
     ts = (rec[tags == tag, 1] - t0) / 1e3
     print(f"tag {tag:3d} {names.get(tag, ''):24s} n={len(ts):4d} min={ts.min():7.1f} med={np.median(ts):7.1f} max={ts.max():7.1f} us")
