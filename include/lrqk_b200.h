@@ -185,6 +185,11 @@ int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *s
  * ref: cache.py:141-171, linalg.py:96-110, attention.py:23-34. */
 int lrqk_score_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
+/* Process-wide switch for lrqk_score_attend / lrqk_decode_step: 0 runs the
+ * split path (lrqk_score + lrqk_select_attend) everywhere; returns the
+ * previous setting.  Default on (environment LRQK_FUSED=0: off). */
+int lrqk_set_fused(int on);
+
 /* Host policy: copy this step's missed K/V rows from the pinned host slow
  * tier into their slots (zero-copy PCIe reads).  ref: cache.py:193-194. */
 int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);

@@ -83,6 +83,7 @@ SIGNATURES = {
     "lrqk_compress_prepare_layers": (C.c_int, [_P, C.POINTER(LayerStruct), C.c_int32, _P]),
     "lrqk_select_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
     "lrqk_score_attend": (C.c_int, [C.POINTER(LayerStruct), _P, _P, _P]),
+    "lrqk_set_fused": (C.c_int, [C.c_int]),
     "lrqk_workspace_size": (C.c_size_t, [C.POINTER(LayerStruct)]),
     "lrqk_score_append": (C.c_int, [C.POINTER(LayerStruct), _P]),
     "lrqk_cache_update": (C.c_int, [C.POINTER(LayerStruct), _P]),

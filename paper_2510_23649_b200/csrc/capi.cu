@@ -229,14 +229,21 @@ int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *s
     return check(launch_select_attend(*L, q, out, (cudaStream_t)stream));
 }
 
-// LRQK_FUSED=0 turns the fused score/select/attend kernel off (A/B runs)
+// LRQK_FUSED=0 (or lrqk_set_fused(0)) turns the fused score/select/attend
+// kernel off: A/B runs, and tests of the split path
+static int g_fused = -1;
 static bool fused_enabled() {
-    static int on = -1;
-    if (on < 0) {
+    if (g_fused < 0) {
         const char *e = getenv("LRQK_FUSED");
-        on = (e && e[0] == '0') ? 0 : 1;
+        g_fused = (e && e[0] == '0') ? 0 : 1;
     }
-    return on != 0;
+    return g_fused != 0;
+}
+
+int lrqk_set_fused(int on) {
+    const int prev = fused_enabled() ? 1 : 0;
+    g_fused = on ? 1 : 0;
+    return prev;
 }
 
 int lrqk_score_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream) {

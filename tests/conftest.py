@@ -23,3 +23,16 @@ def golden(name):
 @pytest.fixture(scope="session")
 def gold():
     return golden
+
+
+@pytest.fixture(params=["fused", "split"])
+def select_path(request):
+    """Run a decode test on both selection paths: the fused score/select/
+    attend kernel (lrqk_score_attend, the default) and the split one
+    (lrqk_score + lrqk_select_attend)."""
+    from paper_2510_23649_b200 import _lib
+
+    lib = _lib.lib()
+    prev = lib.lrqk_set_fused(1 if request.param == "fused" else 0)
+    yield request.param
+    lib.lrqk_set_fused(prev)

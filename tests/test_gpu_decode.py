@@ -74,7 +74,7 @@ def test_free_running_matches_reference_sessions(case):
     dict(B=2, Hq=4, Hkv=2, d=64, r=16, kb=40, lb=8, prompt=500, steps=6),
     dict(B=1, Hq=2, Hkv=1, d=24, r=6, kb=5, lb=3, prompt=40, steps=8),
 ])
-def test_step_locked_parity(dtype, cfg):
+def test_step_locked_parity(dtype, cfg, select_path):
     rng = np.random.default_rng(7)
     B, Hq, Hkv, d, r = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["r"]
     T = cfg["prompt"] + cfg["steps"]
@@ -158,7 +158,7 @@ def _select_exact_check(layer, t, kb, lb):
 
 
 @pytest.mark.parametrize("kind", ["gaussian", "ties", "constant"])
-def test_selection_exact_at_long_context(kind):
+def test_selection_exact_at_long_context(kind, select_path):
     """Contexts beyond 16K rows take the sampled-histogram path (coarse bins
     from a 1/s sample, exact fine histogram of the candidate band); heavy ties
     and constant scores exercise the verification / exact fallback."""
@@ -222,7 +222,7 @@ def test_selection_exact_with_prefill_factors(ctx):
         _select_exact_check(layer, t, kb, lb)
 
 
-def test_engine_matches_per_layer_steps():
+def test_engine_matches_per_layer_steps(select_path):
     """The multi-layer Engine (shared per-step scratch, all layers'
     compress_prepare in one batched launch, CUDA graph replay) must give
     exactly the results of stepping each layer on its own through
@@ -253,6 +253,7 @@ def test_engine_matches_per_layer_steps():
         eng.v_buf[..., :d].copy_(v)
         if step < 3:
             eng.decode_step()
+            assert eng.fused == (select_path == "fused")  # the path under test is the one that ran
         else:
             eng.replay()
         for i in range(nL):
@@ -267,7 +268,7 @@ def test_engine_matches_per_layer_steps():
 
 
 @pytest.mark.parametrize("r,kb", [(16, 256), (32, 1024), (64, 4096)])
-def test_rank_topk_sweep_selection_and_output(r, kb):
+def test_rank_topk_sweep_selection_and_output(r, kb, select_path):
     """SURVEY §8 C5 shapes (r in {16, 32, 64}, k in {256, 1024, 4096}) at a
     shortened context: every step's selection is the exact top-k of the GPU's
     own scores, and the output equals fp32 attention over that selection
@@ -306,7 +307,7 @@ def test_rank_topk_sweep_selection_and_output(r, kb):
             torch.testing.assert_close(out[0, h], w @ Vs, rtol=2e-2, atol=2e-3)
 
 
-def test_mixed_paths_in_one_step_keep_outputs_apart():
+def test_mixed_paths_in_one_step_keep_outputs_apart(select_path):
     """One head misses its threshold window (general select + attention
     kernels) while the others take the fused select_attend path in the same
     step: the two paths share attn_scratch and must use one slot stride, or
@@ -360,7 +361,7 @@ def test_mixed_paths_in_one_step_keep_outputs_apart():
 
 
 @pytest.mark.parametrize("r", [16, 32, 64])
-def test_fused_resident_reduction_matches_torch(r):
+def test_fused_resident_reduction_matches_torch(r, select_path):
     """The tensor-core Y = A_res^T K_res, G = A_res^T A_res that
     select_attend accumulates while it attends (plus the finish kernel's
     bin-D rows and slot sums) must equal a torch fp32 reduction over the

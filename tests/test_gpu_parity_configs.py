@@ -50,7 +50,7 @@ def _prefill_into(layer, Q, K, V, prompt, dtype):
 
 
 @pytest.mark.parametrize("driver", ["decode_step", "engine"])
-def test_c1_step_locked(driver):
+def test_c1_step_locked(driver, select_path):
     from paper_2510_23649_b200.engine import Engine, LayerShape
 
     prompt, steps = 4096, 32
@@ -89,7 +89,7 @@ def test_c1_step_locked(driver):
     assert log.rec["selections_identical"] >= 0.95 * steps * Hq
 
 
-def test_c4_shape_kv_group_128k_bf16():
+def test_c4_shape_kv_group_128k_bf16(select_path):
     torch.manual_seed(0)
     prompt, steps = 131072, 6
     Hq, Hkv, d, r, kb, lb = 4, 1, 128, 32, 2048, 16
