@@ -75,6 +75,9 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     p.add_argument("--batch-per-gpu", type=int, default=1)
+    p.add_argument("--global-batch", type=int, default=None,
+                   help="fixed job batch (strong scaling); fewer sequences than GPUs splits each sequence by KV-head "
+                        "blocks (shard.plan_shards). Default: batch-per-gpu x GPUs (weak scaling)")
     p.add_argument("--ctx", type=int, default=None)
     p.add_argument("--layers", type=int, default=None)
     p.add_argument("--rank", type=int, default=None)
@@ -108,18 +111,29 @@ def workload(args):
     return w
 
 
+def global_batch(args, world):
+    gb = getattr(args, "global_batch", None)
+    return gb if gb else args.batch_per_gpu * world
+
+
 def config_dict(args, world):
     """The `config` object of the JSON line; identical for both arms."""
     w = workload(args)
-    B = args.batch_per_gpu
+    GB = global_batch(args, world)
+    if world == 1:
+        par = "1 GPU"
+    elif GB % world == 0:
+        par = (f"batch-sharded over {world} GPUs ({GB // world} sequence(s) each), no collective inside the step; "
+               f"NCCL all-gather of last-layer outputs per step")
+    else:
+        par = (f"(sequence, KV-head block) shards over {world} GPUs ({world // GB} per sequence), no collective "
+               f"inside the step; NCCL all-gather of last-layer outputs per step")
     return dict(workload=w["desc"], ctx=w["ctx"], layers=w["layers"], n_q_heads=w["hq"], n_kv_heads=w["hkv"],
-                head_dim=w["d"], rank=w["r"], top_k=w["k"], lite=w["lite"], batch_per_gpu=B, global_batch=B * world,
-                slow_tier=args.policy, data=args.data,
-                parallelism=(f"batch-sharded over {world} GPU(s), no collective inside the step; NCCL all-gather of "
-                             f"last-layer outputs per step") if world > 1 else "1 GPU",
+                head_dim=w["d"], rank=w["r"], top_k=w["k"], lite=w["lite"], batch_per_gpu=GB // world if GB % world == 0 else GB / world,
+                global_batch=GB, slow_tier=args.policy, data=args.data, parallelism=par,
                 l2="no flush: each step streams %.1f GB (> 126 MB L2)" % (
-                    step_bytes(w, B, w["ctx"], w["k"] + w["lite"], 2 if w["dtype"] == "bf16" else 4)["total"]
-                    * w["layers"] / 1e9))
+                    step_bytes(w, GB, w["ctx"], w["k"] + w["lite"], 2 if w["dtype"] == "bf16" else 4)["total"]
+                    * w["layers"] / max(world, 1) / 1e9))
 
 
 # --------------------------------------------------------------------------
@@ -291,10 +305,18 @@ def run_ours(args, world, rank, local):
     from paper_2510_23649_b200 import _lib
     from paper_2510_23649_b200.engine import Engine, LayerShape, prefill_factorize_device
 
+    from paper_2510_23649_b200.shard import gather_outputs, plan_shards
+
     w = workload(args)
     dev = torch.device("cuda", local)
-    B = args.batch_per_gpu
-    L, Hq, Hkv, d, ctx, r, k, lite = w["layers"], w["hq"], w["hkv"], w["d"], w["ctx"], w["r"], w["k"], w["lite"]
+    GB = global_batch(args, world)
+    # this rank's (sequence, KV-head) block of the job: whole
+    # sequences when the GPUs divide the batch, else KV-head blocks
+    plan = plan_shards(GB, w["hq"], w["hkv"], world)
+    shard = plan[rank]
+    B = shard.batch
+    L, d, ctx, r, k, lite = w["layers"], w["d"], w["ctx"], w["r"], w["k"], w["lite"]
+    Hq, Hkv = shard.n_q_heads, shard.n_kv_heads
     extra_steps = args.warmup + args.steps + max(args.profile_steps, 0) + 64
     t_max = ctx + 2 * extra_steps
     shape = LayerShape(batch=B, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, rank=r, k_budget=k, lite_budget=lite,
@@ -367,11 +389,7 @@ def run_ours(args, world, rank, local):
     eng.capture()
     gather_buf = None
     if world > 1:
-        from paper_2510_23649_b200.shard import gather_outputs, plan_shards
-
-        plan = plan_shards(B * world, Hq, Hkv, world)
-        assert plan[rank].batch == B and plan[rank].n_q_heads == Hq
-        gather_buf = torch.empty(B * world, Hq, shape.dim_stride, device=dev)
+        gather_buf = torch.empty(GB, w["hq"], shape.dim_stride, device=dev)
 
     def one_step(i):
         load_inputs(i)
@@ -476,12 +494,45 @@ def run_ours(args, world, rank, local):
     eng.raise_status()
     score_ms = float(np.mean([a.elapsed_time(b_) for a, b_ in evs]))
 
+    # ---- the product's dominant kernel: fused score/select/attend ----------
+    # (the step's K3+K4+K6; timed per launch on its stream, as above)
+    fused_ms = None
+    if eng.fused:
+        evs = []
+        for i in range(n_prof):
+            load_inputs(step_i)
+            step_i += 1
+            for li, layer in enumerate(eng.layers):
+                q, kk, vv, out = eng.q_buf[li], eng.k_buf[li], eng.v_buf[li], eng.out_buf[li]
+                _lib.check(lib.lrqk_decode_compress(layer.ptr, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), 1, sp),
+                           "compress")
+                a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                _lib.check(lib.lrqk_score_attend(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "score_attend")
+                b_.record(stream)
+                evs.append((a, b_))
+                _lib.check(lib.lrqk_select(layer.ptr, sp), "select")
+                _lib.check(lib.lrqk_gather_misses(layer.ptr, sp), "gather")
+                _lib.check(lib.lrqk_attention(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "attention")
+            _lib.check(lib.lrqk_compress_prepare_layers(eng._dev_layers.data_ptr(), eng._host_layers, L, sp),
+                       "prepare")
+            _lib.check(lib.lrqk_advance(eng.ctx.data_ptr(), B, sp), "advance")
+        torch.cuda.synchronize()
+        eng.raise_status()
+        fused_ms = float(np.mean([a.elapsed_time(b_) for a, b_ in evs]))
+
+    # ---- fidelity of the last step (f1, outside every timed region) --------
+    rec, err = eng.fidelity()
+    fid = torch.stack([rec.mean(), err[torch.isfinite(err)].mean()]).double()
+
     # ---- aggregate over ranks ------------------------------------------------
     vals = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(fid, op=dist.ReduceOp.SUM)
+        fid /= world
     ms, e2e_ms = float(vals[0]), float(vals[1])
-    total_seq = B * world
+    total_seq = GB
     ms_per_step = ms / args.steps
     tok_s = total_seq * args.steps / (ms / 1e3)
     e2e_tok_s = total_seq * e2e_steps / (e2e_ms / 1e3)
@@ -489,7 +540,7 @@ def run_ours(args, world, rank, local):
     S = k + lite
     e = 2 if w["dtype"] == "bf16" else 4
     t_mid = t_now  # context during the profile steps
-    byt = step_bytes(w, B, t_mid, S, e)
+    byt = step_bytes(dict(w, hq=Hq), B, t_mid, S, e)
     score_bytes = B * Hq * (t_mid + 1) * (r * e + 4)  # A_K read + key write per launch
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -497,10 +548,30 @@ def run_ours(args, world, rank, local):
     score_gbs = score_bytes / (score_ms / 1e3) / 1e9
     traffic, traffic_src = _ncu_traffic(args.workload if args.policy == "hbm" else None, score_bytes)
     step_gbs = byt["total"] * L / (ms_per_step / 1e3) / 1e9
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"
+    k3 = dict(bound="hbm", kernel="score_tma_kernel (split path: proxy scores + window histogram)",
+              achieved=round(score_gbs, 1), peak=hbm_peak, unit="GB/s", frac=round(score_gbs / hbm_peak, 4),
+              traffic=traffic, traffic_source=traffic_src, algorithmic_bytes_per_launch=score_bytes,
+              avg_launch_ms=round(score_ms, 5), step_frac_of_hbm=round(step_gbs / hbm_peak, 4),
+              step_algorithmic_GBps=round(step_gbs, 1), peak_source=peak_src)
+    if fused_ms is not None:
+        # fused kernel: A_K read + keys write/read + the selected rows' K, V
+        # and proxy rows (SURVEY §8d terms a_k + scores + attn + the A half of resid)
+        sa_bytes = B * Hq * ((t_mid + 1) * (r * e + 8) + S * (2 * d + r) * e)
+        sa_gbs = sa_bytes / (fused_ms / 1e3) / 1e9
+        sa_traffic, sa_src = _ncu_traffic(f"{args.workload}:score_attend" if args.policy == "hbm" else None, sa_bytes)
+        roofline = dict(bound="hbm", kernel="score_attend_kernel (fused K3+K4+K6: proxy scores, top-k, attention)",
+                        achieved=round(sa_gbs, 1), peak=hbm_peak, unit="GB/s", frac=round(sa_gbs / hbm_peak, 4),
+                        traffic=sa_traffic, traffic_source=sa_src, algorithmic_bytes_per_launch=sa_bytes,
+                        avg_launch_ms=round(fused_ms, 5), step_frac_of_hbm=round(step_gbs / hbm_peak, 4),
+                        step_algorithmic_GBps=round(step_gbs, 1), peak_source=peak_src, split_path_score_kernel=k3)
+    else:
+        roofline = k3
     return dict(
         metric="decode tokens/s at 128K ctx (LLaMA-3-8B shape); proxy-score HBM GB/s",
         value=round(tok_s, 3), unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-        ms_per_step=round(ms_per_step, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
+        ms_per_step=round(ms_per_step, 4), higher_is_better=True,
+        scaling="strong" if args.global_batch else "weak", vs_baseline=None,
         dtype=w["dtype"],
         data={"random": "synthetic (random N(0,1) Q/K/V per layer; prompt factorised on GPU)",
               "recency": "synthetic recency-biased low-rank Q/K (reference gen_recency_biased structure, r_true=64, "
@@ -509,12 +580,7 @@ def run_ours(args, world, rank, local):
               "drift": "synthetic AR(1)-correlated queries (rho 0.9) over a rank-64 key subspace with the reference's "
                        "recency bias; decode rows continue the prompt; prompt factorised on GPU"}[args.data],
         config=config_dict(args, world),
-        roofline=dict(bound="hbm", kernel="score_kernel (proxy scores + radix histogram)",
-                      achieved=round(score_gbs, 1), peak=hbm_peak, unit="GB/s",
-                      frac=round(score_gbs / hbm_peak, 4), traffic=traffic, traffic_source=traffic_src,
-                      algorithmic_bytes_per_launch=score_bytes, avg_launch_ms=round(score_ms, 5),
-                      step_frac_of_hbm=round(step_gbs / hbm_peak, 4), step_algorithmic_GBps=round(step_gbs, 1),
-                      peak_source="MEASURED_PEAKS.json hbm_gbs (copy, burst)" if peaks else "fallback 6650"),
+        roofline=roofline,
         miss_transfers=dict(misses_per_step=round(misses / max(args.steps, 1), 1),
                             miss_rate=round(misses / max(selected, 1), 4),
                             bytes_per_step=int(miss_bytes / max(args.steps, 1)),
@@ -529,6 +595,10 @@ def run_ours(args, world, rank, local):
         prefill=dict(ms_total_gpu=round(prefill_ms, 2), heads=L * B * Hq, ctx=ctx, setup_s=round(setup_s, 2)),
         bytes_per_token_layer=byt,
         select_paths=sel_modes,
+        fidelity=dict(recall_mean=round(float(fid[0]), 5), output_err_mean=round(float(fid[1]), 6),
+                      heads=L * GB * w["hq"], step=t_now - 1,
+                      note="Engine.fidelity on the device after the timed steps: Omega_t vs the exact top-k of q K^T "
+                           "over the whole history, and output vs full-history attention (ref session.py:119-131)"),
     )
 
 
@@ -649,7 +719,7 @@ def run_reference(args, world, rank):
     sessions (one per process) after W untimed ones; tokens/s is then
     extrapolated to the whole job's head sessions (reported explicitly)."""
     w = workload(args)
-    total_seq = args.batch_per_gpu * world
+    total_seq = global_batch(args, world)
     if rank != 0:
         return None
     cores = os.cpu_count() or 1
@@ -661,8 +731,8 @@ def run_reference(args, world, rank):
     cfg = config_dict(args, world)
     return dict(metric="decode tokens/s at 128K ctx (LLaMA-3-8B shape); proxy-score HBM GB/s",
                 value=round(tok_s, 5), unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-                ms_per_step=round(1e3 * total_seq / tok_s, 3), higher_is_better=True, scaling="weak",
-                vs_baseline=None, dtype="f64", data="synthetic (random N(0,1) K/V/proxy rows per head session)",
+                ms_per_step=round(1e3 * total_seq / tok_s, 3), higher_is_better=True,
+                scaling="strong" if args.global_batch else "weak", vs_baseline=None, dtype="f64", data="synthetic (random N(0,1) K/V/proxy rows per head session)",
                 config=cfg, impl="reference",
                 cpu_baseline=dict(value=round(tok_s, 5), unit="tokens/s", cores=cores, kind="port",
                                   sample=f"{cores} processes x 1 head session, {args.warmup} warm + {args.steps} timed "

@@ -82,17 +82,47 @@ class LayerShape:
         return self.n_q_heads // self.n_kv_heads
 
 
-class HostTier:
-    """Mapped pinned host buffer (cudaHostAlloc) with a numpy view."""
+def numa_local_cpus(device) -> set | None:
+    """CPUs on the GPU's own NUMA node (sysfs local_cpulist of its PCIe
+    function), intersected with this process's affinity; None if unknown."""
+    try:
+        p = torch.cuda.get_device_properties(device)
+        bus = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as fh:
+            txt = fh.read().strip()
+        cpus = set()
+        for part in txt.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        return (cpus & os.sched_getaffinity(0)) or None
+    except Exception:
+        return None
 
-    def __init__(self, nbytes: int):
+
+class HostTier:
+    """Mapped pinned host buffer (cudaHostAlloc) with a numpy view.  With a
+    device, the pages are pinned from a thread bound to that GPU's NUMA node
+    (each GPU's pinned slow tier on its local socket), so the
+    zero-copy miss reads (K5b) do not cross the inter-socket link."""
+
+    def __init__(self, nbytes: int, device=None):
         lib = _lib.lib()
         self.nbytes = nbytes
-        self.ptr = lib.lrqk_host_alloc(nbytes)
+        self.numa_cpus = numa_local_cpus(device) if device is not None else None
+        saved = None
+        if self.numa_cpus:
+            saved = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, self.numa_cpus)
+        try:
+            self.ptr = lib.lrqk_host_alloc(nbytes)
+            if self.ptr:
+                C.memset(self.ptr, 0, nbytes)  # first touch from the bound thread too
+        finally:
+            if saved is not None:
+                os.sched_setaffinity(0, saved)
         if not self.ptr:
             raise MemoryError(f"lrqk_host_alloc({nbytes}) failed: {lib.lrqk_last_error().decode()}")
         self.dev_ptr = lib.lrqk_host_device_ptr(self.ptr)
-        C.memset(self.ptr, 0, nbytes)
 
     def as_tensor(self, dtype, shape):
         buf = (C.c_uint8 * self.nbytes).from_address(self.ptr)
@@ -146,7 +176,7 @@ class LayerState:
             elif name == "ctx_len" and ctx_len is not None:
                 t = ctx_len
             elif name in ("slow_k", "slow_v") and shape.policy == "host":
-                ht = HostTier(max(nb, 16))
+                ht = HostTier(max(nb, 16), device=self.device)
                 self.host_tiers[name] = ht
                 setattr(s, name, ht.dev_ptr)
                 continue
@@ -502,6 +532,63 @@ class Engine:
             self.capture()
         self.graph.replay()
         return self.out_buf
+
+    def fidelity(self, q=None, out=None):
+        """Fidelity of the last decode step for every (layer, sequence,
+        q-head), on the device (ref: session.py:119-131, attention.py:37-50):
+        recall of the step's Omega_t against the exact top-k of q K^T over
+        the whole key history (exact_topk -> selection_recall), and
+        ||out - full|| / ||full|| against full-history attention.  The exact
+        top-k runs through the library's selection kernel (lrqk_select_scores
+        over the scores plus one -inf lite row: plain top-k, ties toward the
+        lower index); the
+        q K^T product and the full softmax attention are cuBLAS / torch
+        device ops.  Returns (recall, output_err) as [L, B, Hq] float32
+        device tensors: no key history crosses to the host."""
+        from .api import _select_device  # the device selection wrapper
+
+        sh = self.shape
+        q = self.q_buf if q is None else q
+        out = self.out_buf if out is None else out
+        L, B, Hq, Hkv, d = self.n_layers, sh.batch, sh.n_q_heads, sh.n_kv_heads, sh.head_dim
+        G = Hq // Hkv
+        recall = torch.zeros(L, B, Hq, dtype=torch.float32, device=self.device)
+        err = torch.zeros_like(recall)
+        ctx = self.ctx.cpu().tolist()  # rows of history per sequence (one int each)
+        S = sh.k_budget + sh.lite_budget
+        for i, layer in enumerate(self.layers):
+            for b in range(B):
+                n = int(ctx[b])  # the last step appended row n - 1
+                if n < 1:
+                    continue
+                k_eff = min(sh.k_budget, n)
+                K = layer.view("slow_k")[b, :, :n, :d]
+                V = layer.view("slow_v")[b, :, :n, :d]
+                qb = q[i, b, :, :d].reshape(Hkv, G, d)
+                if K.dtype == torch.float32:
+                    sc = torch.matmul(qb.float(), K.transpose(1, 2))  # [Hkv, G, n] fp32
+                else:
+                    sc = torch.matmul(qb.to(K.dtype), K.transpose(1, 2)).float()
+                sc = sc.reshape(Hq, n)
+                # plain top-k through select_active: one -inf row appended as
+                # the (single-row) lite window, so Omega_k is the top k of
+                # the n real rows
+                ext = torch.cat([sc, torch.full((Hq, 1), -math.inf, device=self.device)], dim=1).contiguous()
+                omega, _ = _select_device(ext, n, k_eff, 1)
+                mark = torch.zeros(Hq, n, dtype=torch.bool, device=self.device)
+                mark.scatter_(1, omega[:, :k_eff].long(), True)
+                sel = layer.view("res_idx")[b].long().clamp(0, n - 1)
+                cnt = layer.view("res_cnt")[b].long()
+                valid = torch.arange(S, device=self.device)[None, :] < cnt[:, None]
+                hits = (mark.gather(1, sel) & valid).sum(1)
+                recall[i, b] = hits.float() / k_eff
+                w = torch.softmax(sc / math.sqrt(d), dim=1).reshape(Hkv, G, n)
+                full = torch.matmul(w, V.float()).reshape(Hq, d)
+                diff = torch.linalg.vector_norm(out[i, b, :, :d].float() - full, dim=1)
+                den = torch.linalg.vector_norm(full, dim=1)
+                err[i, b] = torch.where(den > 0, diff / den.clamp_min(1e-38),
+                                        torch.where(diff == 0, torch.zeros_like(diff), torch.full_like(diff, math.inf)))
+        return recall, err
 
     def counters(self):
         cm = torch.stack([l.view("c_miss") for l in self.layers])

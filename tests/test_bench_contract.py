@@ -57,3 +57,19 @@ def test_reference_arm_config_matches_ours():
     for key in ("workload", "ctx", "layers", "n_q_heads", "n_kv_heads", "head_dim", "rank", "top_k", "lite",
                 "global_batch", "slow_tier", "parallelism"):
         assert key in c
+
+
+def test_global_batch_config_and_kv_head_split():
+    """--global-batch fixes the job (strong scaling); with fewer sequences
+    than GPUs the plan splits each sequence by KV-head blocks."""
+    from paper_2510_23649_b200.shard import plan_shards
+
+    a = bench.argparse.Namespace(workload="c4", ctx=None, layers=None, rank=None, topk=None, batch_per_gpu=1,
+                                 global_batch=None, policy="hbm", data="random")
+    assert bench.global_batch(a, 8) == 8 and bench.config_dict(a, 8)["batch_per_gpu"] == 1
+    a.global_batch = 1
+    c = bench.config_dict(a, 2)
+    assert c["global_batch"] == 1 and c["batch_per_gpu"] == 0.5 and "KV-head" in c["parallelism"]
+    plan = plan_shards(1, 32, 8, 2)
+    assert [(s.b0, s.b1, s.g0, s.g1) for s in plan] == [(0, 1, 0, 4), (0, 1, 4, 8)]
+    assert all(s.n_q_heads == 16 for s in plan)
