@@ -486,7 +486,6 @@ def run_ours(args, world, rank, local):
             evs.append((a, b_))
             _lib.check(lib.lrqk_select_attend(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "select_attend")
             _lib.check(lib.lrqk_select(layer.ptr, sp), "select")
-            _lib.check(lib.lrqk_gather_misses(layer.ptr, sp), "gather")
             _lib.check(lib.lrqk_attention(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "attention")
         _lib.check(lib.lrqk_compress_prepare_layers(eng._dev_layers.data_ptr(), eng._host_layers, L, sp), "prepare")
         _lib.check(lib.lrqk_advance(eng.ctx.data_ptr(), B, sp), "advance")
@@ -512,7 +511,6 @@ def run_ours(args, world, rank, local):
                 b_.record(stream)
                 evs.append((a, b_))
                 _lib.check(lib.lrqk_select(layer.ptr, sp), "select")
-                _lib.check(lib.lrqk_gather_misses(layer.ptr, sp), "gather")
                 _lib.check(lib.lrqk_attention(layer.ptr, q.data_ptr(), out.data_ptr(), sp), "attention")
             _lib.check(lib.lrqk_compress_prepare_layers(eng._dev_layers.data_ptr(), eng._host_layers, L, sp),
                        "prepare")

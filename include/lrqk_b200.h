@@ -191,7 +191,11 @@ int lrqk_score_attend(const lrqk_layer_t *L, const void *q, float *out, void *st
 int lrqk_set_fused(int on);
 
 /* Host policy: copy this step's missed K/V rows from the pinned host slow
- * tier into their slots (zero-copy PCIe reads).  ref: cache.py:193-194. */
+ * tier into their slots (zero-copy PCIe reads) as a pass of its own.
+ * Optional: lrqk_attention fetches the misses lrqk_select marked (slot bit
+ * 30) itself, overlapped with the hit rows, and lrqk_decode_step relies on
+ * that; after this call lrqk_attention reads every row from its slot.
+ * ref: cache.py:193-194. */
 int lrqk_gather_misses(const lrqk_layer_t *L, void *stream);
 
 /* Exact softmax attention over the selected rows; out [B,Hq,dim_stride] f32.

@@ -121,9 +121,25 @@ attention_kernel(const AttnArgs a) {
         for (int e = 0; e < N; ++e) acc[pp][e] = 0.f;
     const int r0 = split * kAttnRows, r1 = min(S, r0 + kAttnRows);
     const int step = NW * RPW;
-    // the split's row offsets, staged once (one dependent round trip)
+    // the split's row offsets, staged once (one dependent round trip).  Host
+    // policy: rows missed this step (slot | kSlotMiss) are read from the
+    // pinned host tier here, zero-copy over PCIe, in the same loads as the
+    // hits' HBM slot rows (K5b overlapped with the hits), then stored into
+    // their slots; s_tok holds their token index (-1: a hit)
     __shared__ int s_src[kAttnRows];
-    for (int j = tid; j < r1 - r0; j += blockDim.x) s_src[j] = src[r0 + j];
+    __shared__ int s_tok[kAttnRows];
+    const T *hk = nullptr, *hv = nullptr;
+    if (host) {
+        const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
+        hk = reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
+        hv = reinterpret_cast<const T *>(L.slow_v) + kv_rows * d;
+    }
+    for (int j = tid; j < r1 - r0; j += blockDim.x) {
+        const int sv = src[r0 + j];
+        s_src[j] = sv & ~kSlotMiss;
+        s_tok[j] = (host && (sv & kSlotMiss)) ? L.res_idx[(size_t)bh * L.s_cap + r0 + j] : -1;
+        if (s_tok[j] >= 0) L.res_slot[(size_t)bh * L.s_cap + r0 + j] = sv & ~kSlotMiss;  // fetched below
+    }
     __syncthreads();
     // scores of U rows per lane group in flight, K and V kept packed until used
     for (int base = r0 + warp * RPW + sub; base < r1 + sub; base += step * U) {
@@ -132,15 +148,31 @@ attention_kernel(const AttnArgs a) {
         for (int u = 0; u < U; ++u) {
             const int j = base + u * step;
             if (j < r1) {
-                const size_t row = (size_t)s_src[j - r0] * d;
+                const int tok = s_tok[j - r0];
+                const T *kr = tok >= 0 ? hk + (size_t)tok * d : kb + (size_t)s_src[j - r0] * d;
+                const T *vr = tok >= 0 ? hv + (size_t)tok * d : vb + (size_t)s_src[j - r0] * d;
 #pragma unroll
                 for (int pp = 0; pp < PPL; ++pp) {
-                    kx[u][pp] = *reinterpret_cast<const uint4 *>(kb + row + (sl + pp * LPR) * N);
-                    vx[u][pp] = *reinterpret_cast<const uint4 *>(vb + row + (sl + pp * LPR) * N);
+                    kx[u][pp] = *reinterpret_cast<const uint4 *>(kr + (sl + pp * LPR) * N);
+                    vx[u][pp] = *reinterpret_cast<const uint4 *>(vr + (sl + pp * LPR) * N);
                 }
             } else {
 #pragma unroll
                 for (int pp = 0; pp < PPL; ++pp) { kx[u][pp] = make_uint4(0, 0, 0, 0); vx[u][pp] = make_uint4(0, 0, 0, 0); }
+            }
+        }
+        if (host) {  // this step's misses -> their fast-tier slots
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = base + u * step;
+                if (j < r1 && s_tok[j - r0] >= 0) {
+                    const size_t row = (size_t)s_src[j - r0] * d;
+#pragma unroll
+                    for (int pp = 0; pp < PPL; ++pp) {
+                        *reinterpret_cast<uint4 *>(const_cast<T *>(kb) + row + (sl + pp * LPR) * N) = kx[u][pp];
+                        *reinterpret_cast<uint4 *>(const_cast<T *>(vb) + row + (sl + pp * LPR) * N) = vx[u][pp];
+                    }
+                }
             }
         }
         float x[U];
@@ -316,6 +348,9 @@ gather_misses_kernel(const lrqk_layer_t L) {
     const int *mi = L.miss_idx + (size_t)bh * L.s_cap;
     const int *ms = L.miss_slot + (size_t)bh * L.s_cap;
     const int total = n * packs;
+    if (blockIdx.x == 0)  // the rows are in their slots after this kernel: plain slot indices
+        for (int i = threadIdx.x; i < L.res_cnt[bh]; i += blockDim.x)
+            L.res_slot[(size_t)bh * L.s_cap + i] &= ~kSlotMiss;
     constexpr int U = 4;
     for (int e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < total; e0 += gridDim.x * blockDim.x * U) {
         uint4 kx[U], vx[U];

@@ -275,7 +275,7 @@ int lrqk_decode_step(const lrqk_layer_t *L, const void *q, const void *k, const 
         return rc;
     }
     if ((rc = check(launch_select(*L, st)))) return rc;
-    if ((rc = check(launch_gather(*L, st)))) return rc;
+    // host policy: the attention kernel fetches this step's misses itself (K5b fused)
     if ((rc = check(launch_attention(*L, q, out, st)))) return rc;
     if ((rc = check(launch_prepare(*L, st)))) return rc;
     if (advance) rc = check(launch_advance(L->ctx_len, L->batch, st));

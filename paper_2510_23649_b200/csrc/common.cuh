@@ -51,6 +51,11 @@ enum Meta : int {
     M_HINT_QN = 46,    // persistent: |q_hat| (f32 bits) of the step that set M_HINT
 };
 constexpr int kPrevCrit = 8;
+// Host policy: select_kernel marks the fast-tier slots of this step's misses
+// in res_slot with this bit; the attention kernel reads those rows straight
+// from the pinned host tier (zero-copy), stores them into their slots and
+// clears the bit (lrqk_gather_misses does the same copy as a separate pass).
+constexpr int kSlotMiss = 1 << 30;
 
 // attention partial slots per head (attention splits, or select_attend parts)
 // attention partial slots per head: attention splits, or select_attend's

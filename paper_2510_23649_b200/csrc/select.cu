@@ -759,7 +759,7 @@ select_kernel(const lrqk_layer_t L, int parts) {
             for (int j = tid; j < mtot; j += nt) {
                 const int i = miss_pos[j];
                 const int s = free_list[j];
-                news[i] = s;
+                news[i] = s | kSlotMiss;  // fetched by attention_kernel (or lrqk_gather_misses)
                 mi[j] = newl[i];
                 ms[j] = s;
             }

@@ -476,10 +476,11 @@ class Engine:
 
     def launches_per_step(self):
         """Kernels one decode step launches: per layer compress,
-        score_attend (or score + select_attend), select, [gather], attention;
+        score_attend (or score + select_attend), select, attention (which
+        also fetches the host tier's misses);
         then the batched compress_prepare (two kernels for bf16) and the ctx
         advance."""
-        per = 4 if self.fused else 5
+        per = 4 if (self.fused or self.shape.policy == "host") else 5
         prep = 2 if self.shape.dtype == "bf16" else self.n_layers
         return self.n_layers * per + prep + 1
 
@@ -508,7 +509,6 @@ class Engine:
             else:
                 _lib.check(rc, "lrqk_score_attend")
             _lib.check(lib.lrqk_select(lp, sp), "lrqk_select")
-            _lib.check(lib.lrqk_gather_misses(lp, sp), "lrqk_gather_misses")
             _lib.check(lib.lrqk_attention(lp, q[i].data_ptr(), out[i].data_ptr(), sp), "lrqk_attention")
         _lib.check(lib.lrqk_compress_prepare_layers(self._dev_layers.data_ptr(), self._host_layers, self.n_layers, sp),
                    "lrqk_compress_prepare_layers")
@@ -564,6 +564,8 @@ class Engine:
                 k_eff = min(sh.k_budget, n)
                 K = layer.view("slow_k")[b, :, :n, :d]
                 V = layer.view("slow_v")[b, :, :n, :d]
+                if not K.is_cuda:  # host slow tier: the history lives in pinned host memory
+                    K, V = K.to(self.device), V.to(self.device)
                 qb = q[i, b, :, :d].reshape(Hkv, G, d)
                 if K.dtype == torch.float32:
                     sc = torch.matmul(qb.float(), K.transpose(1, 2))  # [Hkv, G, n] fp32
