@@ -122,7 +122,12 @@ LRQK_DEV void score_stream(const lrqk_layer_t &L, int bh, int tile0, int tile1, 
         if (lane == 0) {
             for (int it = it0; it < n_stage_iters; ++it) {  // stages before it0: score_prefetch_stages
                 const int s2 = it % SS::kStages;
-                if (it >= SS::kStages) mbar_wait(empty + s2, ((it / SS::kStages) - 1) & 1);
+                if (it >= SS::kStages) {
+                    mbar_wait(empty + s2, ((it / SS::kStages) - 1) & 1);
+                    // the consumers' generic-proxy reads of this stage, observed through
+                    // the empty barrier, before the async-proxy (TMA) overwrite
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
                 const int nt = min(kCW, tile1 - tile0 - it * kCW);
                 const uint32_t bytes = (uint32_t)nt * SS::kTileBytes;
                 mbar_expect_tx(full + s2, bytes);
