@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define LRQK_ABI_VERSION 1
+#define LRQK_ABI_VERSION 2
 
 /* storage dtypes */
 #define LRQK_F32 0
@@ -119,6 +119,12 @@ typedef struct lrqk_layer {
 
     /* ---- per-step scratch: rows whose score key clears the candidate bound ---- */
     uint32_t *cmask;               /* [B,Hq,ceil(t_max/32)] one bit per row (lrqk_score)          */
+
+    /* ---- persistent: row-major copy of the proxy store (optional, may be NULL) ---- */
+    void *proxy_rowmajor;          /* [B,Hq,t_max,rank_stride] dtype: the same A_K rows, one contiguous */
+                                   /* rank_stride run per row, kept by lrqk_decode_compress's append;   */
+                                   /* the selected rows' gathers read it (one 64-byte run per row      */
+                                   /* at r=32 bf16 instead of rank_stride/8 scattered 16-byte packs)   */
 } lrqk_layer_t;
 
 /* Sizes (bytes) of every buffer in lrqk_layer_t for the given configuration,

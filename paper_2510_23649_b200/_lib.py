@@ -34,7 +34,7 @@ BUFFER_NAMES = ("proxy", "B_Q", "B_K", "slow_k", "slow_v", "slot_k", "slot_v", "
                 "res_slot", "res_cnt", "spare_slot", "miss_idx", "miss_slot", "miss_cnt", "c_miss",
                 "c_total", "step_miss", "step_total", "q_hat", "k_hat", "eta", "keys", "hist",
                 "sel_meta", "sure_idx", "cand", "red_scratch", "attn_scratch", "counters", "status", "pre",
-                "fcand", "fcnt", "res_bits", "cmask")
+                "fcand", "fcnt", "res_bits", "cmask", "proxy_rowmajor")
 
 
 class LayerStruct(C.Structure):

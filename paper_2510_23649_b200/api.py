@@ -887,6 +887,8 @@ class DecodeSession:
         new.view("slow_v")[:, :, :t].copy_(old.view("slow_v")[:, :, :t])
         tl = (t + 31) // 32
         new.proxy_tiles()[:, :, :tl].copy_(old.proxy_tiles()[:, :, :tl])
+        if old.shape.row_mirror:
+            new.view("proxy_rowmajor")[:, :, :t].copy_(old.view("proxy_rowmajor")[:, :, :t])
         new.buf["pre"].copy_(old.buf["pre"])
         self._layer = new
 

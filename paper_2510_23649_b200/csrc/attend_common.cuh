@@ -89,7 +89,8 @@ __device__ void attend_list(const T *kb, const T *vb, const int *rows, int n, co
 // compression needs over Omega_t (compress.cu K2p), so compress_prepare
 // does not gather these rows again.
 template <typename T, int LPR, int PPL, int YGM, int CR = kMmaRows, int NS = 2>
-__device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *vb, const T *proxy, const int *rows,
+__device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *vb, const T *proxy, const T *arows,
+                                   const int *rows,
                                    int n, const float (&qv)[PPL][Pack<T>::N], float c, float &m, float &l,
                                    float (&acc)[PPL][Pack<T>::N], uint8_t *stage,
                                    float (&yacc)[YGM > 0 ? YGM : 1][2][4],
@@ -126,7 +127,9 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
             for (int e = tid; e < CR * PA; e += blockDim.x) {
                 const int j = e / PA, pk = e % PA;
                 uint8_t *da = aS + j * lda + pk * 16;
-                if (j < nr) cp_async16(da, proxy + proxy_pack_offset(rows[r0 + j], pk, PA) * 8);
+                if (j < nr)  // the row-major copy when the layer keeps one: one contiguous run per row
+                    cp_async16(da, arows ? arows + (size_t)rows[r0 + j] * (PA * 8) + pk * 8
+                                         : proxy + proxy_pack_offset(rows[r0 + j], pk, PA) * 8);
                 else *reinterpret_cast<uint4 *>(da) = make_uint4(0, 0, 0, 0);
             }
         } else {

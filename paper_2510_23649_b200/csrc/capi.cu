@@ -111,7 +111,7 @@ const char *lrqk_last_error(void) { return g_err; }
 const char *lrqk_buffer_names(void) {
     return "proxy,B_Q,B_K,slow_k,slow_v,slot_k,slot_v,ctx_len,res_idx,res_slot,res_cnt,spare_slot,miss_idx,"
            "miss_slot,miss_cnt,c_miss,c_total,step_miss,step_total,q_hat,k_hat,eta,keys,hist,sel_meta,sure_idx,"
-           "cand,red_scratch,attn_scratch,counters,status,pre,fcand,fcnt,res_bits,cmask";
+           "cand,red_scratch,attn_scratch,counters,status,pre,fcand,fcnt,res_bits,cmask,proxy_rowmajor";
 }
 
 int lrqk_red_chunks(const lrqk_layer_t *L) { return compress_chunks(*L); }
@@ -161,6 +161,7 @@ int lrqk_layer_buffer_bytes(const lrqk_layer_t *L, size_t *out, int max_out) {
         (size_t)score_part_rows(*L) * 4,                // fcnt
         BH * (size_t)((L->t_max + 31) / 32) * 4,        // res_bits
         BH * (size_t)((L->t_max + 31) / 32) * 4,        // cmask
+        BH * T * R * e,                                 // proxy_rowmajor
     };
     const int n = (int)(sizeof v / sizeof v[0]);
     for (int i = 0; i < n && i < max_out; ++i) out[i] = v[i];

@@ -49,6 +49,7 @@ enum Meta : int {
     M_KC = 44,         // this step's candidate bound (key) of cmask; 0xFFFFFFFF: no mask
     M_YG_FOLD = 45,    // attention_kernel already summed the M_YG slots into slot 0
     M_HINT_QN = 46,    // persistent: |q_hat| (f32 bits) of the step that set M_HINT
+    M_QN = 47,         // |q_hat| (f32 bits) of this step, written by compress
 };
 constexpr int kPrevCrit = 8;
 // Host policy: select_kernel marks the fast-tier slots of this step's misses

@@ -1533,6 +1533,12 @@ compress_kernel(const CompressArgs args) {
         L.q_hat[(size_t)bh * R + i] = qh[i];
         L.k_hat[(size_t)bh * R + i] = kh[i];
     }
+    if (warp == 0) {  // |q_hat|: the selection scales its threshold hint by it (select_common.cuh)
+        float a = 0.f;
+        for (int i = lane; i < R; i += 32) a = fmaf(qh[i], qh[i], a);
+        a = warp_sum(a);
+        if (lane == 0) L.sel_meta[(size_t)bh * kMetaInts + M_QN] = __float_as_int(sqrtf(a));
+    }
     if (tid == 0 && !(args.update_b && args.defer_b)) {
         L.eta[(size_t)bh * 2 + 0] = s_scalar[2];
         L.eta[(size_t)bh * 2 + 1] = s_scalar[3];
@@ -1543,6 +1549,10 @@ compress_kernel(const CompressArgs args) {
         T *base = reinterpret_cast<T *>(L.proxy) + head_rows * R;
         for (int i = tid; i < R; i += blockDim.x)
             base[proxy_pack_offset(t, i / N, apacks) * N + (i % N)] = from_float<T>(kh[i]);
+        if (L.proxy_rowmajor) {  // and to its row-major copy (the gathers read that one)
+            T *rm = reinterpret_cast<T *>(L.proxy_rowmajor) + (head_rows + t) * R;
+            for (int i = tid; i < R; i += blockDim.x) rm[i] = from_float<T>(kh[i]);
+        }
     }
     if (h % G == 0) {  // append k, v once per KV head (cache.py:209-210)
         T *dk = reinterpret_cast<T *>(L.slow_k) + (kv_rows + t) * d;

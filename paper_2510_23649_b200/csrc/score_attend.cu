@@ -190,6 +190,8 @@ score_attend_kernel(const SAArgs a) {
     const T *kb = reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
     const T *vb = reinterpret_cast<const T *>(L.slow_v) + kv_rows * d;
     const T *proxy = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
+    const T *arows = L.proxy_rowmajor ? reinterpret_cast<const T *>(L.proxy_rowmajor) + (size_t)bh * L.t_max * R
+                                      : nullptr;
     uint32_t wv[4];
     {
         const uint32_t *cmw = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5) + w0;
@@ -464,7 +466,7 @@ score_attend_kernel(const SAArgs a) {
     for (int i = 0; i < MT * 8; ++i) yacc[i / 8][(i / 4) & 1][i & 3] = 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) gacc[i / 4][i & 3] = 0.f;
-    if (ok) attend_reduce_list<T, LPR, PPL, YGM, CR, NS>(L, kb, vb, proxy, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc,
+    if (ok) attend_reduce_list<T, LPR, PPL, YGM, CR, NS>(L, kb, vb, proxy, arows, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc,
                                                       stage, yacc, gacc);
     trace(52);
     const size_t PF = yg_part_floats(R, d);

@@ -102,6 +102,8 @@ select_attend_kernel(const FArgs a) {
     const T *kb = reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
     const T *vb = reinterpret_cast<const T *>(L.slow_v) + kv_rows * d;
     const T *proxy = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
+    const T *arows = L.proxy_rowmajor ? reinterpret_cast<const T *>(L.proxy_rowmajor) + (size_t)bh * L.t_max * R
+                                      : nullptr;
     const float c = 1.4426950408889634f * rsqrtf((float)L.head_dim);  // log2(e) / sqrt(d)
     const size_t PF = yg_part_floats(R, d);
     float *yg = L.red_scratch + (size_t)bh * a.yg_slots * PF;
@@ -236,7 +238,7 @@ select_attend_kernel(const FArgs a) {
     }
     __syncthreads();
     trace(56);
-    attend_reduce_list<T, LPR, PPL, YGM>(L, kb, vb, proxy, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc, stage, yacc,
+    attend_reduce_list<T, LPR, PPL, YGM>(L, kb, vb, proxy, arows, s_rows, min(nloc, L.s_cap), qv, c, m, l, acc, stage, yacc,
                                         gacc);
     trace(52);
     if constexpr (YG) mma_write_partial<MT, 2>(yacc, gacc, R, d, yg + (size_t)part * PF);
@@ -319,7 +321,7 @@ select_attend_kernel(const FArgs a) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) gacc[i / 4][i & 3] = 0.f;
     if (nwin > kMmaRows) {
-        attend_reduce_list<T, LPR, PPL, YGM>(L, kb, vb, proxy, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
+        attend_reduce_list<T, LPR, PPL, YGM>(L, kb, vb, proxy, arows, s_list, nwin, qv, c, m, l, acc, stage, yacc, gacc);
         if constexpr (YG) mma_write_partial<MT, 2>(yacc, gacc, R, d, yg + (size_t)P * PF);
     } else {
         // a handful of rows: attention from registers; Y, G on the CUDA cores

@@ -31,13 +31,11 @@ LRQK_DEV uint64_t make_comp(uint32_t key, int idx) {
 }
 LRQK_DEV int comp_index(uint64_t c) { return (int)(kIdxMax - (uint32_t)(c & kIdxMax)); }
 
-// |q_hat| of head bh this step (the hint's scale reference)
+// |q_hat| of head bh this step (the hint's scale reference), as compress
+// left it in sel_meta; 0 when no compress ran (standalone selection)
 LRQK_DEV float qhat_norm(const lrqk_layer_t &L, int bh) {
-    if (L.q_hat == nullptr) return 0.f;  // standalone selection (lrqk_select_scores): no q_hat
-    const float *qh = L.q_hat + (size_t)bh * L.rank_stride;
-    float a = 0.f;
-    for (int e = 0; e < L.rank_stride; ++e) a = fmaf(qh[e], qh[e], a);
-    return sqrtf(a);
+    if (L.q_hat == nullptr) return 0.f;
+    return __int_as_float(L.sel_meta[(size_t)bh * kMetaInts + M_QN]);
 }
 
 // This step's threshold hint: the previous step's k-th largest score, scaled

@@ -64,6 +64,7 @@ class LayerShape:
     t_max: int
     dtype: str = "bf16"      # storage dtype of proxy rows and K/V rows
     policy: str = "hbm"      # "hbm" | "host"  (slow-tier placement)
+    row_mirror: bool = True  # keep the row-major proxy copy the gathers read (+ t_max*rank*e per head)
 
     def __post_init__(self):
         # stores are tiled in 32-row groups (proxy layout, common.cuh)
@@ -175,6 +176,9 @@ class LayerState:
                     raise ValueError(f"shared buffer {name} too small")
             elif name == "ctx_len" and ctx_len is not None:
                 t = ctx_len
+            elif name == "proxy_rowmajor" and not shape.row_mirror:
+                setattr(s, name, None)  # gathers read the tiled store
+                continue
             elif name in ("slow_k", "slow_v") and shape.policy == "host":
                 ht = HostTier(max(nb, 16), device=self.device)
                 self.host_tiers[name] = ht
@@ -224,6 +228,7 @@ class LayerState:
             "status": (torch.int32, (1,)),
             "res_bits": (torch.int32, (B, Hq, (T + 31) // 32)),
             "sel_meta": (torch.int32, (B, Hq, 48)),
+            "proxy_rowmajor": (self.sdt, (B, Hq, T, rs)),
         }[name]
         dt, shp = spec
         if name in self.host_tiers:
@@ -295,6 +300,8 @@ class LayerState:
         rows = A_K.new_zeros(sh.batch, sh.n_q_heads, tl * 32, sh.rank_stride)
         rows[:, :, :l, : A_K.shape[-1]] = A_K
         self.proxy_tiles()[:, :, :tl].copy_(to_tiles(rows.to(self.sdt), self.pack_elems))
+        if self.shape.row_mirror:
+            self.view("proxy_rowmajor")[:, :, :l].copy_(rows[:, :, :l].to(self.sdt))
         self.view("B_Q")[:, :, : B_Q.shape[2], : B_Q.shape[3]].copy_(B_Q)
         self.view("B_K")[:, :, : B_K.shape[2], : B_K.shape[3]].copy_(B_K)
         sk, sv = self.view("slow_k"), self.view("slow_v")

@@ -34,7 +34,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_binding_matches_header_layout():
     lib = _lib.load_library()
-    assert lib.lrqk_abi_version() == 1
+    assert lib.lrqk_abi_version() == 2
     assert lib.lrqk_sizeof_layer() == ctypes.sizeof(_lib.LayerStruct)
     assert lib.lrqk_sizeof_prefill() == ctypes.sizeof(_lib.PrefillStruct)
     assert set(_lib.SIGNATURES) >= set(declared_functions())

@@ -408,3 +408,39 @@ def test_fused_resident_reduction_matches_torch(r, select_path):
             P = pre[base + offP: base + offP + R * R].view(R, R)
             torch.testing.assert_close(W - BQ[h], Y, rtol=1e-4, atol=1e-3 * Y.abs().max().item())
             torch.testing.assert_close(P - BQ[h] @ BQ[h].T, G, rtol=1e-4, atol=1e-3 * G.abs().max().item())
+
+
+def test_row_mirror_matches_tiled_gathers(select_path):
+    """The selected rows' proxy gathers read the row-major copy of the
+    proxy store (LayerShape.row_mirror, the default) or the tiled store
+    itself: the same values, so every output and every factor is identical."""
+    from paper_2510_23649_b200.engine import LayerShape, LayerState
+
+    torch.manual_seed(11)
+    B, Hq, Hkv, d, r, kb, lb, l = 1, 4, 2, 128, 32, 128, 16, 9000
+    layers = [LayerState(LayerShape(batch=B, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, rank=r, k_budget=kb,
+                                    lite_budget=lb, t_max=l + 16, dtype="bf16", row_mirror=m)) for m in (True, False)]
+    assert layers[1].struct.proxy_rowmajor is None
+    AK = torch.randn(B, Hq, l, r, device="cuda")
+    BQ = torch.randn(B, Hq, r, d, device="cuda") / d ** 0.5
+    BK = torch.randn(B, Hq, r, d, device="cuda") / d ** 0.5
+    K = torch.randn(B, Hkv, l, d, device="cuda").bfloat16()
+    V = torch.randn(B, Hkv, l, d, device="cuda").bfloat16()
+    for L in layers:
+        L.load_prompt(AK, BQ, BK, K, V)
+    outs = [torch.zeros(B, Hq, d, device="cuda") for _ in layers]
+    for step in range(6):
+        q = torch.randn(B, Hq, d, device="cuda").bfloat16()
+        k = torch.randn(B, Hkv, d, device="cuda").bfloat16()
+        v = torch.randn(B, Hkv, d, device="cuda").bfloat16()
+        for L, o in zip(layers, outs):
+            L.step(q, k, v, o)
+        torch.cuda.synchronize()
+        for L in layers:
+            L.raise_status()
+        assert torch.equal(outs[0], outs[1]), step
+        for name in ("res_cnt", "B_Q", "B_K", "q_hat", "k_hat"):
+            assert torch.equal(layers[0].view(name), layers[1].view(name)), (name, step)
+    n = l + 6
+    tiled = layers[0].proxy_rows()[:, :, :n, :r]
+    assert torch.equal(layers[0].view("proxy_rowmajor")[:, :, :n, :r], tiled)  # the copy tracks the appends

@@ -20,7 +20,7 @@ using T = __nv_bfloat16;
 
 constexpr int kThr = 288;
 
-template <int CR, int NS, int MODE>
+template <int CR, int NS, int MODE, bool AROW = false, int YGM = 2>
 __global__ void __maxnreg__(96) bench_kernel(lrqk_layer_t L, const int *rows_all, const int *nrows, int cap,
                                                     const T *q, float *parts, long long *clk) {
     extern __shared__ __align__(128) uint8_t smem[];
@@ -38,10 +38,11 @@ __global__ void __maxnreg__(96) bench_kernel(lrqk_layer_t L, const int *rows_all
     float qv[1][8];
     Pack<T>::load(q + (size_t)h * 128 + sl * 8, qv[0]);
     float m = -INFINITY, l = 0.f, acc[1][8] = {};
-    float yacc[2][2][4] = {}, gacc[4][4] = {};
+    float yacc[YGM > 0 ? YGM : 1][2][4] = {}, gacc[4][4] = {};
     const float c = 1.4426950408889634f * rsqrtf(128.f);
     if constexpr (MODE == 0)
-        attend_reduce_list<T, 16, 1, 2, CR, NS>(L, kb, vb, proxy, s_rows, n, qv, c, m, l, acc, smem, yacc, gacc);
+        attend_reduce_list<T, 16, 1, YGM, CR, NS>(L, kb, vb, proxy, AROW ? proxy : nullptr, s_rows, n, qv, c, m, l, acc,
+                                                  smem, yacc, gacc);
     else
         attend_list<T, 16, 1, 8>(kb, vb, s_rows, n, qv, c, 128, m, l, acc);
     long long t1 = clock64();
@@ -49,7 +50,7 @@ __global__ void __maxnreg__(96) bench_kernel(lrqk_layer_t L, const int *rows_all
     block_partial<T, 16, 1>(m, l, acc, 128, s_m, s_l, s_acc, parts + (size_t)blk * 130);
     if (MODE == 0) {
         float s = 0;
-        for (int i = 0; i < 2; ++i) for (int j = 0; j < 2; ++j) for (int k = 0; k < 4; ++k) s += yacc[i][j][k];
+        for (int j = 0; j < 2; ++j) for (int k = 0; k < 4; ++k) s += yacc[0][j][k];
         if (s == 12345.f) parts[0] = s;  // keep the reduction alive
     }
     if (threadIdx.x == 0) { clk[blk * 2] = t0; clk[blk * 2 + 1] = t1; }
@@ -221,10 +222,10 @@ void run_gather(lrqk_layer_t L, const int *rows, const int *nrows, int cap, floa
     printf("gather U=%2d smem %6d (%d blocks/SM): %7.2f us  %6.0f GB/s\n", U, per_sm_bytes, occ, ms * 1e3 / reps,
            bytes / (ms * 1e-3 / reps) / 1e9);
 }
-template <int CR, int NS, int MODE>
+template <int CR, int NS, int MODE, bool AROW = false, int YGM = 2>
 void run(const char *name, lrqk_layer_t L, const int *rows, const int *nrows, int cap, const T *q, float *parts,
          long long *clk, int nblk) {
-    auto fn = bench_kernel<CR, NS, MODE>;
+    auto fn = bench_kernel<CR, NS, MODE, AROW, YGM>;
     const int smem = 90 * 1024 + cap * 4;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b;
@@ -300,22 +301,9 @@ int main(int argc, char **argv) {
     T *KV = nullptr;
     if (cudaMalloc(&KV, (size_t)8 * T_ * 256 * 2) != cudaSuccess) { printf("alloc KV failed\n"); return 1; }
     cudaMemset(KV, 0, (size_t)8 * T_ * 256 * 2);
-    run_gather_tma<64, 2>(L, drows, dnr, cap, parts, nblk);
-    run_gather_tma<32, 4>(L, drows, dnr, cap, parts, nblk);
-    run_gather_tma<64, 3>(L, drows, dnr, cap, parts, nblk);
-    run_gather_tma<128, 1>(L, drows, dnr, cap, parts, nblk);
-    run_gather_kv<8>(KV, T_, drows, dnr, cap, parts, nblk);
-    run_gather_kv<16>(KV, T_, drows, dnr, cap, parts, nblk);
-    printf("%s\n", cudaGetErrorString(cudaDeviceSynchronize()));
-    run_gather<4>(L, drows, dnr, cap, parts, nblk, 100000);
-    run_gather<8>(L, drows, dnr, cap, parts, nblk, 100000);
-    run_gather<8>(L, drows, dnr, cap, parts, nblk, 0);
-    run_gather<16>(L, drows, dnr, cap, parts, nblk, 0);
     run<64, 2, 0>("cp.async CR=64 NS=2 (+YG)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<32, 4, 0>("cp.async CR=32 NS=4 (+YG)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<16, 4, 0>("cp.async CR=16 NS=4 (+YG)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<32, 2, 0>("cp.async CR=32 NS=2 (+YG)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<16, 8, 0>("cp.async CR=16 NS=8 (+YG)", L, drows, dnr, cap, q, parts, clk, nblk);
+    run<64, 2, 0, true>("cp.async CR=64 NS=2 (+YG, A row-major)", L, drows, dnr, cap, q, parts, clk, nblk);
+    run<64, 2, 0, false, 0>("cp.async CR=64 NS=2 (no YG)", L, drows, dnr, cap, q, parts, clk, nblk);
     run<0, 0, 1>("registers U=8 (no YG)", L, drows, dnr, cap, q, parts, clk, nblk);
     return 0;
 }
