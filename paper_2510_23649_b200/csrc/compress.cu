@@ -426,6 +426,9 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ldk = d * 2 + 16, lda = R * 2 + 16;  // bytes
     const int stage = mma_stage_bytes(R, d);
+    // the proxy rows from the row-major copy when the layer keeps one
+    const __nv_bfloat16 *arows = L.proxy_rowmajor
+        ? reinterpret_cast<const __nv_bfloat16 *>(L.proxy_rowmajor) + (size_t)bh * L.t_max * R : nullptr;
     const int *ridx = L.res_idx + (size_t)bh * L.s_cap + row0;
     const int *rslot = L.res_slot + (size_t)bh * L.s_cap + row0;
     const int MT = R / 16;            // m tiles (rank rows)
@@ -466,7 +469,8 @@ __device__ void prepare_reduce_mma(const lrqk_layer_t &L, int bh, int row0, int 
                 const int j = e2 / ap, pk = e2 - j * ap;
                 if (j < ns) {
                     const int x = s_ridx ? (host ? s_rproxy[s0 + j] : s_ridx[s0 + j]) : ridx[s0 + j];
-                    cp_async16(ab_s + j * lda + pk * 16, proxy + proxy_pack_offset(x, pk, ap) * 8);
+                    cp_async16(ab_s + j * lda + pk * 16,
+                               arows ? arows + (size_t)x * R + pk * 8 : proxy + proxy_pack_offset(x, pk, ap) * 8);
                 }
                 else *reinterpret_cast<uint4 *>(ab_s + j * lda + pk * 16) = make_uint4(0, 0, 0, 0);
             }
@@ -637,6 +641,8 @@ prepare_kernel(const lrqk_layer_t L) {
     const bool host = L.policy == LRQK_SLOW_HOST;
     const size_t kv_rows = ((size_t)b * L.n_kv_heads + g) * L.t_max;
     const T *proxy = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
+    const T *arows = L.proxy_rowmajor ? reinterpret_cast<const T *>(L.proxy_rowmajor) + (size_t)bh * L.t_max * R
+                                      : nullptr;
     const T *kbase = host ? reinterpret_cast<const T *>(L.slot_k) + (size_t)bh * L.n_slots * d
                           : reinterpret_cast<const T *>(L.slow_k) + kv_rows * d;
     float *hs = L.red_scratch + (size_t)bh * red_head_floats(R, d, nchunks);
@@ -702,7 +708,9 @@ prepare_kernel(const lrqk_layer_t L) {
                         } else {
                             const int e2 = e - ns * kp;
                             const int j = e2 / ap, pk = e2 - j * ap;
-                            v[u] = *reinterpret_cast<const uint4 *>(proxy + proxy_pack_offset(ridx[s0 + j], pk, ap) * N);
+                            v[u] = *reinterpret_cast<const uint4 *>(
+                                arows ? arows + (size_t)ridx[s0 + j] * R + pk * N
+                                      : proxy + proxy_pack_offset(ridx[s0 + j], pk, ap) * N);
                             dst[u] = (1 << 30) | (j * ldA + pk * N);
                         }
                     }
