@@ -149,19 +149,16 @@ __device__ void attend_reduce_list(const lrqk_layer_t &L, const T *kb, const T *
         cp_async_commit();
     };
     // NS-stage pipeline: NS - 1 chunks in flight while one is consumed (a
-    // commit group per chunk slot, empty past the end, so wait_group counts)
-#pragma unroll
-    for (int s0 = 0; s0 < NS - 1; ++s0) {
-        if (s0 < nch) issue(s0);
-        else cp_async_commit();
-    }
-    for (int ch = 0; ch < nch; ++ch) {
+    // commit group per chunk slot, empty past the end, so wait_group counts).
+    // One loop issues the prologue too (ch < 0), so the gather code exists
+    // once and the loop stays in the instruction cache.
+#pragma unroll 1
+    for (int ch = -(NS - 1); ch < nch; ++ch) {
         if (ch + NS - 1 < nch) issue(ch + NS - 1);
         else cp_async_commit();
+        if (ch < 0) continue;
         cp_async_wait<NS - 1>();
         __syncthreads();
-        if (ch == 0) trace(59);
-        if (ch == 3) trace(60);
         const uint8_t *kS = stage + (ch % NS) * buf, *vS = kS + tile_kv, *aS = vS + tile_kv;
         const int nr = min(CR, n - ch * CR);
         // online softmax over this chunk: group gidx takes rows gidx, gidx + ng, ...

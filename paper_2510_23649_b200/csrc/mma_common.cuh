@@ -50,7 +50,7 @@ LRQK_DEV void mma_reduce_tile(const uint8_t *kb_s, int ldk, const uint8_t *ab_s,
     constexpr int RR = MT * 16;  // rank_stride (== R)
     constexpr int GT = (RR / 16) * (RR / 8);
     (void)R;
-#pragma unroll
+#pragma unroll 1  // one k-step of code: the gather loop around it must stay in the instruction cache
     for (int ks = 0; ks < KR; ks += 16) {
         uint32_t af[MT][4];
 #pragma unroll
