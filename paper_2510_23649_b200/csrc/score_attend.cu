@@ -275,36 +275,39 @@ score_attend_kernel(const SAArgs a) {
             }
             __syncthreads();
             trace(49);
-            for (int r0 = 0; r0 < tot_c; r0 += 4 * (int)blockDim.x) {
-                int xi[4];
-                uint32_t kk[4];
+            // thread t classifies the contiguous candidates [t*per, (t+1)*per)
+            // (their keys loaded together), then one scan places the winners:
+            // ascending when per <= kCl (rounds of kCl keep the registers
+            // bounded; past that the order is still deterministic)
+            constexpr int kCl = 8;
+            const int per = (tot_c + blockDim.x - 1) / blockDim.x;
+            for (int c0 = 0; c0 < per; c0 += kCl) {
+                const int j0 = tid * per + c0, j1 = min(tid * per + min(per, c0 + kCl), tot_c);
+                uint32_t kk[kCl];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int j = r0 + u * (int)blockDim.x + tid;
-                    xi[u] = j < tot_c ? s_cl[j] : -1;
-                    kk[u] = xi[u] >= 0 ? __ldcg(keys + xi[u]) : 0u;
-                }
+                for (int u = 0; u < kCl; ++u) kk[u] = j0 + u < j1 ? __ldcg(keys + s_cl[j0 + u]) : 0u;
+                uint32_t wmask = 0;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (r0 + u * (int)blockDim.x >= tot_c) break;  // uniform
-                    int win_u = 0;
-                    if (xi[u] >= 0 && kk[u] >= klo) {
-                        const uint32_t dk = kk[u] - klo;
-                        if (dk >= kWinKeys || (int)(dk >> kWinShift) > D) {
-                            win_u = 1;
-                        } else if ((int)(dk >> kWinShift) == D) {
-                            const int q = atomicAdd(&s_ncrit, 1);
-                            if (q < kFCrit) s_crit[q] = make_comp(kk[u], xi[u]);
-                        }
+                for (int u = 0; u < kCl; ++u) {
+                    if (j0 + u >= j1 || kk[u] < klo) continue;
+                    const uint32_t dk = kk[u] - klo;
+                    if (dk >= kWinKeys || (int)(dk >> kWinShift) > D) {
+                        wmask |= 1u << u;
+                    } else if ((int)(dk >> kWinShift) == D) {
+                        const int q = atomicAdd(&s_ncrit, 1);
+                        if (q < kFCrit) s_crit[q] = make_comp(kk[u], s_cl[j0 + u]);
                     }
-                    int tot2;
-                    const int o = nloc + block_exclusive_scan(win_u, s_scan, &tot2);
-                    if (win_u) {
-                        if (o < L.s_cap) s_rows[o] = xi[u];
-                        if (out + o < k_eff) dst[out + o] = xi[u];
-                    }
-                    nloc += tot2;
                 }
+                int tot2;
+                int o = nloc + block_exclusive_scan(__popc(wmask), s_scan, &tot2);
+                while (wmask) {
+                    const int x = s_cl[j0 + __ffs(wmask) - 1];
+                    wmask &= wmask - 1u;
+                    if (o < L.s_cap) s_rows[o] = x;
+                    if (out + o < k_eff) dst[out + o] = x;
+                    ++o;
+                }
+                nloc += tot2;
             }
             trace(58);
         }
@@ -364,6 +367,8 @@ score_attend_kernel(const SAArgs a) {
         for (int i = part * blockDim.x + tid; i < kHistLevels * kHistBins; i += P * blockDim.x) ghist[i] = 0u;
     }
     const int need2 = k_eff - nabove;
+    // the list's first 32 entries travel with its length (one round trip)
+    const uint64_t v0 = warp == 0 ? __ldcg(cand + lane) : 0ull;
     const int n_crit = __ldcg(meta + M_CAND);
     const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && n_crit <= kFCrit;
     // bin-D winners, ascending, in the (now free) stage area
@@ -379,7 +384,7 @@ score_attend_kernel(const SAArgs a) {
         // one warp: bitonic sort of the composites (descending), then of the
         // winners' indices (ascending), through shuffles
         if (warp == 0) {
-            uint64_t v = lane < n_crit ? __ldcg(cand + lane) : 0ull;
+            uint64_t v = lane < n_crit ? v0 : 0ull;
 #pragma unroll
             for (int kk = 2; kk <= 32; kk <<= 1)
 #pragma unroll
