@@ -444,3 +444,58 @@ def test_row_mirror_matches_tiled_gathers(select_path):
     n = l + 6
     tiled = layers[0].proxy_rows()[:, :, :n, :r]
     assert torch.equal(layers[0].view("proxy_rowmajor")[:, :, :n, :r], tiled)  # the copy tracks the appends
+
+
+def test_graph_replay_hands_a_head_to_the_general_path():
+    """During CUDA-graph replay one head leaves the fused path (a zero query:
+    q_hat = 0, every score ties at 0, far below its threshold hint, so its
+    window misses) while the others stay fused: the general select +
+    attention kernels in the same replayed step must serve it (right
+    selection size and output) without disturbing the fused heads."""
+    from paper_2510_23649_b200.engine import Engine, LayerShape
+
+    torch.manual_seed(9)
+    B, Hq, Hkv, d, r, kb, lb, l = 1, 8, 2, 128, 16, 256, 16, 24000
+    eng = Engine(1, LayerShape(batch=B, n_q_heads=Hq, n_kv_heads=Hkv, head_dim=d, rank=r, k_budget=kb,
+                               lite_budget=lb, t_max=l + 32, dtype="bf16"), device="cuda")
+    K = torch.randn(B, Hkv, l, d, device="cuda").bfloat16()
+    V = torch.randn(B, Hkv, l, d, device="cuda").bfloat16()
+    eng.layers[0].load_prompt(torch.randn(B, Hq, l, r, device="cuda"),
+                              torch.randn(B, Hq, r, d, device="cuda") / d ** 0.5,
+                              torch.randn(B, Hq, r, d, device="cuda") / d ** 0.5, K, V)
+    G = Hq // Hkv
+    L = eng.layers[0]
+    for step in range(9):
+        q = torch.randn(1, B, Hq, d, device="cuda")
+        if step in (6, 7):
+            q[0, 0, 3] = 0.0
+        eng.q_buf[..., :d].copy_(q.bfloat16())
+        eng.k_buf[..., :d].copy_(torch.randn(1, B, Hkv, d, device="cuda").bfloat16())
+        eng.v_buf[..., :d].copy_(torch.randn(1, B, Hkv, d, device="cuda").bfloat16())
+        if step < 3:
+            eng.decode_step()
+        else:
+            if step == 3:
+                eng.capture()
+                assert eng.fused
+            eng.replay()
+        torch.cuda.synchronize()
+        eng.raise_status()
+        modes = L.view("sel_meta")[0, :, 7].tolist()
+        if step in (6, 7):
+            assert modes[3] != 6 and all(m == 6 for i, m in enumerate(modes) if i != 3), (step, modes)
+        elif step in (4, 5):
+            assert all(m == 6 for m in modes), (step, modes)
+        elif step == 8:  # head 3 is back on real scores; its hint (set at 0) recovers over a few steps
+            assert all(m == 6 for i, m in enumerate(modes) if i != 3), (step, modes)
+        n = int(eng.ctx[0].item())
+        Ks = L.view("slow_k")[0, :, :n, :d].float()
+        Vs = L.view("slow_v")[0, :, :n, :d].float()
+        cnt = L.view("res_cnt")[0].cpu()
+        idx = L.view("res_idx")[0].cpu()
+        qb = eng.q_buf[0, 0, :, :d].float()
+        for h in range(Hq):
+            sel = idx[h, : int(cnt[h])].long().cuda()
+            assert int(cnt[h]) == kb + lb and (n - 1) in sel.tolist()
+            w = torch.softmax(qb[h] @ Ks[h // G][sel].T / d ** 0.5, -1)
+            torch.testing.assert_close(eng.out_buf[0, 0, h, :d], w @ Vs[h // G][sel], rtol=2e-2, atol=2e-3)
