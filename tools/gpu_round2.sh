@@ -31,13 +31,19 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none \
   -c 600 --csv --log-file $o/launches_c4.csv python bench.py --profile-steps 6 --no-cpu-baseline > $o/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_attend -s 96 -c 1 \
   -o $o/score_attend_full python bench.py --profile-steps 6 --no-cpu-baseline > $o/ncu_full.log 2>&1
+# the reports stay on the box (gpurun copies back <= 64 MiB): text summaries only
+summ() { rep=$1; kern=$2; out=$3; ncu -i $rep.ncu-rep --page details > $out 2>&1; echo >> $out; \
+  python tools/ncu_stalls.py $rep.ncu-rep $kern 40 >> $out 2>&1; \
+  ncu -i $rep.ncu-rep --page raw --csv > $rep.raw.csv 2>/dev/null; rm -f $rep.ncu-rep; }
+summ $o/score_attend_full score_attend $o/score_attend_ncu_full.txt
 timeout 300 python tools/prefill_bench.py > $o/prefill_c4.json 2>&1
 timeout 300 python tools/prefill_bench.py --ctx 4096 --dtype f32 > $o/prefill_c1.json 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -k regex:"pf_" --csv --log-file $o/prefill_launches.csv python tools/prefill_bench.py --reps 1 > $o/ncu_prefill_launch.log 2>&1
-for k in pf_gram pf_mat; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 2 -c 1 \
+for k in pf_gram pf_mat; do  # -s 1: the timed call, after the warm-up call
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 1 -c 1 \
     -o $o/prefill_${k}_full python tools/prefill_bench.py --reps 1 > $o/ncu_prefill_$k.log 2>&1
+  summ $o/prefill_${k}_full $k $o/prefill_${k}_ncu_full.txt
 done
 make trace -j8 > /dev/null 2>&1
 timeout 300 python tools/step_timeline.py --layers 1 --fused-names > $o/timeline_1layer.txt 2>&1
