@@ -20,13 +20,13 @@ using T = __nv_bfloat16;
 
 constexpr int kThr = 288;
 
-template <int CR, int NS, int MODE, bool AROW = false, int YGM = 2>
+template <int CR, int NS, int MODE, bool AROW = false, int YGM = 2, int PPH = 9>
 __global__ void __maxnreg__(96) bench_kernel(lrqk_layer_t L, const int *rows_all, const int *nrows, int cap,
                                                     const T *q, float *parts, long long *clk) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ float s_m[9], s_l[9];
-    int *s_rows = reinterpret_cast<int *>(smem + 90 * 1024);
-    const int blk = blockIdx.x, h = blk / 9, g = h / 4;
+    int *s_rows = reinterpret_cast<int *>(smem + (PPH == 9 ? 90 : 42) * 1024);
+    const int blk = blockIdx.x, h = blk / PPH, g = h / 4;
     const int n = nrows[blk];
     for (int i = threadIdx.x; i < n; i += blockDim.x) s_rows[i] = rows_all[blk * cap + i];
     __syncthreads();
@@ -222,21 +222,22 @@ void run_gather(lrqk_layer_t L, const int *rows, const int *nrows, int cap, floa
     printf("gather U=%2d smem %6d (%d blocks/SM): %7.2f us  %6.0f GB/s\n", U, per_sm_bytes, occ, ms * 1e3 / reps,
            bytes / (ms * 1e-3 / reps) / 1e9);
 }
-template <int CR, int NS, int MODE, bool AROW = false, int YGM = 2>
+template <int CR, int NS, int MODE, bool AROW = false, int YGM = 2, int PPH = 9>
 void run(const char *name, lrqk_layer_t L, const int *rows, const int *nrows, int cap, const T *q, float *parts,
          long long *clk, int nblk) {
-    auto fn = bench_kernel<CR, NS, MODE, AROW, YGM>;
-    const int smem = 90 * 1024 + cap * 4;
+    auto fn = bench_kernel<CR, NS, MODE, AROW, YGM, PPH>;
+    const int smem = (PPH == 9 ? 90 : 42) * 1024 + cap * 4;
+    const int thr = PPH == 9 ? kThr : 160;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
-    for (int w = 0; w < 3; ++w) fn<<<nblk, kThr, smem>>>(L, rows, nrows, cap, q, parts, clk);
+    for (int w = 0; w < 3; ++w) fn<<<nblk, thr, smem>>>(L, rows, nrows, cap, q, parts, clk);
     const int reps = 20;
     float ms = 0.f;
     for (int w = 0; w < reps; ++w) {
         cudaMemsetAsync(g_flush, w, (size_t)256 << 20);  // evict the gathered rows from L2
         cudaEventRecord(a);
-        fn<<<nblk, kThr, smem>>>(L, rows, nrows, cap, q, parts, clk);
+        fn<<<nblk, thr, smem>>>(L, rows, nrows, cap, q, parts, clk);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float x; cudaEventElapsedTime(&x, a, b);
@@ -248,7 +249,7 @@ void run(const char *name, lrqk_layer_t L, const int *rows, const int *nrows, in
     for (int i = 0; i < nblk; ++i) d.push_back((c[2 * i + 1] - c[2 * i]) / 1965.0);
     std::sort(d.begin(), d.end());
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThr, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, thr, smem);
     printf("%-28s kernel %7.2f us  attend phase med %6.2f max %6.2f us  (%d blocks/SM) %s\n", name, ms * 1e3 / reps,
            d[nblk / 2], d.back(), occ, cudaGetErrorString(cudaGetLastError()));
 }
@@ -267,9 +268,9 @@ int main(int argc, char **argv) {
     cudaMemset(V, 0, (size_t)8 * T_ * 128 * 2);
     cudaMemset(A, 0, (size_t)Hq * T_ * 32 * 2);
     cudaMemset(q, 0, Hq * 128 * 2);
-    std::vector<int> rows(nblk * cap), nr(nblk);
+    std::vector<int> rows(nblk * cap), nr(nblk), rows18(2 * nblk * cap), nr18(2 * nblk);
     std::mt19937 rng(1);
-    const int part = 131072 / P;
+    const int part = 131072 / P, part18 = 131072 / 18;
     for (int h = 0; h < Hq; ++h) {
         std::vector<int> pick;
         std::uniform_int_distribution<int> U(0, 131071);
@@ -277,19 +278,20 @@ int main(int argc, char **argv) {
         std::sort(pick.begin(), pick.end());
         pick.erase(std::unique(pick.begin(), pick.end()), pick.end());
         for (int p = 0; p < P; ++p) nr[h * P + p] = 0;
+        for (int p = 0; p < 18; ++p) nr18[h * 18 + p] = 0;
         for (int x : pick) {
             const int p = std::min(P - 1, x / part);
             rows[(h * P + p) * cap + nr[h * P + p]++] = x;
+            const int p2 = std::min(17, x / part18);
+            rows18[(h * 18 + p2) * cap + nr18[h * 18 + p2]++] = x;
         }
-        if (mode_rows == 2)
-            for (int p = 0; p < P; ++p)
-                for (int j = 0; j < nr[h * P + p]; ++j) rows[(h * P + p) * cap + j] = p * part + (h % 4) * 4000 + j;
-        if (!sorted_rows)
-            for (int p = 0; p < P; ++p) std::shuffle(rows.begin() + (h * P + p) * cap, rows.begin() + (h * P + p) * cap + nr[h * P + p], rng);
     }
-    int *drows, *dnr; float *parts; long long *clk;
+    int *drows, *dnr, *drows18, *dnr18; float *parts; long long *clk;
     cudaMalloc(&drows, rows.size() * 4); cudaMalloc(&dnr, nblk * 4);
-    cudaMalloc(&parts, nblk * 130 * 4); cudaMalloc(&clk, nblk * 16);
+    cudaMalloc(&drows18, rows18.size() * 4); cudaMalloc(&dnr18, 2 * nblk * 4);
+    cudaMemcpy(drows18, rows18.data(), rows18.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dnr18, nr18.data(), 2 * nblk * 4, cudaMemcpyHostToDevice);
+    cudaMalloc(&parts, 2 * nblk * 130 * 4); cudaMalloc(&clk, 2 * nblk * 16);
     cudaMemcpy(drows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dnr, nr.data(), nblk * 4, cudaMemcpyHostToDevice);
     cudaMalloc(&g_flush, (size_t)256 << 20);
@@ -301,9 +303,9 @@ int main(int argc, char **argv) {
     T *KV = nullptr;
     if (cudaMalloc(&KV, (size_t)8 * T_ * 256 * 2) != cudaSuccess) { printf("alloc KV failed\n"); return 1; }
     cudaMemset(KV, 0, (size_t)8 * T_ * 256 * 2);
-    run<64, 2, 0>("cp.async CR=64 NS=2 (+YG)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<64, 2, 0, true>("cp.async CR=64 NS=2 (+YG, A row-major)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<64, 2, 0, false, 0>("cp.async CR=64 NS=2 (no YG)", L, drows, dnr, cap, q, parts, clk, nblk);
-    run<0, 0, 1>("registers U=8 (no YG)", L, drows, dnr, cap, q, parts, clk, nblk);
+    run<64, 2, 0, true, 0>("P=9  288thr CR=64 NS=2 no YG", L, drows, dnr, cap, q, parts, clk, nblk);
+    run<32, 2, 0, true, 0, 18>("P=18 160thr CR=32 NS=2 no YG", L, drows18, dnr18, cap, q, parts, clk, 2 * nblk);
+    run<0, 0, 1>("P=9  288thr registers U=8", L, drows, dnr, cap, q, parts, clk, nblk);
+    run<0, 0, 1, false, 0, 18>("P=18 160thr registers U=8", L, drows18, dnr18, cap, q, parts, clk, 2 * nblk);
     return 0;
 }
