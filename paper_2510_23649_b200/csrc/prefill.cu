@@ -262,30 +262,40 @@ __global__ void pf_combine_kernel(const PfGeom G, const float *__restrict__ part
 // K1s: the reference sweep in d-space, float64, one block per query head
 // ---------------------------------------------------------------------------
 // Block-wide product out(i, j) = sum_k a(i, k) b(k, j) with compile-time
-// shapes: 2 x 2 register tiles; when there are fewer tiles than threads, KS
-// adjacent lanes split the k range and combine with shuffles (fixed order).
+// shapes: 2 x 2 register tiles (rows i, i + M/2; columns j, j + N/2, so
+// adjacent lanes touch adjacent columns).  When there are fewer tiles than
+// threads, KS lanes of one warp (lane bits above the tile bits) split the k
+// range in chunks of CW rows -- slice s takes rows s*CW.. of every KS*CW --
+// and combine with shuffles in a fixed order.  With the padded shared-memory
+// strides of pf_solve (odd: C rows R + 1, B rows D + 1) the two slices a
+// half-warp holds read rows 8 apart, i.e. the other 8 banks.
 template <int M, int N, int K, class FA, class FB, class FO>
 LRQK_DEV void tile_mm(FA a, FB b, FO o) {
     static_assert(M % 2 == 0 && N % 2 == 0, "even shapes");
     constexpr int TN = N / 2, NTILE = (M / 2) * TN;
     constexpr int KS = NTILE >= kSolveThreads ? 1 : (NTILE * 2 >= kSolveThreads ? 2 : (NTILE * 4 >= kSolveThreads ? 4 : 8));
-    constexpr int TOTAL = NTILE * KS;
-    static_assert(TOTAL % 32 == 0, "whole warps");
+    constexpr int TOTAL = NTILE * KS, TPW = 32 / KS;  // tiles per warp
+    constexpr int CW = K / KS < 8 ? K / KS : 8;
+    static_assert(TOTAL % 32 == 0 && K % (KS * CW) == 0, "whole warps and chunks");
 #pragma unroll 1
     for (int t = threadIdx.x; t < TOTAL; t += kSolveThreads) {
-        const int tile = t / KS, sl = t % KS;
-        const int i0 = (tile / TN) * 2, j0 = (tile % TN) * 2;
+        const int lane = t & 31, sl = lane / TPW, tile = (t >> 5) * TPW + lane % TPW;
+        const int i0 = tile / TN, j0 = tile % TN, i1 = i0 + M / 2, j1 = j0 + N / 2;
         double a00 = 0.0, a01 = 0.0, a10 = 0.0, a11 = 0.0;
-#pragma unroll 8
-        for (int k = sl; k < K; k += KS) {
-            const double x0 = a(i0, k), x1 = a(i0 + 1, k), y0 = b(k, j0), y1 = b(k, j0 + 1);
-            a00 = fma(x0, y0, a00);
-            a01 = fma(x0, y1, a01);
-            a10 = fma(x1, y0, a10);
-            a11 = fma(x1, y1, a11);
+#pragma unroll 1
+        for (int kc = sl * CW; kc < K; kc += KS * CW) {
+#pragma unroll
+            for (int u = 0; u < CW; ++u) {
+                const int k = kc + u;
+                const double x0 = a(i0, k), x1 = a(i1, k), y0 = b(k, j0), y1 = b(k, j1);
+                a00 = fma(x0, y0, a00);
+                a01 = fma(x0, y1, a01);
+                a10 = fma(x1, y0, a10);
+                a11 = fma(x1, y1, a11);
+            }
         }
 #pragma unroll
-        for (int off = 1; off < KS; off <<= 1) {
+        for (int off = TPW; off < 32; off <<= 1) {
             a00 += __shfl_xor_sync(0xffffffffu, a00, off);
             a01 += __shfl_xor_sync(0xffffffffu, a01, off);
             a10 += __shfl_xor_sync(0xffffffffu, a10, off);
@@ -293,9 +303,9 @@ LRQK_DEV void tile_mm(FA a, FB b, FO o) {
         }
         if (sl == 0) {
             o(i0, j0, a00);
-            o(i0, j0 + 1, a01);
-            o(i0 + 1, j0, a10);
-            o(i0 + 1, j0 + 1, a11);
+            o(i0, j1, a01);
+            o(i1, j0, a10);
+            o(i1, j1, a11);
         }
     }
     __syncthreads();
@@ -307,16 +317,18 @@ LRQK_DEV void block_sums(double (&v)[NV], double *red) {
 #pragma unroll
     for (int j = 0; j < NV; ++j)
         for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_xor_sync(0xffffffffu, v[j], o);
+    // then every warp sums the per-warp partials with the same shuffle tree
     constexpr int nw = kSolveThreads / 32;
-    if ((threadIdx.x & 31) == 0)
+    static_assert(nw == 32, "one partial per lane");
+    const int lane = threadIdx.x & 31;
+    if (lane == 0)
 #pragma unroll
         for (int j = 0; j < NV; ++j) red[j * 32 + (threadIdx.x >> 5)] = v[j];
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < nw; ++w) t += red[j * 32 + w];
+        double t = red[j * 32 + lane];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
         v[j] = t;
     }
     __syncthreads();
@@ -409,6 +421,19 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
     double *wk = reinterpret_cast<double *>(scr + G.off_work) + (size_t)h * kWorkMats * D * R;
     double *Cq = wk, *Ck = Cq + D * R, *Wq = Ck + D * R, *Wk = Wq + D * R, *Wn = Wk + D * R, *Dt = Wn + D * R;
     double *Bq = Dt + D * R, *Bk = Bq + D * R, *Boq = Bk + D * R, *Bok = Boq + D * R;
+    // C_Q, C_K, B_Q, B_K and the new W live in shared memory when they fit
+    // (rank stride <= 32): the products of update_B / update_W read them many
+    // times.  Their rows are padded to an odd stride (LC, LB) so the
+    // transposed reads of update_B (lanes walking down a column) hit 16
+    // different banks; the other work matrices keep the dense global layout.
+    constexpr bool kSm = R <= 32;
+    constexpr int LC = kSm ? R + 1 : R, LB = kSm ? D + 1 : D;
+    if constexpr (kSm) {
+        double *sm5 = red + 5 * 32;
+        Cq = sm5; Ck = Cq + D * LC; Wn = Ck + D * LC; Bq = Wn + D * LC; Bk = Bq + R * LB;
+    }
+    auto cix = [](int i, int p) { return i * LC + p; };  // C, Wn (D x R)
+    auto bix = [](int p, int i) { return p * LB + i; };  // B (R x D)
     float *Wout = reinterpret_cast<float *>(scr + G.off_w);  // [2][H][128][RS] fp32 (Q then K)
     float *obj = P.objective ? P.objective + (size_t)h * (P.max_iter + 1) : nullptr;
 
@@ -421,7 +446,13 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
     for (int p = tid; p < R; p += nt) { c5[3] += G0Q[p * R + p]; c5[4] += G0K[p * R + p]; }
     block_sums<5>(c5, red);
     const double qk2 = c5[0], tq = c5[1], tk = c5[2], trg0q = c5[3], trg0k = c5[4];
-    for (int e = tid; e < D * R; e += nt) { Cq[e] = CQ0[e]; Ck[e] = CK0[e]; Bq[e] = 0.0; Bk[e] = 0.0; }
+    for (int e = tid; e < D * R; e += nt) {
+        const int i = e / R, p = e % R;
+        Cq[cix(i, p)] = CQ0[e];
+        Ck[cix(i, p)] = CK0[e];
+        Bq[bix(p, i)] = 0.0;
+        Bk[bix(p, i)] = 0.0;
+    }
     for (int e = tid; e < R * R; e += nt) { GAQ[e] = G0Q[e]; GAK[e] = G0K[e]; BBq[e] = 0.0; BBk[e] = 0.0; }
     __syncthreads();
 
@@ -430,10 +461,10 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
     auto objective = [&]() -> double {
         double v4[4] = {0.0, 0.0, 0.0, 0.0};  // cross, approx, q-resid, k-resid
         for (int e = tid; e < D * R; e += nt) {
-            const int i = e / R, p = e % R;
-            v4[0] += Cq[e] * Ck[e];
-            v4[2] -= 2.0 * Bq[p * D + i] * Cq[e];
-            v4[3] -= 2.0 * Bk[p * D + i] * Ck[e];
+            const int i = e / R, p = e % R, c = cix(i, p), b = bix(p, i);
+            v4[0] += Cq[c] * Ck[c];
+            v4[2] -= 2.0 * Bq[b] * Cq[c];
+            v4[3] -= 2.0 * Bk[b] * Ck[c];
         }
         for (int e = tid; e < R * R; e += nt) {
             v4[1] += GAQ[e] * GAK[e];
@@ -457,9 +488,9 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
         for (int e = tid; e < R * R; e += nt) Mm[e] = GA[e];
         __syncthreads();
         if (!inverse(Mm)) return false;
-        tile_mm<R, D, R>([&](int p, int q) { return Mm[p * R + q]; }, [&](int q, int i) { return Cx[i * R + q]; },
-                         [&](int p, int i, double v) { B[p * D + i] = v; });
-        tile_mm<R, R, D>([&](int p, int i) { return B[p * D + i]; }, [&](int i, int q) { return B[q * D + i]; },
+        tile_mm<R, D, R>([&](int p, int q) { return Mm[p * R + q]; }, [&](int q, int i) { return Cx[cix(i, q)]; },
+                         [&](int p, int i, double v) { B[bix(p, i)] = v; });
+        tile_mm<R, R, D>([&](int p, int i) { return B[bix(p, i)]; }, [&](int i, int q) { return B[bix(q, i)]; },
                          [&](int p, int q, double v) { BB[p * R + q] = v; });
         return true;
     };
@@ -468,8 +499,8 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
         for (int e = tid; e < R * R; e += nt) Mm[e] = GA[e] + lam * BB[e];
         __syncthreads();
         if (!inverse(Mm)) return false;
-        tile_mm<D, R, R>([&](int i, int q) { return Cx[i * R + q] + lam * B[q * D + i]; },
-                         [&](int q, int p) { return Mm[q * R + p]; }, [&](int i, int p, double v) { Wn[i * R + p] = v; });
+        tile_mm<D, R, R>([&](int i, int q) { return Cx[cix(i, q)] + lam * B[bix(q, i)]; },
+                         [&](int q, int p) { return Mm[q * R + p]; }, [&](int i, int p, double v) { Wn[cix(i, p)] = v; });
         return true;
     };
     // after Wn: new C = GX W, G_A = W^T C, and ||A' - A||^2 (sweep 1: against A0)
@@ -477,20 +508,29 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
                        double trg0, bool first) -> double {
         double dv[1] = {0.0};
         if (first) {
-            tile_mm<D, R, D>([&](int i, int j) { return GX[i * D + j]; }, [&](int j, int p) { return Wn[j * R + p]; },
-                             [&](int i, int p, double v) { Cx[i * R + p] = v; });
-            for (int e = tid; e < D * R; e += nt) { dv[0] += Wn[e] * (Cx[e] - 2.0 * C0[e]); W[e] = Wn[e]; }
+            tile_mm<D, R, D>([&](int i, int j) { return GX[i * D + j]; }, [&](int j, int p) { return Wn[cix(j, p)]; },
+                             [&](int i, int p, double v) { Cx[cix(i, p)] = v; });
+            for (int e = tid; e < D * R; e += nt) {
+                const int c = cix(e / R, e % R);
+                dv[0] += Wn[c] * (Cx[c] - 2.0 * C0[e]);
+                W[e] = Wn[c];
+            }
             block_sums<1>(dv, red);
             dv[0] += trg0;
         } else {
-            for (int e = tid; e < D * R; e += nt) W[e] = Wn[e] - W[e];  // dW
+            for (int e = tid; e < D * R; e += nt) W[e] = Wn[cix(e / R, e % R)] - W[e];  // dW
             __syncthreads();
             tile_mm<D, R, D>([&](int i, int j) { return GX[i * D + j]; }, [&](int j, int p) { return W[j * R + p]; },
                              [&](int i, int p, double v) { Dt[i * R + p] = v; });
-            for (int e = tid; e < D * R; e += nt) { dv[0] += W[e] * Dt[e]; Cx[e] += Dt[e]; W[e] = Wn[e]; }
+            for (int e = tid; e < D * R; e += nt) {
+                const int c = cix(e / R, e % R);
+                dv[0] += W[e] * Dt[e];
+                Cx[c] += Dt[e];
+                W[e] = Wn[c];
+            }
             block_sums<1>(dv, red);
         }
-        tile_mm<R, R, D>([&](int p, int i) { return W[i * R + p]; }, [&](int i, int q) { return Cx[i * R + q]; },
+        tile_mm<R, R, D>([&](int p, int i) { return W[i * R + p]; }, [&](int i, int q) { return Cx[cix(i, q)]; },
                          [&](int p, int q, double v) { Mm[p * R + q] = v; });
         for (int e = tid; e < R * R; e += nt) GA[e] = 0.5 * (Mm[e] + Mm[(e % R) * R + e / R]);
         __syncthreads();
@@ -506,7 +546,11 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
     }
     int sweeps = 0, conv = 0, ok = 1;
     for (int s = 0; s < P.max_iter; ++s) {
-        for (int e = tid; e < R * D; e += nt) { Boq[e] = Bq[e]; Bok[e] = Bk[e]; }
+        for (int e = tid; e < R * D; e += nt) {
+            const int b = bix(e / D, e % D);
+            Boq[e] = Bq[b];
+            Bok[e] = Bk[b];
+        }
         __syncthreads();
         if (!update_B(GAQ, Cq, Bq, BBq) || !update_B(GAK, Ck, Bk, BBk)) { ok = 0; break; }
         if (!update_W(GAQ, Cq, Bk, BBk, lk)) { ok = 0; break; }
@@ -516,7 +560,8 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
         ++sweeps;
         double v3[3] = {0.0, 0.0, 0.0};  // ||dB_Q||^2, ||dB_K||^2, non-finite count
         for (int e = tid; e < R * D; e += nt) {
-            const double a = Bq[e] - Boq[e], b = Bk[e] - Bok[e];
+            const int bi = bix(e / D, e % D);
+            const double a = Bq[bi] - Boq[e], b = Bk[bi] - Bok[e];
             v3[0] += a * a;
             v3[1] += b * b;
             v3[2] += (isfinite(Wq[e]) && isfinite(Wk[e])) ? 0.0 : 1.0;
@@ -542,8 +587,8 @@ pf_solve_kernel(const PfGeom G, lrqk_prefill_t P, uint8_t *scr) {
     float *BQo = P.B_Q + (size_t)h * R * G.ds, *BKo = P.B_K + (size_t)h * R * G.ds;
     for (int e = tid; e < R * G.ds; e += nt) {
         const int p = e / G.ds, i = e % G.ds;
-        BQo[e] = ok ? (float)Bq[p * D + i] : 0.f;
-        BKo[e] = ok ? (float)Bk[p * D + i] : 0.f;
+        BQo[e] = ok ? (float)Bq[bix(p, i)] : 0.f;
+        BKo[e] = ok ? (float)Bk[bix(p, i)] : 0.f;
     }
     float *WQo = Wout + (size_t)h * D * R, *WKo = Wout + ((size_t)G.H + h) * D * R;
     for (int e = tid; e < D * R; e += nt) {
@@ -927,7 +972,10 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
         pf_combine_kernel<<<grid, 256, 0, st>>>(G, part, scr);
     }
     // ---- K1s -----------------------------------------------------------------
-    const size_t ssm = (6 * (size_t)G.rs * G.rs + 256 + 5 * 32) * sizeof(double);
+    // the R x R work, the reduction scratch, and (rank stride <= 32) five D x R
+    // work matrices kept on chip
+    const size_t ssm = (6 * (size_t)G.rs * G.rs + 256 + 5 * 32 + (G.rs <= 32 ? 3 * (size_t)kTile * (G.rs + 1) + 2 * (size_t)G.rs * (kTile + 1) : 0)) *
+                       sizeof(double);
 #define LRQK_PF_SOLVE(RV)                                                                               \
     do {                                                                                                \
         cudaFuncSetAttribute(pf_solve_kernel<RV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm); \
