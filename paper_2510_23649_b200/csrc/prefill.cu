@@ -51,6 +51,9 @@ constexpr int kGramThreads = 128;
 constexpr int kMatThreads = 192;           // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 constexpr int kSolveThreads = 1024;
 constexpr int kMaxStages = 6;
+constexpr int kEpiStride = 36;                 // pf_mat staged epilogue: padded row (floats)
+constexpr int kEpiWarpFloats = 32 * kEpiStride;
+constexpr int kEpiBytes = 1024 + 4 * kEpiWarpFloats * 4;  // barrier room + four warp buffers
 constexpr int kWorkMats = 10;              // float64 d x r work matrices per head (solver)
 
 enum PfMap { MQ = 0, MQL = 1, MK = 2, MKL = 3, MYQ = 4, MYK = 5, kNumMaps = 6 };
@@ -613,7 +616,7 @@ __host__ __device__ inline void mat_unit(const PfGeom &G, int u, int &kside, int
 
 __global__ void __launch_bounds__(kMatThreads, 1)
 pf_mat_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, const float *__restrict__ W, float *A_Q, float *A_K,
-              int u0, int S2, int budget) {
+              int u0, int S2, int budget, int staged) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
     const int u = u0 + blockIdx.x / S2, s = blockIdx.x % S2;
@@ -719,7 +722,30 @@ pf_mat_kernel(const __grid_constant__ PfMaps maps, const PfGeom G, const float *
             const int grow = t * kTile + row;
             for (int j = 0; j < nh; ++j) {
                 float *dst = Aout + ((size_t)(h0 + j) * G.l + grow) * RS;
-                if (RS >= 32) {
+                if (RS >= 32 && staged) {
+                    // rows through a padded per-warp buffer so that each store
+                    // instruction writes four whole 128-B row segments
+                    float *eb = reinterpret_cast<float *>(sm + budget + 1024) + q4 * kEpiWarpFloats;
+                    for (int c0 = 0; c0 < RS; c0 += 32) {
+                        float hi[32], lo[32];
+                        tc::tmem_ld32(ta + j * 2 * RS + c0, hi);
+                        tc::tmem_ld32(ta + j * 2 * RS + RS + c0, lo);
+#pragma unroll
+                        for (int p = 0; p < 32; p += 4)
+                            *reinterpret_cast<float4 *>(eb + lane * kEpiStride + p) =
+                                make_float4(hi[p] + lo[p], hi[p + 1] + lo[p + 1], hi[p + 2] + lo[p + 2], hi[p + 3] + lo[p + 3]);
+                        __syncwarp();
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            const int rr = 4 * m + (lane >> 3), cc = (lane & 7) * 4;
+                            const int gr = t * kTile + q4 * 32 + rr;
+                            if (gr < G.l)
+                                *reinterpret_cast<float4 *>(Aout + ((size_t)(h0 + j) * G.l + gr) * RS + c0 + cc) =
+                                    *reinterpret_cast<const float4 *>(eb + rr * kEpiStride + cc);
+                        }
+                        __syncwarp();
+                    }
+                } else if (RS >= 32) {
                     for (int c0 = 0; c0 < RS; c0 += 32) {
                         float hi[32], lo[32];
                         tc::tmem_ld32(ta + j * 2 * RS + c0, hi);
@@ -989,18 +1015,20 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
     // ---- K1m -----------------------------------------------------------------
     // query heads: two CTAs per SM for bf16 (N = 2r, W^T 16 KB, 2 stages);
     // K heads: one CTA per SM, one K tile for up to 256 / 2r heads of its group
-    cudaFuncSetAttribute(pf_mat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 2048);
+    cudaFuncSetAttribute(pf_mat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 2048 + kEpiBytes);
     const float *Wsp = reinterpret_cast<const float *>(scr + G.off_w);
     const int nsm = num_sms();
     {
-        const int budget = G.parts == 1 ? 96 * 1024 : 200 * 1024;
+        // bf16: 80 KB = W^T (16 KB) + two 32-KB stages, so two CTAs fit with their epilogue staging
+        const int budget = G.parts == 1 ? 80 * 1024 : 200 * 1024;
         const int S2 = pick_slabs(G.H, G.tiles, nsm * (G.parts == 1 ? 2 : 1));
-        pf_mat_kernel<<<G.H * S2, kMatThreads, budget + 2048, st>>>(maps, G, Wsp, P.A_Q, P.A_K, 0, S2, budget);
+        pf_mat_kernel<<<G.H * S2, kMatThreads, budget + 2048 + kEpiBytes, st>>>(maps, G, Wsp, P.A_Q, P.A_K, 0, S2,
+                                                                                budget, 1);
     }
     {
         const int nk = G.Hk * G.nsub, S2 = pick_slabs(nk, G.tiles, nsm);
-        pf_mat_kernel<<<nk * S2, kMatThreads, 200 * 1024 + 2048, st>>>(maps, G, Wsp, P.A_Q, P.A_K, G.H, S2,
-                                                                       200 * 1024);
+        pf_mat_kernel<<<nk * S2, kMatThreads, 200 * 1024 + 2048 + kEpiBytes, st>>>(maps, G, Wsp, P.A_Q, P.A_K, G.H,
+                                                                                   S2, 200 * 1024, 1);
     }
     return cudaGetLastError() == cudaSuccess ? LRQK_OK : LRQK_ECUDA;
 }
