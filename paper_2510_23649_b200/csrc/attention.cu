@@ -46,6 +46,16 @@ __device__ void fold_yg_slots(const lrqk_layer_t &L, int bh, int yg_slots, int b
     if (blk == 0 && threadIdx.x == 0) const_cast<int *>(meta)[M_YG_FOLD] = 1;
 }
 
+// Output of a head whose selection ran in score_attend_kernel: its P
+// partials (slot stride attn_slots_dev(P)) merged by one block.
+__device__ void merge_score_attend_partials(const lrqk_layer_t &L, int bh, float *out) {
+    __shared__ float s_w[64], s_red[2];
+    const int d = L.dim_stride;
+    const int np = L.sel_meta[(size_t)bh * kMetaInts + M_ATT_PARTS];
+    const float *parts = L.attn_scratch + (size_t)bh * attn_slots_dev(L, np) * (size_t)(d + 2);
+    merge_partials(parts, np, d, out + (size_t)bh * d, s_w, s_red);
+}
+
 // One block = one split of kAttnRows selected rows of one (b, h).  Lanes are
 // grouped LPR per row (16-byte packs across d); each group runs an online
 // softmax over its rows; groups, warps and finally splits are merged with the
@@ -89,8 +99,12 @@ attention_kernel(const AttnArgs a) {
         else if (a.yg_slots > 0) fold_yg_slots(L, bh, a.yg_slots, split - 1, gridDim.x - 1);
         return;
     }
-    if (mode == 6) {  // score_attend_kernel wrote the output: only fold its Y|G slots
-        if (a.yg_slots > 0) fold_yg_slots(L, bh, a.yg_slots, split, gridDim.x);
+    if (mode == 6) {
+        // score_attend_kernel left P softmax partials: split 0 merges them into
+        // the output, the other splits fold its Y|G slots
+        if (split == 0) merge_score_attend_partials(L, bh, a.out);
+        if (a.yg_slots > 0 && (split > 0 || gridDim.x == 1))
+            fold_yg_slots(L, bh, a.yg_slots, gridDim.x == 1 ? 0 : split - 1, gridDim.x == 1 ? 1 : gridDim.x - 1);
         return;
     }
     const int S = L.res_cnt[bh];

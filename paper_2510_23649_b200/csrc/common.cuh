@@ -73,7 +73,7 @@ LRQK_DEV int attn_slots_dev(const lrqk_layer_t &L, int parts) {
 // reduce writes slot 0.  yg_slots is computed on the host (capi.cu).
 __host__ __device__ inline size_t yg_part_floats(int R, int d) { return (size_t)R * d + (size_t)R * R; }
 
-enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3, C_PREPARE = 4, C_FUSED = 5 };
+enum Counter : int { C_COMPRESS = 0, C_SCORE = 1, C_ATTN = 2, C_SELECT = 3, C_PREPARE = 4, C_FUSED = 5, C_POOL = 6 };
 
 // ---------------------------------------------------------------------------
 // vector loads: 16 bytes of storage -> float lanes

@@ -28,8 +28,9 @@
 //            lite window.
 //   attend   the block gathers its winners' K, V (and proxy rows, for the
 //            next step's Y = A^T K, G = A^T A) and writes one online-softmax
-//            partial; the last block to finish merges the head's P partials
-//            into the output and publishes the step's selection metadata.
+//            partial; the last block to finish publishes the step's
+//            selection metadata.  attention_kernel merges the head's P
+//            partials into the output (and folds the Y|G slots) next.
 //
 // The barriers need the head's P blocks co-resident: the launcher only takes
 // this path when the whole grid fits on the GPU at once (occupancy check) and
@@ -62,6 +63,7 @@ struct SAArgs {
     int parts;
     int yg_slots;
     int union_bytes;  // shared bytes shared by the stream stages + histograms and the attention chunks
+    int pool_pct;     // share of each part's tiles streamed from the head's shared pool (StreamPool)
 };
 
 LRQK_DEV int ld_acquire(const int *p) {
@@ -123,10 +125,12 @@ score_attend_kernel(const SAArgs a) {
     uint64_t *full = reinterpret_cast<uint64_t *>(sa_smem + a.union_bytes);
     uint64_t *empty = full + SS::kStages;
     int *s_rows = reinterpret_cast<int *>(full + 2 * SS::kStages);
-    __shared__ float s_m[kSAThreads / 32], s_l[kSAThreads / 32], s_w[64], s_red[2];
+    __shared__ float s_m[kSAThreads / 32], s_l[kSAThreads / 32];
     __shared__ int s_scan[32];
     __shared__ int s_flag, s_above, s_ncrit, s_cbase, s_nmine;
     __shared__ int s_out[2];
+    __shared__ int s_off[2];
+    __shared__ int s_pt[16];  // StreamPool stage tiles | counts
     __shared__ uint32_t s_hint;
     __shared__ uint64_t s_crit[kFCrit];
     trace(40);
@@ -144,6 +148,15 @@ score_attend_kernel(const SAArgs a) {
     const int tiles = (n + 31) >> 5;
     const int tpp = (tiles + P - 1) / P;
     const int tile0 = min(tiles, part * tpp), tile1 = min(tiles, tile0 + tpp);
+    // the part streams the first ns tiles of its range itself; the rest of
+    // every range is the head's shared pool (classification and attention
+    // keep the static ranges [tile0, tile1))
+    const int ns = min(tpp, (tpp * (100 - a.pool_pct) / 100) / kCW * kCW);
+    const int s_end = min(tile1, tile0 + ns);
+    const int cpp = (tpp - ns + kCW - 1) / kCW;
+    int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
+    int *pool_ctr = L.counters + (size_t)bh * kCounterInts + C_POOL;
+    const StreamPool sp{pool_ctr, tpp, ns, tiles, cpp, P * cpp, s_pt, s_pt + 8};
     const int stride = sample_stride(lite_start);
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     // hint window (persistent meta written by the previous step's selection)
@@ -161,24 +174,25 @@ score_attend_kernel(const SAArgs a) {
     }
     __syncthreads();
     int it0 = 0;  // stages in flight before the wait (producer lane)
-    if (warp == kCW && lane == 0) it0 = score_prefetch_stages<T, NPK>(L, bh, tile0, tile1, t, stage, full);
+    if (warp == kCW && lane == 0) it0 = score_prefetch_stages<T, NPK>(L, bh, tile0, s_end, t, stage, full);
     pdl_wait();  // q_hat, the appended proxy row and ctx_len come from compress
     pdl_trigger();
     if (win) hint_window(scaled_hint(meta, qhat_norm(L, bh)), klo, kc);
 
     // ---- stream ------------------------------------------------------------
-    score_stream<T, NPK>(L, bh, tile0, tile1, n, lite_start, stride, win, klo, kc, stage, full, empty, s_hist, s_win,
-                         &s_above, it0);
+    score_stream<T, NPK, false, true>(L, bh, tile0, s_end, n, lite_start, stride, win, klo, kc, stage, full, empty,
+                                      s_hist, s_win, &s_above, it0, nullptr, nullptr, 0xFFFFFFFFu, sp);
     trace(41);
     __syncthreads();
-    score_flush(L, bh, P, part, win, s_hist, s_win, s_above, s_scan);
+    // merged histograms only: a part's rows were not all streamed by the part
+    score_flush(L, bh, P, part, win, s_hist, s_win, s_above, s_scan, false);
     const int k_eff = min(L.k_budget, lite_start);
-    int *cnt = L.counters + (size_t)bh * kCounterInts + C_SCORE;
     if (!win || lite_start == 0 || k_eff >= lite_start) {
         // no hint (the first step after a prompt) or everything fits: the
         // score kernel's hand-off to select_kernel
         if (!last_arrival(cnt, P, &s_flag)) return;
-        score_last_block(L, bh, P, win, klo, kc, lite_start, stride, s_hist, s_win, s_scan, s_out);
+        if (tid == 0) atomicExch(pool_ctr, 0);  // every part has left the stream
+        score_last_block(L, bh, P, win, klo, kc, lite_start, stride, s_hist, s_win, s_scan, s_out, false);
         return;
     }
 
@@ -192,7 +206,12 @@ score_attend_kernel(const SAArgs a) {
     const T *proxy = reinterpret_cast<const T *>(L.proxy) + (size_t)bh * L.t_max * R;
     const T *arows = L.proxy_rowmajor ? reinterpret_cast<const T *>(L.proxy_rowmajor) + (size_t)bh * L.t_max * R
                                       : nullptr;
-    uint32_t wv[4];
+
+    // ---- B1: the head's window histogram (and every row's key) is complete ---------
+    head_barrier(cnt, P, L.status);
+    trace(42);
+    if (part == 0 && tid == 0) atomicExch(pool_ctr, 0);  // every part has left the stream
+    uint32_t wv[4];  // this part's candidate mask words (streamed by any part)
     {
         const uint32_t *cmw = L.cmask + (size_t)bh * ((L.t_max + 31) >> 5) + w0;
 #pragma unroll
@@ -201,10 +220,6 @@ score_attend_kernel(const SAArgs a) {
             wv[u] = (u < wpt && wi < nwrd) ? __ldcg(cmw + wi) : 0u;
         }
     }
-
-    // ---- B1: the head's window histogram is complete -------------------------
-    head_barrier(cnt, P, L.status);
-    trace(42);
     const uint32_t *gwin = L.hist + (size_t)bh * kHistLevels * kHistBins + 2 * kHistBins;
     const int above_win = __ldcg(meta + M_ABOVE);
     for (int i = tid; i < kHistBins; i += blockDim.x) s_win[i] = (int)__ldcg(gwin + i);
@@ -217,31 +232,11 @@ score_attend_kernel(const SAArgs a) {
         nabove = above_win + s_out[1];
     }
     trace(47);
-    // the parts' certain-winner counts: this part's output offset, and the total
-    __shared__ int s_off[2];
-    if (warp == 0) {
-        int o = 0, tt = 0;
-        if (D >= 0) {
-            const uint32_t *ph0 = reinterpret_cast<const uint32_t *>(L.fcand) + (size_t)bh * P * kPartHist;
-            for (int q0 = 0; q0 < P; q0 += 32) {
-                const int q = q0 + lane;
-                const int c = q < P ? (int)__ldcg(ph0 + (size_t)q * kPartHist + D + 1) : 0;
-                tt += c;
-                o += q < part ? c : 0;
-            }
-            tt = __reduce_add_sync(0xffffffffu, tt);
-            o = __reduce_add_sync(0xffffffffu, o);
-        }
-        if (lane == 0) { s_off[0] = o; s_off[1] = tt; }
-    }
-    __syncthreads();
-    const int out = s_off[0], tot = s_off[1];
-    trace(48);
-    if (D < 0 || tot != nabove || s_win[D] > kFCrit) {
+    if (D < 0 || s_win[D] > kFCrit) {
         // window miss, or a threshold bin too large to rank here: the last
         // block to get here hands the head to select_kernel (mode 3 / 0)
         if (final_arrival(cnt, 2, 3 * P, &s_flag))
-            score_last_block(L, bh, P, win, klo, kc, lite_start, stride, s_hist, s_win, s_scan, s_out);
+            score_last_block(L, bh, P, win, klo, kc, lite_start, stride, s_hist, s_win, s_scan, s_out, false);
         return;
     }
 
@@ -304,7 +299,6 @@ score_attend_kernel(const SAArgs a) {
                     const int x = s_cl[j0 + __ffs(wmask) - 1];
                     wmask &= wmask - 1u;
                     if (o < L.s_cap) s_rows[o] = x;
-                    if (out + o < k_eff) dst[out + o] = x;
                     ++o;
                 }
                 nloc += tot2;
@@ -344,7 +338,6 @@ score_attend_kernel(const SAArgs a) {
             smask &= smask - 1u;
             const int x = base + tid * 32 + bpos;
             if (o < L.s_cap) s_rows[o] = x;
-            if (out + o < k_eff) dst[out + o] = x;
             ++o;
         }
         nloc += tot2;
@@ -356,6 +349,7 @@ score_attend_kernel(const SAArgs a) {
         __syncthreads();
         for (int j = tid; j < nc; j += blockDim.x)
             if (s_cbase + j < L.cand_cap) cand[s_cbase + j] = s_crit[j];
+        if (tid == 0) L.fcnt[(size_t)bh * P + part] = nloc;  // certain winners: the parts' offsets after B2
     }
     trace(44);
 
@@ -370,7 +364,19 @@ score_attend_kernel(const SAArgs a) {
     // the list's first 32 entries travel with its length (one round trip)
     const uint64_t v0 = warp == 0 ? __ldcg(cand + lane) : 0ull;
     const int n_crit = __ldcg(meta + M_CAND);
-    const bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && n_crit <= kFCrit;
+    if (warp == 1) {  // the parts' certain-winner counts: this part's output offset, and the total
+        int o = 0, tt = 0;
+        for (int q0 = 0; q0 < P; q0 += 32) {
+            const int q = q0 + lane;
+            const int c = q < P ? __ldcg(L.fcnt + (size_t)bh * P + q) : 0;
+            tt += c;
+            o += q < part ? c : 0;
+        }
+        tt = __reduce_add_sync(0xffffffffu, tt);
+        o = __reduce_add_sync(0xffffffffu, o);
+        if (lane == 0) { s_off[0] = o; s_off[1] = tt; }
+    }
+    bool ok = need2 >= 0 && need2 <= n_crit && n_crit <= L.cand_cap && n_crit <= kFCrit;
     // bin-D winners, ascending, in the (now free) stage area
     int *s_list = reinterpret_cast<int *>(stage);
     uint64_t *crit = reinterpret_cast<uint64_t *>(stage + kFCrit * 4);
@@ -421,6 +427,15 @@ score_attend_kernel(const SAArgs a) {
         for (int i = tid; i < need2; i += blockDim.x) s_list[i] = (int)crit[i];
     }
     __syncthreads();
+    trace(48);
+    const int out = s_off[0];
+    if (ok && s_off[1] != nabove) {  // the certain winners disagree with the histogram (never expected)
+        ok = false;
+        if (tid == 0) set_status(L.status, LRQK_ST_INDEX_RANGE);
+    }
+    if (ok)
+        for (int i = tid; i < min(nloc, L.s_cap); i += blockDim.x)
+            if (out + i < k_eff) dst[out + i] = s_rows[i];
     const int nwin = ok ? need2 : 0;
     // part 0 writes the bin-D winners; every block attends those in its rows
     if (part == 0)
@@ -483,10 +498,10 @@ score_attend_kernel(const SAArgs a) {
     block_partial<T, LPR, PPL>(m, l, acc, d, s_m, s_l, s_acc, parts + (size_t)part * (d + 2));
     trace(57);
 
-    // ---- the last block of the head: merge, publish -------------------------------
+    // ---- the last block of the head: publish (attention_kernel merges the
+    // P partials into the output, beside its Y|G fold) ----------------------------
     if (!final_arrival(cnt, 1, 3 * P, &s_flag)) return;
     trace(53);
-    merge_partials(parts, P, d, a.out + (size_t)bh * d, s_w, s_red);
     if (tid == 0) {
         L.res_cnt[bh] = k_eff + nl;
         meta[M_KLO] = (int)klo;
@@ -577,7 +592,12 @@ static int launch_sa(const SAArgs &a0, cudaStream_t st) {
 // lrqk_score + lrqk_select_attend instead.
 int launch_score_attend(const lrqk_layer_t &L, const void *q, float *out, cudaStream_t st) {
     if (L.policy != LRQK_SLOW_HBM || L.dim_stride != 128) return LRQK_EUNSUPPORTED;
-    SAArgs a{L, q, out, score_tma_parts(L), yg_slots(L), 0};
+    static const int pool_pct = [] {
+        const char *e = getenv("LRQK_SA_POOL");  // percent of each part's tiles in the shared pool
+        const int v = e ? atoi(e) : 10;
+        return v < 0 ? 0 : (v > 100 ? 100 : v);
+    }();
+    SAArgs a{L, q, out, score_tma_parts(L), yg_slots(L), 0, pool_pct};
     if (L.dtype == LRQK_BF16) {
         switch (L.rank_stride) {
             case 16: return launch_sa<__nv_bfloat16, 2, 16, 1, 1, 64, 2>(a, st);

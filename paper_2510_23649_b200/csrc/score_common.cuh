@@ -89,6 +89,19 @@ LRQK_DEV int score_prefetch_stages(const lrqk_layer_t &L, int bh, int tile0, int
     return it;
 }
 
+// Shared tail of a head's stream (the fused kernel): every part streams the
+// first ns tiles of its own range, then the parts take the remaining stages
+// of all the head's ranges from one counter, so a part that started late or
+// streams slowly is helped by the others.  Pool item j = stage c of part p's
+// tail (j = p * cpp + c), tiles [p*tpp + ns + c*kCW, ...) within the part's
+// range.  s_tile / s_nt: per-stage tile base and count, handed by the
+// producer to the consumers through the full barrier (-1: no more stages).
+struct StreamPool {
+    int *ctr;
+    int tpp, ns, tiles, cpp, npool;
+    int *s_tile, *s_nt;
+};
+
 // Phase 1 of both score kernels, for the tiles [tile0, tile1) of head bh:
 // one producer warp (warp kCW) keeps the TMA bulk-copy pipeline full, the
 // kCW consumer warps score one 32-row tile per stage (lane = row), store the
@@ -102,11 +115,13 @@ LRQK_DEV int score_prefetch_stages(const lrqk_layer_t &L, int bh, int tile0, int
 // k-th largest key, so mostly this step's winners -- have their K and V rows
 // (pf_k, pf_v) and their proxy row prefetched into L2 (evict-last) while the
 // stream still runs, so the attention gathers after the selection hit L2.
-template <typename T, int NPK, bool PF = false>
+//
+// DYN: [tile0, tile1) is the part's own share; the pool (sp) follows it.
+template <typename T, int NPK, bool PF = false, bool DYN = false>
 LRQK_DEV void score_stream(const lrqk_layer_t &L, int bh, int tile0, int tile1, int n, int lite_start, int stride,
                            bool win, uint32_t klo, uint32_t kc, uint8_t *tsm, uint64_t *full, uint64_t *empty,
                            int *s_hist, int *s_win, int *s_above, int it0 = 0, const T *pf_k = nullptr,
-                           const T *pf_v = nullptr, uint32_t kpf = 0xFFFFFFFFu) {
+                           const T *pf_v = nullptr, uint32_t kpf = 0xFFFFFFFFu, StreamPool sp = {}) {
     using SS = ScoreStages<NPK>;
     constexpr int N = Pack<T>::N;
     constexpr int R = NPK * N;
@@ -136,6 +151,40 @@ LRQK_DEV void score_stream(const lrqk_layer_t &L, int bh, int tile0, int tile1, 
                 bulk_g2s_hint(tsm + s2 * SS::kStageBytes, src + (size_t)(tile0 + it * kCW) * SS::kTileBytes, bytes,
                               full + s2, pol_stream);
             }
+            if constexpr (DYN) {
+                int it = n_stage_iters > it0 ? n_stage_iters : it0;
+                int j = atomicAdd(sp.ctr, 1);
+                for (;; ++it) {
+                    int ta = -1, te = 0;
+                    while (j < sp.npool) {
+                        const int p = j / sp.cpp, c = j - p * sp.cpp;
+                        ta = p * sp.tpp + sp.ns + c * kCW;
+                        te = min(sp.tiles, (p + 1) * sp.tpp);
+                        if (ta < te) break;
+                        ta = -1;
+                        j = atomicAdd(sp.ctr, 1);
+                    }
+                    const int s2 = it % SS::kStages;
+                    if (it >= SS::kStages) {
+                        mbar_wait(empty + s2, ((it / SS::kStages) - 1) & 1);
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    }
+                    if (ta < 0) {  // pool drained: release the consumers
+                        sp.s_tile[s2] = -1;
+                        mbar_arrive(full + s2);
+                        break;
+                    }
+                    const int nt = min(kCW, te - ta);
+                    sp.s_tile[s2] = ta;
+                    sp.s_nt[s2] = nt;
+                    const int jn = atomicAdd(sp.ctr, 1);  // the next grab, in flight during this copy
+                    const uint32_t bytes = (uint32_t)nt * SS::kTileBytes;
+                    mbar_expect_tx(full + s2, bytes);
+                    bulk_g2s_hint(tsm + s2 * SS::kStageBytes, src + (size_t)ta * SS::kTileBytes, bytes, full + s2,
+                                  pol_stream);
+                    j = jn;
+                }
+            }
         }
     } else {
         // ---------------- consumers ----------------
@@ -144,11 +193,18 @@ LRQK_DEV void score_stream(const lrqk_layer_t &L, int bh, int tile0, int tile1, 
 #pragma unroll
         for (int e = 0; e < R; ++e) qv[e] = qh[e];
         int above = 0;
-        for (int it = 0; it < n_stage_iters; ++it) {
+        for (int it = 0;; ++it) {
+            if (!DYN && it >= n_stage_iters) break;
             const int s2 = it % SS::kStages;
             mbar_wait(full + s2, (it / SS::kStages) & 1);
-            const int tile = tile0 + it * kCW + warp;
-            if (tile < tile1) {
+            int ta = tile0 + it * kCW, ntl = min(kCW, tile1 - ta);
+            if (DYN && it >= n_stage_iters) {
+                ta = sp.s_tile[s2];
+                if (ta < 0) break;
+                ntl = sp.s_nt[s2];
+            }
+            const int tile = ta + warp;
+            if (warp < ntl) {
                 const uint4 *p4 = reinterpret_cast<const uint4 *>(tsm + s2 * SS::kStageBytes + warp * SS::kTileBytes) + lane;
                 float s0 = 0.f, s1 = 0.f;
 #pragma unroll
@@ -201,7 +257,7 @@ LRQK_DEV void score_stream(const lrqk_layer_t &L, int bh, int tile0, int tile1, 
 // ph[i] = rows of the part with a key in window bin >= i or above the
 // window; ph[kHistBins] = above.  Whole block.
 LRQK_DEV void score_flush(const lrqk_layer_t &L, int bh, int P, int part, bool win, const int *s_hist,
-                          const int *s_win, int s_above, int *s_scan) {
+                          const int *s_win, int s_above, int *s_scan, bool part_hist = true) {
     const int tid = threadIdx.x;
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;
@@ -211,7 +267,7 @@ LRQK_DEV void score_flush(const lrqk_layer_t &L, int bh, int P, int part, bool w
         if (s_win[i]) atomicAdd(gwin + i, (uint32_t)s_win[i]);
     }
     if (tid == 0 && s_above) atomicAdd(meta + M_ABOVE, s_above);
-    if (win) {
+    if (win && part_hist) {
         uint32_t *ph = reinterpret_cast<uint32_t *>(L.fcand) + ((size_t)bh * P + part) * kPartHist;
         constexpr int CB = kHistBins / 256;  // bins per thread (threads 0..255)
         int loc = 0;
@@ -240,7 +296,7 @@ LRQK_DEV void score_flush(const lrqk_layer_t &L, int bh, int P, int part, bool w
 template <int Dummy = 0>
 __device__ __forceinline__ void score_last_block(const lrqk_layer_t &L, int bh, int P, bool win, uint32_t klo, uint32_t kc,
                                               int lite_start, int stride, int *s_hist, int *s_win, int *s_scan,
-                                              int *s_out) {
+                                              int *s_out, bool allow5 = true) {
     const int tid = threadIdx.x;
     int *meta = L.sel_meta + (size_t)bh * kMetaInts;
     uint32_t *ghist = L.hist + (size_t)bh * kHistLevels * kHistBins;
@@ -268,7 +324,7 @@ __device__ __forceinline__ void score_last_block(const lrqk_layer_t &L, int bh, 
         if (D >= 0) {
             const int nabove = above_win + s_out[1];
             int mode = 3;
-            if (L.policy == LRQK_SLOW_HBM) {
+            if (L.policy == LRQK_SLOW_HBM && allow5) {
                 // mode 5: certain winners per part -> exclusive offsets (fcnt)
                 mode = 5;
                 const uint32_t *ph0 = reinterpret_cast<const uint32_t *>(L.fcand) + (size_t)bh * P * kPartHist;

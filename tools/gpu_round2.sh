@@ -40,7 +40,7 @@ timeout 300 python tools/prefill_bench.py > $o/prefill_c4.json 2>&1
 timeout 300 python tools/prefill_bench.py --ctx 4096 --dtype f32 > $o/prefill_c1.json 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   -k regex:"pf_" --csv --log-file $o/prefill_launches.csv python tools/prefill_bench.py --reps 1 > $o/ncu_prefill_launch.log 2>&1
-for k in pf_gram pf_mat; do  # -s 1: the timed call, after the warm-up call
+for k in pf_gram pf_mat pf_solve; do  # -s 1: the timed call, after the warm-up call
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 1 -c 1 \
     -o $o/prefill_${k}_full python tools/prefill_bench.py --reps 1 > $o/ncu_prefill_$k.log 2>&1
   summ $o/prefill_${k}_full $k $o/prefill_${k}_ncu_full.txt
