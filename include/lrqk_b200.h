@@ -181,13 +181,14 @@ int lrqk_select(const lrqk_layer_t *L, void *stream);
  * after it.  ref: cache.py:149-171, attention.py:23-34. */
 int lrqk_select_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
-/* lrqk_score + lrqk_select_attend + the partial merge as ONE kernel (HBM
- * policy, dim_stride 128): each head's blocks meet at per-head barriers, so
- * a head selects and attends as soon as its own parts have streamed.  Heads
- * off the hint-window path this step are left to lrqk_select /
- * lrqk_attention as after lrqk_score.  Returns LRQK_EUNSUPPORTED (nothing
- * launched) for layouts it does not cover or when its grid cannot be
- * co-resident; run lrqk_score + lrqk_select_attend then.
+/* lrqk_score + lrqk_select_attend as ONE kernel (HBM policy, dim_stride
+ * 128): each head's blocks meet at per-head barriers, so a head selects and
+ * attends as soon as its own parts have streamed; its softmax partials are
+ * merged into out by lrqk_attention (launch it after lrqk_select, as after
+ * lrqk_select_attend).  Heads off the hint-window path this step are left
+ * to lrqk_select / lrqk_attention as after lrqk_score.  Returns
+ * LRQK_EUNSUPPORTED (nothing launched) for layouts it does not cover or when
+ * its grid cannot be co-resident; run lrqk_score + lrqk_select_attend then.
  * ref: cache.py:141-171, linalg.py:96-110, attention.py:23-34. */
 int lrqk_score_attend(const lrqk_layer_t *L, const void *q, float *out, void *stream);
 
