@@ -299,7 +299,10 @@ typedef struct lrqk_prefill {
     int32_t want_objective; /* record the Lagrangian after init and each sweep */
     const void *Q;          /* [n_heads, len, dim_stride]                     */
     const void *K;          /* [n_heads/group, len, dim_stride]               */
-    float *A_Q, *A_K;       /* [n_heads, len, rank_stride] in: init, out: factors */
+    float *A_Q, *A_K;       /* [n_heads, len, rank_stride] in: init, out: factors;
+                             * A_Q may be NULL when A_Q0 is given: the query
+                             * factor is then not materialised (decode reads
+                             * only A_K, B_Q, B_K) */
     float *B_Q, *B_K;       /* [n_heads, rank_stride, dim_stride] out         */
     float *objective;       /* [n_heads, max_iter+1] (NaN where not reached)  */
     int32_t *sweeps;        /* [n_heads]                                      */

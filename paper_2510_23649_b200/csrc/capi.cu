@@ -393,7 +393,7 @@ size_t lrqk_prefill_scratch_bytes(const lrqk_prefill_t *P) {
 }
 
 int lrqk_prefill_factorize(const lrqk_prefill_t *P, void *stream) {
-    if (!P || P->n_heads < 1 || P->len < 1 || !P->Q || !P->K || !P->A_Q || !P->A_K || !P->B_Q || !P->B_K ||
+    if (!P || P->n_heads < 1 || P->len < 1 || !P->Q || !P->K || !(P->A_Q || P->A_Q0) || !P->A_K || !P->B_Q || !P->B_K ||
         !P->scratch || !P->sweeps || !P->converged || P->max_iter < 1)
         return LRQK_EINVAL;
     if (P->want_objective && !P->objective) return LRQK_EINVAL;

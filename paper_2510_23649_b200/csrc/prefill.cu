@@ -1018,7 +1018,7 @@ int launch_prefill(const lrqk_prefill_t &P, cudaStream_t st) {
     cudaFuncSetAttribute(pf_mat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024 + 2048 + kEpiBytes);
     const float *Wsp = reinterpret_cast<const float *>(scr + G.off_w);
     const int nsm = num_sms();
-    {
+    if (P.A_Q) {  // NULL (with a separate init): the query factor is not materialised
         // bf16: 80 KB = W^T (16 KB) + two 32-KB stages, so two CTAs fit with their epilogue staging
         const int budget = G.parts == 1 ? 80 * 1024 : 200 * 1024;
         const int S2 = pick_slabs(G.H, G.tiles, nsm * (G.parts == 1 ? 2 : 1));

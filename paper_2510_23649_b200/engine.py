@@ -373,13 +373,15 @@ def randn_init(l: int, r: int, seed: int):
 
 def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter=2, tol=1e-2,
                              A_Q0=None, A_K0=None, want_objective=False, dtype="bf16", seed=0,
-                             group=None):
+                             group=None, want_a_q=True):
     """Batched prefill factorisation on the GPU (ref: prefill.py:197-230).
 
     Q [H, l, d], K [H/group, l, d] device tensors.  A_Q0/A_K0: [l, r] or
     [H, l, r] initial factors (default: the reference randn draw).
     Returns dict(A_Q, A_K [H,l,r], B_Q, B_K [H,r,d], objective [H, max_iter+1],
-    sweeps [H], converged [H]) as device tensors.
+    sweeps [H], converged [H]) as device tensors.  want_a_q=False skips the
+    query factor's materialisation (A_Q None): a decode engine only reads
+    A_K, B_Q and B_K, and A_Q is the largest write of the call.
     """
     lib = _lib.lib()
     dev = Q.device
@@ -412,7 +414,7 @@ def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter
     if not shared:
         A0q = A0q.expand(H, l, rs).contiguous() if A0q.dim() == 2 else A0q
         A0k = A0k.expand(H, l, rs).contiguous() if A0k.dim() == 2 else A0k
-    A_Q = torch.empty(H, l, rs, dtype=torch.float32, device=dev)
+    A_Q = torch.empty(H, l, rs, dtype=torch.float32, device=dev) if want_a_q else None
     A_K = torch.empty(H, l, rs, dtype=torch.float32, device=dev)
     B_Q = torch.zeros(H, rs, ds, dtype=torch.float32, device=dev)
     B_K = torch.zeros(H, rs, ds, dtype=torch.float32, device=dev)
@@ -426,7 +428,7 @@ def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter
     P.lambda_q, P.lambda_k, P.tol = lambda_q, lambda_k, tol
     P.want_objective = int(want_objective)
     P.Q, P.K = Qp.data_ptr(), Kp.data_ptr()
-    P.A_Q, P.A_K, P.B_Q, P.B_K = A_Q.data_ptr(), A_K.data_ptr(), B_Q.data_ptr(), B_K.data_ptr()
+    P.A_Q, P.A_K, P.B_Q, P.B_K = (A_Q.data_ptr() if want_a_q else 0), A_K.data_ptr(), B_Q.data_ptr(), B_K.data_ptr()
     P.objective, P.sweeps, P.converged = obj.data_ptr(), sweeps.data_ptr(), conv.data_ptr()
     P.status = status.data_ptr()
     P.A_Q0, P.A_K0, P.init_shared = A0q.data_ptr(), A0k.data_ptr(), int(shared)
@@ -441,7 +443,7 @@ def prefill_factorize_device(Q, K, rank, *, lambda_q=1.0, lambda_k=1.0, max_iter
         raise NonFiniteError("prefill factors diverged")
     if st & _lib.ST_SOLVE_FAILED:
         raise SolveFailedError("prefill SPD solve failed even with jitter")
-    return dict(A_Q=A_Q[..., :rank], A_K=A_K[..., :rank], B_Q=B_Q[:, :rank, :d], B_K=B_K[:, :rank, :d],
+    return dict(A_Q=A_Q[..., :rank] if want_a_q else None, A_K=A_K[..., :rank], B_Q=B_Q[:, :rank, :d], B_K=B_K[:, :rank, :d],
                 A_K_padded=A_K, B_Q_padded=B_Q, B_K_padded=B_K, objective=obj, sweeps=sweeps,
                 converged=conv)
 

@@ -107,3 +107,22 @@ def test_prefill_tensor_core_pass_matches_fp32_path(r):
         assert err < 2e-3, (name, float(err))
     np.testing.assert_allclose(b["objective"].cpu().numpy(), a["objective"].cpu().numpy(), rtol=2e-3)
     assert torch.equal(a["sweeps"], b["sweeps"])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_prefill_without_query_factor(dtype):
+    """want_a_q=False (the decode engine's load path) skips only the query
+    factor's materialisation: A_K, B_Q, B_K, the objective trajectory and the
+    sweep counts are bit-identical to the full call."""
+    from paper_2510_23649_b200.engine import prefill_factorize_device
+
+    rng = np.random.default_rng(11)
+    H, G, l, d, r = 8, 4, 3000, 128, 32
+    Q = torch.as_tensor(rng.standard_normal((H, l, d)), dtype=torch.float32).cuda()
+    K = torch.as_tensor(rng.standard_normal((H // G, l, d)), dtype=torch.float32).cuda()
+    full = prefill_factorize_device(Q, K, r, want_objective=True, dtype=dtype, group=G)
+    lean = prefill_factorize_device(Q, K, r, want_objective=True, dtype=dtype, group=G, want_a_q=False)
+    torch.cuda.synchronize()
+    assert lean["A_Q"] is None and full["A_Q"] is not None
+    for name in ("A_K", "B_Q", "B_K", "objective", "sweeps", "converged"):
+        assert torch.equal(full[name], lean[name]), name
