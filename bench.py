@@ -443,9 +443,11 @@ def run_ours(args, world, rank, local):
                          [int(x) for x in mstat]))
 
     # ---- end to end: host inputs in, host outputs out, per step ------------
-    q_host = q_pool[:4].cpu().pin_memory()
-    k_host = k_pool[:4].cpu().pin_memory()
-    v_host = v_pool[:4].cpu().pin_memory()
+    # the same input sequence as the timed loop (the whole pool, continuing at
+    # step_i), so the selections -- and the host tier's misses -- match it
+    q_host = q_pool.cpu().pin_memory()
+    k_host = k_pool.cpu().pin_memory()
+    v_host = v_pool.cpu().pin_memory()
     out_host = torch.empty(L, B, Hq, shape.dim_stride, dtype=torch.float32).pin_memory()
     h2d = (q_host[0].numel() + k_host[0].numel() + v_host[0].numel()) * q_host.element_size()
     d2h = out_host.numel() * 4
@@ -456,7 +458,7 @@ def run_ours(args, world, rank, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(e2e_steps):
-        j = i % 4
+        j = (step_i + i) % pool
         eng.q_buf[..., :d].copy_(q_host[j], non_blocking=True)
         eng.k_buf[..., :d].copy_(k_host[j], non_blocking=True)
         eng.v_buf[..., :d].copy_(v_host[j], non_blocking=True)
