@@ -6,7 +6,7 @@
 //   (c) TMA tile::gather4 (cp.async.bulk.tensor.2d ... tile::gather4: four
 //       rows of a 2-D tensor map per instruction),
 // each with L2 flushed between launches.  Checks that (c) lands the right
-// rows.  Usage: gather4_bench
+// rows.  Usage: gather4_bench [rows per head] [1: consecutive rows]
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -62,6 +62,48 @@ __global__ void __launch_bounds__(kThr) plain_kernel(const T *K, const T *V, int
     const uint4 *kb = reinterpret_cast<const uint4 *>(K + (size_t)g * t_max * 128);
     const uint4 *vb = reinterpret_cast<const uint4 *>(V + (size_t)g * t_max * 128);
     const int *rows = rows_all + blk * cap;
+    const int step = (blockDim.x >> 5) * 2;
+    uint32_t acc = 0;
+    for (int b0 = warp * 2 + sub; b0 < n; b0 += step * U) {
+        uint4 x[U], y[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = b0 + u * step;
+            const int r = j < n ? __ldg(rows + j) : 0;
+            x[u] = kb[(size_t)r * 16 + sl];
+            y[u] = vb[(size_t)r * 16 + sl];
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += x[u].x ^ y[u].y ^ x[u].z ^ y[u].w;
+    }
+    if (acc == 0x12345u) sink[blk] = acc;
+}
+
+// (a') plain loads after an L2 prefetch of every row of the block: PF 1 =
+// prefetch.global.L2 per 128-byte line, PF 2 = cp.async.bulk.prefetch.L2 per row
+template <int U, int PF>
+__global__ void __launch_bounds__(kThr) plain_pf_kernel(const T *K, const T *V, int t_max, const int *rows_all,
+                                                        const int *nrows, int cap, unsigned *sink) {
+    const int blk = blockIdx.x, g = blk / 9 / 4;
+    const int n = nrows[blk];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane >> 4, sl = lane & 15;
+    const T *kr = K + (size_t)g * t_max * 128, *vr = V + (size_t)g * t_max * 128;
+    const int *rows = rows_all + blk * cap;
+    if (PF == 1) {
+        for (int e = threadIdx.x; e < n * 4; e += blockDim.x) {
+            const int j = e >> 2, part = e & 3;
+            const T *base = (part & 2) ? vr : kr;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (size_t)rows[j] * 128 + (part & 1) * 64));
+        }
+    } else if (PF == 2) {
+        for (int e = threadIdx.x; e < n * 2; e += blockDim.x) {
+            const int j = e >> 1;
+            const T *base = (e & 1) ? vr : kr;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 256;" ::"l"(base + (size_t)rows[j] * 128) : "memory");
+        }
+    }
+    const uint4 *kb = reinterpret_cast<const uint4 *>(kr);
+    const uint4 *vb = reinterpret_cast<const uint4 *>(vr);
     const int step = (blockDim.x >> 5) * 2;
     uint32_t acc = 0;
     for (int b0 = warp * 2 + sub; b0 < n; b0 += step * U) {
@@ -161,9 +203,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
 }
 
-int main() {
-    const int T_ = 131072 + 64, Hq = 32, P = 9, S = 2064, Hkv = 8;
-    const int nblk = Hq * P, cap = 1024;
+int main(int argc, char **argv) {
+    // argv[1]: rows per head (default 2064 = C4's S); argv[2]: 1 = consecutive rows
+    const int T_ = 131072 + 64, Hq = 32, P = 9, Hkv = 8;
+    const int S = argc > 1 ? atoi(argv[1]) : 2064;
+    const bool consecutive = argc > 2 && atoi(argv[2]) == 1;
+    const int nblk = Hq * P, cap = std::max(1024, 2 * S / P + 64);
     const long long nrows_all = (long long)Hkv * T_;
     T *K, *V;
     cudaMalloc(&K, nrows_all * 256);
@@ -178,6 +223,10 @@ int main() {
     for (int h = 0; h < Hq; ++h) {
         std::vector<int> pick;
         std::uniform_int_distribution<int> U(0, 131071);
+        if (consecutive) {
+            const int start = U(rng) % (131072 - S);
+            for (int i = 0; i < S; ++i) pick.push_back(start + i);
+        }
         while ((int)pick.size() < S) pick.push_back(U(rng));
         std::sort(pick.begin(), pick.end());
         pick.erase(std::unique(pick.begin(), pick.end()), pick.end());
@@ -237,6 +286,10 @@ int main() {
                hb, cudaGetErrorString(cudaGetLastError()));
     };
     time("plain loads U=8", [&] { plain_kernel<8><<<nblk, kThr>>>(K, V, T_, drows, dnr, cap, sink); });
+    time("plain loads U=2", [&] { plain_kernel<2><<<nblk, kThr>>>(K, V, T_, drows, dnr, cap, sink); });
+    time("L2 prefetch (lines) + loads U=8", [&] { plain_pf_kernel<8, 1><<<nblk, kThr>>>(K, V, T_, drows, dnr, cap, sink); });
+    time("L2 prefetch (bulk rows) + loads U=8", [&] { plain_pf_kernel<8, 2><<<nblk, kThr>>>(K, V, T_, drows, dnr, cap, sink); });
+    time("L2 prefetch (lines) + loads U=2", [&] { plain_pf_kernel<2, 1><<<nblk, kThr>>>(K, V, T_, drows, dnr, cap, sink); });
 #define TMA_RUN(CR, NS, G4, NAME)                                                                          \
     {                                                                                                      \
         auto kf = tma_kernel<CR, NS, G4>;                                                                  \
